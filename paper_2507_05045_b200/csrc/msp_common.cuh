@@ -1,0 +1,116 @@
+// msp_common.cuh -- shared device types and helpers for the B200 market-split solver.
+//
+// Data layout in HBM:
+//   quarter table t in {A,B,C,D}: sorted row-0 weights (u64), subset masks (u32) and the
+//   companion rows 1..m-1 packed two u16 per u32 word ("P16"), SW words per entry (AoS, 16 B at
+//   m <= 9) so one LDG.128 brings a whole companion vector.
+//   Dense per-weight run arrays (start, end) index every equal-weight run of a table.
+// The enumeration space of one alpha-batch is a union of rectangles X-run(alpha - w) x Y-run(w)
+// (SURVEY.md §0 restatement); a warp tile covers 32 entries of the longer run x TQ of the other.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace msp {
+
+constexpr int kTQ = 32;            // loop entries per warp tile
+constexpr int kMaxMC = 15;         // companion coordinates supported by P16 (m <= 16)
+constexpr uint64_t kFnvOffset = 0xCBF29CE484222325ull;  // validate.py:34, fastval.py:42
+constexpr uint64_t kFnvPrime = 0x100000001B3ull;         // validate.py:35, fastval.py:43
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kHitFlag = 1ull << 63;
+
+// Host-side FNV fold step (validate.py:40-42) -- also used for the per-batch constant h0.
+__host__ __device__ inline uint64_t fnv_step64(uint64_t h, uint64_t v) { return (h ^ v) * kFnvPrime; }
+
+// One FNV-1a-style fold step on a 64-bit state held as two u32 halves, for a coordinate value
+// v < 2^32:  (h ^ v) * (2^40 + 435)  mod 2^64.  Four integer ops: LOP3, IMAD.WIDE.U32, IMAD, LEA.
+__device__ __forceinline__ void fnv_step(uint32_t &lo, uint32_t &hi, uint32_t v) {
+  const uint32_t x = lo ^ v;
+  const uint64_t p = (uint64_t)x * 435u;
+  hi = hi * 435u + (uint32_t)(p >> 32) + (x << 8);
+  lo = (uint32_t)p;
+}
+
+struct TableDev {
+  const uint64_t *w;         // row-0 weights in table order
+  const uint32_t *mask;      // subset masks (bit t <-> column start+t)
+  const uint32_t *comp;      // packed companions, sw words per entry
+  const uint32_t *run_start; // dense over [0, S]
+  const uint32_t *run_end;   // dense over [0, S]; run empty iff end == start
+  uint32_t S;                // largest row-0 weight (block row-0 sum)
+  uint32_t size;
+};
+
+struct YRuns {               // distinct weights of a Y table (B for left, D for right)
+  const uint32_t *w;
+  const uint32_t *start;
+  const uint32_t *len;
+  uint32_t n;
+};
+
+// One (batch, side[, pass]) unit of a launch.
+struct UnitDesc {
+  uint64_t tile_base;        // first launch tile of the unit
+  uint64_t h0;               // FNV state after coordinate 0 (= alpha on both sides)
+  uint32_t xw_total;         // alpha (left) / beta (right): X weight = xw_total - Y weight
+  uint32_t side;             // 0 left (A x B), 1 right (C x D)
+  uint32_t prefix_off;       // offset of the unit's Y-run tile prefix (nY + 1 u32)
+  uint32_t gid;              // batch index within the solve
+  uint32_t slot;             // wave-local batch slot (counters, zero-key counts)
+  uint32_t region_base;      // join table / hit-set region (slots)
+  uint32_t region_log2;      // log2 capacity of the region
+  uint32_t pass, npass;      // hash-range pass filter (npass == 1: all keys)
+  uint32_t count_filter;     // count overshooting right pairs in this unit
+  uint32_t flags;            // bit0: hit set contains key 0
+  uint32_t pad;
+};
+
+struct EnumArgs {
+  TableDev tab[4];
+  YRuns yr[2];               // [0] = B runs, [1] = D runs
+  const uint32_t *prefix;    // tile prefixes of all (batch, side)
+  const UnitDesc *units;
+  uint32_t nunits;
+  uint64_t total_tiles;
+  uint64_t chunk_tiles;      // tiles per warp work item
+  uint64_t nchunks;
+  uint32_t dpack[8];         // d rows 1..m-1 packed, +0x8000 guard per half (right side)
+  unsigned long long *unit_filtered;  // per unit
+  unsigned long long *unit_hits;      // per unit
+};
+
+__device__ __forceinline__ uint32_t pass_of(uint64_t key, uint32_t npass) {
+  return (uint32_t)(((key >> 32) * (uint64_t)npass) >> 32);
+}
+
+__device__ __forceinline__ uint32_t home_slot(uint64_t key, uint32_t log2cap) {
+  return (uint32_t)((key * kGolden) >> (64 - log2cap));
+}
+
+template <int SW>
+__device__ __forceinline__ void load_vec(const uint32_t *__restrict__ base, uint32_t idx, uint32_t (&v)[SW]) {
+  const uint32_t *p = base + (size_t)idx * SW;
+  if constexpr (SW == 1) {
+    v[0] = __ldg(p);
+  } else if constexpr (SW == 2) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2 *>(p));
+    v[0] = t.x; v[1] = t.y;
+  } else {
+#pragma unroll
+    for (int k = 0; k < SW; k += 4) {
+      const uint4 t = __ldg(reinterpret_cast<const uint4 *>(p + k));
+      v[k] = t.x; v[k + 1] = t.y; v[k + 2] = t.z; v[k + 3] = t.w;
+    }
+  }
+}
+
+__host__ __device__ constexpr int words_for(int mc) { return (mc + 1) / 2; }
+__host__ __device__ constexpr int stride_for(int mc) {
+  return words_for(mc) <= 1 ? 1 : words_for(mc) <= 2 ? 2 : words_for(mc) <= 4 ? 4 : 8;
+}
+
+struct HitRec { uint32_t gid, pad; uint64_t key; };
+struct PairRec { uint32_t gid, side, xidx, yidx, xmask, ymask; uint64_t key; };
+
+}  // namespace msp

@@ -1,0 +1,83 @@
+// msp_kernels.h -- host-visible argument structs and launch wrappers of the solver kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "msp_common.cuh"
+
+namespace msp {
+
+struct MergeStep {
+  const uint64_t *sw; const uint32_t *sm;  // sorted list of n entries
+  uint64_t *dw; uint32_t *dm;              // merged list of 2n entries
+  uint32_t n;                              // 0: table already complete
+  uint64_t a;                              // row-0 coefficient of the new column
+  uint32_t bit;                            // mask bit of the new column
+  int asc;
+};
+struct MergeArgs { MergeStep s[4]; };
+
+struct PackTable { const uint32_t *mask; uint32_t *comp; uint32_t size; int start, b; };
+struct PackArgs { PackTable t[4]; const uint64_t *a; int m, n, sw; };
+
+struct RunTable { const uint64_t *w; uint32_t *run_start, *run_end; uint32_t size; };
+struct RunArgs { RunTable t[4]; };
+
+struct YRunTable {
+  const uint32_t *run_start, *run_end; uint32_t S;
+  uint32_t *out_w, *out_start, *out_len, *out_n;
+};
+struct YRunArgs { YRunTable t[2]; };
+
+struct ConvSide {
+  const uint32_t *x_start, *x_end; uint32_t SX;  // X table dense runs (A or C)
+  const uint32_t *yw, *ylen; const uint32_t *ny; // Y runs (B or D)
+  uint32_t vmax; unsigned long long *out;
+};
+struct ConvArgs { ConvSide s[2]; };
+
+struct GroupArgs {
+  const unsigned long long *hl, *hr; uint64_t amax, bmax, target, alpha_lo, alpha_hi;
+  uint64_t *alpha; unsigned long long *nl, *nr; uint32_t *count; uint32_t max_groups;
+};
+
+struct PrefixSide {
+  const uint32_t *x_start, *x_end; uint32_t SX;
+  const uint32_t *yw, *ylen; const uint32_t *ny;
+  size_t off, stride;
+};
+struct PrefixArgs {
+  PrefixSide s[2]; const uint64_t *alpha; uint64_t target; const uint32_t *count;
+  uint32_t *prefix; unsigned long long *tiles; int *err;
+};
+
+struct BruteArgs {
+  const uint64_t *a, *d; int m, n;
+  unsigned long long *count; uint64_t *out; uint64_t cap;
+};
+
+// Global-hash-table join sinks (build / probe / recover), see msp_enum.cu.
+struct JoinTable {
+  unsigned long long *keys;    // 0 = empty
+  unsigned long long *cnt;     // (count - 1) | kHitFlag
+  unsigned long long *zero;    // per wave slot: count of key 0
+  unsigned int *zero_hit;      // per wave slot
+  HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;
+  PairRec *recs; unsigned long long *nrecs; uint64_t rec_cap;
+  int *err;
+};
+
+void launch_merge_step(const MergeArgs &a, uint32_t max_n, cudaStream_t st);
+void launch_pack(const PackArgs &a, uint32_t max_size, cudaStream_t st);
+void launch_runs(const RunArgs &a, uint32_t max_size, cudaStream_t st);
+void launch_yruns(const YRunArgs &a, cudaStream_t st);
+void launch_conv(const ConvArgs &a, uint32_t vmax, cudaStream_t st);
+void launch_groups(const GroupArgs &a, cudaStream_t st);
+void launch_tile_prefix(const PrefixArgs &a, uint32_t max_groups, cudaStream_t st);
+void launch_brute(const BruteArgs &a, cudaStream_t st);
+
+enum SinkKind { SINK_BUILD = 0, SINK_PROBE = 1, SINK_RECOVER = 2 };
+// Enumerate every pair of the launch's units, hash it, and hand the key to the sink.
+int launch_enum(int mc, SinkKind kind, const EnumArgs &args, const JoinTable &jt, int num_sms,
+                cudaStream_t st);
+
+}  // namespace msp

@@ -1,0 +1,874 @@
+// msp_solve.cu -- host orchestration and the C-ABI of libmsp_b200.so.
+//
+// One msp_solve call = the reference's table path (solver.py:213-245) on one GPU:
+//   K1 quarter tables -> K2 plan (runs, convolution, batch list, tile prefixes) -> one host sync
+//   -> join waves (build / probe launches over the global hash table) -> hit recovery -> exact
+//   confirmation on the host (validate.py:285-313) -> solution bit vectors.
+// All arithmetic on the hot path runs in the kernels of msp_tables.cu / msp_enum.cu; the host only
+// plans waves and confirms the (rare) full-hash hits exactly, as the reference does on its CPU.
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "msp_b200.h"
+#include "msp_common.cuh"
+#include "msp_kernels.h"
+
+namespace msp {
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+#define CK(x)                                                                 \
+  do {                                                                        \
+    cudaError_t e_ = (x);                                                     \
+    if (e_ != cudaSuccess) {                                                  \
+      set_err("%s failed: %s", #x, cudaGetErrorString(e_));                   \
+      return MSP_CUDA_ERROR;                                                  \
+    }                                                                         \
+  } while (0)
+
+struct DBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t c = std::max<size_t>(bytes + bytes / 4, 256);
+    cudaError_t e = cudaMalloc(&p, c);
+    if (e == cudaSuccess) cap = c;
+    return e;
+  }
+  template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+};
+
+struct Device {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::mutex mu;
+  DBuf a, d;
+  DBuf tw[4], tm[4], tw2[4], tm2[4], comp[4], rs[4], re[4];
+  DBuf yw[2], ys[2], yl[2], yn;
+  DBuf hl, hr, galpha, gnl, gnr, gcount, prefix, tiles, err;
+  DBuf units, ufilt, uhits;
+  DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
+  DBuf bout, bcnt;
+  DBuf rkeys, runits, rfilt, rhits;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t pev[2] = {nullptr, nullptr};
+  void release_all() {
+    DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &prefix, &tiles, &err,
+                   &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
+                   &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits};
+    for (DBuf *b : all) b->release();
+    for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
+                                  comp[i].release(); rs[i].release(); re[i].release(); }
+    for (int i = 0; i < 2; ++i) { yw[i].release(); ys[i].release(); yl[i].release(); }
+  }
+};
+
+std::mutex g_devices_mu;
+std::map<int, Device *> g_devices;
+
+int get_device(int dev, Device **out) {
+  std::lock_guard<std::mutex> lk(g_devices_mu);
+  auto it = g_devices.find(dev);
+  if (it != g_devices.end()) { *out = it->second; return MSP_OK; }
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (dev < 0 || dev >= ndev) { set_err("device %d out of range (%d devices)", dev, ndev); return MSP_INVALID_ARGUMENT; }
+  CK(cudaSetDevice(dev));
+  Device *D = new Device();
+  D->dev = dev;
+  CK(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
+  CK(cudaDeviceGetAttribute(&D->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  for (auto &e : D->ev) CK(cudaEventCreate(&e));
+  for (auto &e : D->pev) CK(cudaEventCreate(&e));
+  g_devices[dev] = D;
+  *out = D;
+  return MSP_OK;
+}
+
+void block_sizes(int n, int out[4]) {  // enumerate1d.py:81-83
+  const int q = n / 4, r = n % 4;
+  for (int i = 0; i < 4; ++i) out[i] = i < r ? q + 1 : q;
+}
+
+uint32_t pow2ceil(uint64_t v) {
+  uint32_t l = 0;
+  while ((1ull << l) < v) ++l;
+  return l;
+}
+
+// Everything msp_solve needs after K1 + K2.
+struct Plan {
+  int m = 0, n = 0, mc = 0, sw = 1;
+  int b[4] = {0, 0, 0, 0}, start[4] = {0, 0, 0, 0};
+  uint32_t S[4] = {0, 0, 0, 0};
+  uint64_t target = 0;
+  uint32_t ny[2] = {0, 0};
+  uint32_t G = 0;
+  std::vector<uint64_t> alpha, nl, nr, tiles;  // tiles[2g + side]
+  size_t stride[2] = {0, 0}, off[2] = {0, 0};
+  EnumArgs base{};
+  int merge_w_cur[4] = {0, 0, 0, 0};  // which ping-pong buffer holds the final table
+};
+
+const uint64_t *table_w(Device &D, const Plan &P, int t) {
+  return P.merge_w_cur[t] ? D.tw2[t].as<uint64_t>() : D.tw[t].as<uint64_t>();
+}
+const uint32_t *table_m(Device &D, const Plan &P, int t) {
+  return P.merge_w_cur[t] ? D.tm2[t].as<uint32_t>() : D.tm[t].as<uint32_t>();
+}
+
+// Checks the arithmetic mode preconditions (P16 packing, dense row-0 plan).
+int check_instance(const msp_problem *pr, Plan &P) {
+  P.m = pr->m;
+  P.n = pr->n;
+  if (P.m < 1 || P.n < 1 || !pr->a || !pr->d) { set_err("invalid problem"); return MSP_INVALID_ARGUMENT; }
+  if (P.n < 4) { set_err("four-block split needs n >= 4, got n=%d", P.n); return MSP_INVALID_ARGUMENT; }
+  block_sizes(P.n, P.b);
+  for (int t = 0, s = 0; t < 4; ++t) { P.start[t] = s; s += P.b[t]; }
+  if (P.b[0] > 24) { set_err("block size %d > 24 unsupported", P.b[0]); return MSP_UNSUPPORTED; }
+  P.mc = P.m - 1;
+  if (P.mc > kMaxMC) { set_err("m=%d > %d rows unsupported by the packed-16 path", P.m, kMaxMC + 1); return MSP_UNSUPPORTED; }
+  P.sw = stride_for(P.mc);
+  for (int t = 0; t < 4; ++t) {
+    unsigned __int128 s0 = 0;
+    for (int j = 0; j < P.b[t]; ++j) s0 += pr->a[P.start[t] + j];
+    if (s0 > (1u << 24)) { set_err("row-0 block sum exceeds the dense alpha plan (2^24)"); return MSP_UNSUPPORTED; }
+    P.S[t] = (uint32_t)s0;
+    for (int r = 1; r < P.m; ++r) {
+      unsigned __int128 s = 0;
+      for (int j = 0; j < P.b[t]; ++j) s += pr->a[(size_t)r * P.n + P.start[t] + j];
+      if (s > 16384) { set_err("row %d block sum exceeds the packed-16 companion range", r + 1); return MSP_UNSUPPORTED; }
+    }
+  }
+  for (int r = 1; r < P.m; ++r)
+    if (pr->d[r] > 32767) { set_err("d[%d] exceeds the packed-16 residual range", r); return MSP_UNSUPPORTED; }
+  P.target = pr->d[0];
+  return MSP_OK;
+}
+
+// K1 + K2 on the device; ends with the batch list and tile totals on the host.
+int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uint64_t alpha_hi,
+               cudaStream_t st, int64_t &launches) {
+  const int m = P.m, n = P.n;
+  CK(D.a.ensure(sizeof(uint64_t) * m * n));
+  CK(D.d.ensure(sizeof(uint64_t) * m));
+  CK(cudaMemcpyAsync(D.a.p, pr->a, sizeof(uint64_t) * m * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(D.d.p, pr->d, sizeof(uint64_t) * m, cudaMemcpyHostToDevice, st));
+  uint32_t maxsize = 0;
+  for (int t = 0; t < 4; ++t) {
+    const size_t sz = (size_t)1 << P.b[t];
+    maxsize = std::max<uint32_t>(maxsize, (uint32_t)sz);
+    CK(D.tw[t].ensure(8 * sz)); CK(D.tw2[t].ensure(8 * sz));
+    CK(D.tm[t].ensure(4 * sz)); CK(D.tm2[t].ensure(4 * sz));
+    CK(D.comp[t].ensure(4 * sz * P.sw));
+    CK(D.rs[t].ensure(4 * ((size_t)P.S[t] + 1))); CK(D.re[t].ensure(4 * ((size_t)P.S[t] + 1)));
+    CK(cudaMemsetAsync(D.tw[t].p, 0, 8, st));  // the empty subset: weight 0, mask 0
+    CK(cudaMemsetAsync(D.tm[t].p, 0, 4, st));
+    P.merge_w_cur[t] = 0;
+  }
+  // ---- K1: merge-doubling, one launch per column step over all four tables
+  const int bmax = *std::max_element(P.b, P.b + 4);
+  for (int step = 0; step < bmax; ++step) {
+    MergeArgs ma{};
+    uint32_t mx = 0;
+    for (int t = 0; t < 4; ++t) {
+      MergeStep &s = ma.s[t];
+      if (step >= P.b[t]) { s.n = 0; continue; }
+      const int cur = P.merge_w_cur[t];
+      s.sw = cur ? D.tw2[t].as<uint64_t>() : D.tw[t].as<uint64_t>();
+      s.sm = cur ? D.tm2[t].as<uint32_t>() : D.tm[t].as<uint32_t>();
+      s.dw = cur ? D.tw[t].as<uint64_t>() : D.tw2[t].as<uint64_t>();
+      s.dm = cur ? D.tm[t].as<uint32_t>() : D.tm2[t].as<uint32_t>();
+      s.n = 1u << step;
+      s.a = pr->a[P.start[t] + step];
+      s.bit = step;
+      s.asc = t < 2;
+      mx = std::max(mx, s.n);
+      P.merge_w_cur[t] ^= 1;
+    }
+    launch_merge_step(ma, mx, st);
+    ++launches;
+  }
+  PackArgs pa{};
+  RunArgs ra{};
+  for (int t = 0; t < 4; ++t) {
+    pa.t[t] = PackTable{table_m(D, P, t), D.comp[t].as<uint32_t>(), 1u << P.b[t], P.start[t], P.b[t]};
+    ra.t[t] = RunTable{table_w(D, P, t), D.rs[t].as<uint32_t>(), D.re[t].as<uint32_t>(), 1u << P.b[t]};
+    CK(cudaMemsetAsync(D.rs[t].p, 0, 4 * ((size_t)P.S[t] + 1), st));
+    CK(cudaMemsetAsync(D.re[t].p, 0, 4 * ((size_t)P.S[t] + 1), st));
+  }
+  pa.a = D.a.as<uint64_t>(); pa.m = m; pa.n = n; pa.sw = P.sw;
+  launch_pack(pa, maxsize, st);
+  launch_runs(ra, maxsize, st);
+  launches += 2;
+  // ---- K2: Y-run lists, convolution, batch list
+  CK(D.yn.ensure(8));
+  YRunArgs ya{};
+  for (int s = 0; s < 2; ++s) {
+    const int t = s ? 3 : 1;
+    const size_t cap = (size_t)P.S[t] + 1;
+    CK(D.yw[s].ensure(4 * cap)); CK(D.ys[s].ensure(4 * cap)); CK(D.yl[s].ensure(4 * cap));
+    ya.t[s] = YRunTable{D.rs[t].as<uint32_t>(), D.re[t].as<uint32_t>(), P.S[t], D.yw[s].as<uint32_t>(),
+                        D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), D.yn.as<uint32_t>() + s};
+  }
+  launch_yruns(ya, st);
+  const uint64_t vmaxL = (uint64_t)P.S[0] + P.S[1], vmaxR = (uint64_t)P.S[2] + P.S[3];
+  CK(D.hl.ensure(8 * (vmaxL + 1)));
+  CK(D.hr.ensure(8 * (vmaxR + 1)));
+  ConvArgs ca{};
+  ca.s[0] = ConvSide{D.rs[0].as<uint32_t>(), D.re[0].as<uint32_t>(), P.S[0], D.yw[0].as<uint32_t>(),
+                     D.yl[0].as<uint32_t>(), D.yn.as<uint32_t>(), (uint32_t)vmaxL, D.hl.as<unsigned long long>()};
+  ca.s[1] = ConvSide{D.rs[2].as<uint32_t>(), D.re[2].as<uint32_t>(), P.S[2], D.yw[1].as<uint32_t>(),
+                     D.yl[1].as<uint32_t>(), D.yn.as<uint32_t>() + 1, (uint32_t)vmaxR, D.hr.as<unsigned long long>()};
+  launch_conv(ca, (uint32_t)std::max(vmaxL, vmaxR), st);
+  const uint32_t maxG = (uint32_t)(vmaxL + 1);
+  CK(D.galpha.ensure(8 * maxG)); CK(D.gnl.ensure(8 * maxG)); CK(D.gnr.ensure(8 * maxG));
+  CK(D.gcount.ensure(8));
+  GroupArgs ga{D.hl.as<unsigned long long>(), D.hr.as<unsigned long long>(), vmaxL, vmaxR, P.target,
+               alpha_lo, alpha_hi ? alpha_hi : ~0ull, D.galpha.as<uint64_t>(),
+               D.gnl.as<unsigned long long>(), D.gnr.as<unsigned long long>(), D.gcount.as<uint32_t>(), maxG};
+  launch_groups(ga, st);
+  launches += 3;
+  uint32_t hdr[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(hdr, D.gcount.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hdr + 2, D.yn.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  P.G = hdr[0];
+  P.ny[0] = hdr[2];
+  P.ny[1] = hdr[3];
+  P.alpha.resize(P.G); P.nl.resize(P.G); P.nr.resize(P.G); P.tiles.assign(2 * (size_t)P.G, 0);
+  if (P.G == 0) return MSP_OK;
+  // ---- tile prefixes per (batch, side)
+  P.stride[0] = P.ny[0] + 1;
+  P.stride[1] = P.ny[1] + 1;
+  P.off[0] = 0;
+  P.off[1] = (size_t)P.G * P.stride[0];
+  const size_t npre = P.off[1] + (size_t)P.G * P.stride[1];
+  if (npre > 0xFFFFFFFFull) { set_err("tile prefix table too large"); return MSP_UNSUPPORTED; }
+  CK(D.prefix.ensure(4 * npre));
+  CK(D.tiles.ensure(16 * (size_t)P.G));
+  CK(D.err.ensure(16));
+  CK(cudaMemsetAsync(D.err.p, 0, 16, st));
+  PrefixArgs pp{};
+  for (int s = 0; s < 2; ++s) {
+    const int X = s ? 2 : 0;
+    pp.s[s] = PrefixSide{D.rs[X].as<uint32_t>(), D.re[X].as<uint32_t>(), P.S[X], D.yw[s].as<uint32_t>(),
+                         D.yl[s].as<uint32_t>(), D.yn.as<uint32_t>() + s, P.off[s], P.stride[s]};
+  }
+  pp.alpha = D.galpha.as<uint64_t>();
+  pp.target = P.target;
+  pp.count = D.gcount.as<uint32_t>();
+  pp.prefix = D.prefix.as<uint32_t>();
+  pp.tiles = D.tiles.as<unsigned long long>();
+  pp.err = D.err.as<int>();
+  launch_tile_prefix(pp, P.G, st);
+  ++launches;
+  int err = 0;
+  CK(cudaMemcpyAsync(P.alpha.data(), D.galpha.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(P.nl.data(), D.gnl.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(P.nr.data(), D.gnr.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(P.tiles.data(), D.tiles.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (err) { set_err("tile count of one batch side exceeds 2^32"); return MSP_UNSUPPORTED; }
+  // ---- launch-invariant enumeration arguments
+  EnumArgs &A = P.base;
+  for (int t = 0; t < 4; ++t)
+    A.tab[t] = TableDev{table_w(D, P, t), table_m(D, P, t), D.comp[t].as<uint32_t>(), D.rs[t].as<uint32_t>(),
+                        D.re[t].as<uint32_t>(), P.S[t], 1u << P.b[t]};
+  for (int s = 0; s < 2; ++s)
+    A.yr[s] = YRuns{D.yw[s].as<uint32_t>(), D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), P.ny[s]};
+  A.prefix = D.prefix.as<uint32_t>();
+  for (int k = 0; k < 8; ++k) {
+    const int c0 = 2 * k + 1, c1 = 2 * k + 2;  // rows c0, c1 (1-based companion rows)
+    const uint32_t lo = (c0 < m ? (uint32_t)pr->d[c0] : 0u) + 0x8000u;
+    const uint32_t hi = (c1 < m ? (uint32_t)pr->d[c1] : 0u) + 0x8000u;
+    A.dpack[k] = lo | (hi << 16);
+  }
+  return MSP_OK;
+}
+
+struct Wave {
+  size_t ub0 = 0, ub1 = 0;   // build units [ub0, ub1) in the global unit array
+  size_t up0 = 0, up1 = 0;   // probe units
+  uint64_t slots = 0;        // table slots used
+  uint32_t nslot = 0;        // batches (zero-key slots)
+  uint64_t build_tiles = 0, probe_tiles = 0;
+  uint64_t pairs = 0;        // candidate pairs enumerated by the wave
+};
+
+UnitDesc make_unit(const Plan &P, uint32_t g, int side, uint64_t tile_base) {
+  UnitDesc u{};
+  u.tile_base = tile_base;
+  u.h0 = fnv_step64(kFnvOffset, P.alpha[g]);
+  u.xw_total = (uint32_t)(side == 0 ? P.alpha[g] : P.target - P.alpha[g]);
+  u.side = side;
+  u.prefix_off = (uint32_t)(P.off[side] + (size_t)g * P.stride[side]);
+  u.gid = g;
+  u.npass = 1;
+  return u;
+}
+
+void set_enum_range(EnumArgs &A, const UnitDesc *units_dev, size_t nunits, uint64_t total_tiles,
+                    int num_sms) {
+  A.units = units_dev;
+  A.nunits = (uint32_t)nunits;
+  A.total_tiles = total_tiles;
+  const uint64_t warps = (uint64_t)num_sms * 64;
+  uint64_t ct = total_tiles / (warps * 4);
+  ct = std::max<uint64_t>(1, std::min<uint64_t>(ct, 64));
+  A.chunk_tiles = ct;
+  A.nchunks = (total_tiles + ct - 1) / ct;
+}
+
+struct Residual { std::vector<unsigned __int128> v; };
+
+// Exact confirmation of full-hash hits (validate.py:285-313 + assemble_solution enumerate1d.py:313-327).
+int confirm(const msp_problem *pr, const Plan &P, const std::vector<PairRec> &recs,
+            std::vector<std::vector<uint8_t>> &sols, int64_t &host_hash_hits) {
+  const int m = P.m, n = P.n;
+  auto block_sum = [&](int t, uint32_t mask, int row) {
+    unsigned __int128 s = 0;
+    for (int b = 0; b < P.b[t]; ++b)
+      if ((mask >> b) & 1u) s += pr->a[(size_t)row * n + P.start[t] + b];
+    return s;
+  };
+  struct Key { uint32_t gid; uint64_t key; bool operator<(const Key &o) const { return gid != o.gid ? gid < o.gid : key < o.key; } };
+  std::map<Key, std::pair<std::vector<const PairRec *>, std::vector<const PairRec *>>> by;
+  for (const PairRec &r : recs) {
+    auto &e = by[Key{r.gid, r.key}];
+    (r.side ? e.second : e.first).push_back(&r);
+  }
+  host_hash_hits = 0;
+  for (auto &kv : by) {
+    auto &L = kv.second.first;
+    auto &R = kv.second.second;
+    host_hash_hits += (int64_t)L.size() * (int64_t)R.size();
+    if (L.empty() || R.empty()) continue;
+    std::map<std::vector<unsigned __int128>, std::vector<const PairRec *>> lv;
+    for (const PairRec *l : L) {
+      std::vector<unsigned __int128> v(m);
+      for (int i = 0; i < m; ++i) v[i] = block_sum(0, l->xmask, i) + block_sum(1, l->ymask, i);
+      lv[v].push_back(l);
+    }
+    for (const PairRec *r : R) {
+      std::vector<unsigned __int128> v(m);
+      bool ok = true;
+      for (int i = 0; i < m && ok; ++i) {
+        const unsigned __int128 s = block_sum(2, r->xmask, i) + block_sum(3, r->ymask, i);
+        if (s > pr->d[i]) ok = false; else v[i] = (unsigned __int128)pr->d[i] - s;
+      }
+      if (!ok) return MSP_INTERNAL;  // a filtered pair reached the join
+      auto it = lv.find(v);
+      if (it == lv.end()) continue;  // full-hash collision, not a solution
+      for (const PairRec *l : it->second) {
+        std::vector<uint8_t> x(n, 0);
+        const uint32_t mk[4] = {l->xmask, l->ymask, r->xmask, r->ymask};
+        for (int t = 0; t < 4; ++t)
+          for (int b = 0; b < P.b[t]; ++b) x[P.start[t] + b] = (mk[t] >> b) & 1u;
+        for (int i = 0; i < m; ++i) {  // verify_solution (instances.py:322-336)
+          unsigned __int128 s = 0;
+          for (int j = 0; j < n; ++j) if (x[j]) s += pr->a[(size_t)i * n + j];
+          if (s != pr->d[i]) { set_err("internal error: residual match failed full verification"); return MSP_INTERNAL; }
+        }
+        sols.push_back(std::move(x));
+      }
+    }
+  }
+  return MSP_OK;
+}
+
+int brute_force(Device &D, const msp_problem *pr, cudaStream_t st, std::vector<std::vector<uint8_t>> &sols,
+                int64_t &launches) {
+  const int m = pr->m, n = pr->n;
+  if (n > 28) { set_err("brute force capped at n <= 28, got n=%d", n); return MSP_INVALID_ARGUMENT; }
+  for (int i = 0; i < m; ++i) {
+    unsigned __int128 s = 0;
+    for (int j = 0; j < n; ++j) s += pr->a[(size_t)i * n + j];
+    if (s > ~0ull) { set_err("row sum overflow"); return MSP_INVALID_ARGUMENT; }
+  }
+  uint64_t cap = 1 << 16;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    CK(D.a.ensure(8 * (size_t)m * n)); CK(D.d.ensure(8 * (size_t)m));
+    CK(D.bout.ensure(8 * cap)); CK(D.bcnt.ensure(8));
+    CK(cudaMemcpyAsync(D.a.p, pr->a, 8 * (size_t)m * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(D.d.p, pr->d, 8 * (size_t)m, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(D.bcnt.p, 0, 8, st));
+    BruteArgs ba{D.a.as<uint64_t>(), D.d.as<uint64_t>(), m, n, D.bcnt.as<unsigned long long>(), D.bout.as<uint64_t>(), cap};
+    launch_brute(ba, st);
+    ++launches;
+    CK(cudaGetLastError());
+    unsigned long long cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, D.bcnt.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (cnt > cap) { cap = cnt; continue; }
+    std::vector<uint64_t> enc(cnt);
+    if (cnt) CK(cudaMemcpy(enc.data(), D.bout.p, 8 * cnt, cudaMemcpyDeviceToHost));
+    std::sort(enc.begin(), enc.end());
+    for (uint64_t e : enc) {
+      std::vector<uint8_t> x(n);
+      for (int j = 0; j < n; ++j) x[j] = (e >> (n - 1 - j)) & 1;
+      sols.push_back(std::move(x));
+    }
+    return MSP_OK;
+  }
+  set_err("brute force result buffer overflow");
+  return MSP_INTERNAL;
+}
+
+float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) return 0;
+  return ms;
+}
+
+int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
+  const double t0 = now_s();
+  memset(res, 0, sizeof(*res));
+  if (!pr || !opt || !res) { set_err("null argument"); return MSP_INVALID_ARGUMENT; }
+  res->n = pr->n;
+  Device *Dp = nullptr;
+  int rc = get_device(opt->device, &Dp);
+  if (rc) return rc;
+  Device &D = *Dp;
+  std::lock_guard<std::mutex> lk(D.mu);
+  CK(cudaSetDevice(D.dev));
+  cudaStream_t st = opt->stream ? (cudaStream_t)opt->stream : D.stream;
+  msp_stats &S = res->stats;
+  std::vector<std::vector<uint8_t>> sols;
+  const bool profile = opt->flags & MSP_FLAG_PROFILE;
+  const int bf_max = opt->brute_force_max_n < 0 ? 12 : opt->brute_force_max_n;
+  auto emit = [&](void) -> int {
+    res->n_solutions = (int64_t)sols.size();
+    if (!sols.empty()) {
+      res->xbits = (uint8_t *)malloc(sols.size() * (size_t)pr->n);
+      for (size_t i = 0; i < sols.size(); ++i) memcpy(res->xbits + i * pr->n, sols[i].data(), pr->n);
+    }
+    S.t_total = now_s() - t0;
+    return MSP_OK;
+  };
+  if (!(opt->flags & MSP_FLAG_FORCE_TABLE_PATH) && pr->n <= bf_max) {
+    CK(cudaEventRecord(D.ev[0], st));
+    rc = brute_force(D, pr, st, sols, S.kernel_launches);
+    if (rc) return rc;
+    CK(cudaEventRecord(D.ev[1], st));
+    CK(cudaEventSynchronize(D.ev[1]));
+    S.dev_ms_total = elapsed_ms(D.ev[0], D.ev[1]);
+    if (opt->mode == MSP_MODE_FIRST && sols.size() > 1) sols.resize(1);
+    S.fallback = 1;
+    S.exact_hits = (int64_t)sols.size();
+    return emit();
+  }
+  Plan P;
+  rc = check_instance(pr, P);
+  if (rc) return rc;
+  const double deadline = opt->time_limit_s > 0 ? t0 + opt->time_limit_s : 0;
+  CK(cudaEventRecord(D.ev[0], st));
+  rc = build_plan(D, pr, P, opt->alpha_lo, opt->alpha_hi, st, S.kernel_launches);
+  if (rc) return rc;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(D.ev[1], st));
+  S.t_build = now_s() - t0;
+  S.peak_table_entries = 0;
+  for (int t = 0; t < 4; ++t) S.peak_table_entries += (int64_t)1 << P.b[t];
+  S.peak_heap1 = (int64_t)1 << P.b[1];
+  S.peak_heap2 = (int64_t)1 << P.b[3];
+  S.batches = P.G;
+  unsigned __int128 row1 = 0;
+  for (uint32_t g = 0; g < P.G; ++g) {
+    S.candidates_left += (int64_t)P.nl[g];
+    S.candidates_right += (int64_t)P.nr[g];
+    row1 += (unsigned __int128)P.nl[g] * P.nr[g];
+  }
+  S.row1_pairs_lo = (uint64_t)row1;
+  S.row1_pairs_hi = (uint64_t)(row1 >> 64);
+  if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
+
+  // ---- wave plan (global-table join): build on the smaller side of each batch
+  const uint64_t slot_budget = opt->wave_keys ? std::max<uint64_t>(1024, opt->wave_keys) : (1ull << 22);
+  std::vector<UnitDesc> units;
+  std::vector<Wave> waves;
+  Wave cur;
+  uint64_t tb_build = 0, tb_probe = 0;
+  std::vector<UnitDesc> pend_build, pend_probe;
+  auto flush = [&]() {
+    if (pend_build.empty()) return;
+    cur.ub0 = units.size();
+    units.insert(units.end(), pend_build.begin(), pend_build.end());
+    cur.ub1 = units.size();
+    cur.up0 = units.size();
+    units.insert(units.end(), pend_probe.begin(), pend_probe.end());
+    cur.up1 = units.size();
+    cur.build_tiles = tb_build;
+    cur.probe_tiles = tb_probe;
+    waves.push_back(cur);
+    cur = Wave();
+    pend_build.clear();
+    pend_probe.clear();
+    tb_build = tb_probe = 0;
+  };
+  for (uint32_t g = 0; g < P.G; ++g) {
+    const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
+    const uint64_t nb = bside ? P.nr[g] : P.nl[g];
+    const uint64_t need = 1ull << std::max<uint32_t>(6, pow2ceil(2 * nb));
+    uint32_t npass = 1;
+    uint64_t cap = need;
+    if (need > slot_budget) {
+      npass = (uint32_t)((2 * nb + slot_budget - 1) / slot_budget);
+      do {
+        ++npass;
+        cap = 1ull << std::max<uint32_t>(6, pow2ceil((uint64_t)(2.2 * (double)nb / npass) + 64));
+      } while (cap > slot_budget);
+      flush();
+    }
+    for (uint32_t p = 0; p < npass; ++p) {
+      if (npass == 1 && cur.slots + cap > slot_budget) flush();
+      UnitDesc ub = make_unit(P, g, bside, tb_build);
+      UnitDesc up = make_unit(P, g, 1 - bside, tb_probe);
+      for (UnitDesc *u : {&ub, &up}) {
+        u->slot = cur.nslot;
+        u->region_base = (uint32_t)cur.slots;
+        u->region_log2 = pow2ceil(cap);
+        u->pass = p;
+        u->npass = npass;
+        u->count_filter = (u->side == 1 && p == 0);
+      }
+      tb_build += P.tiles[2 * g + bside];
+      tb_probe += P.tiles[2 * g + 1 - bside];
+      cur.pairs += P.nl[g] + P.nr[g];
+      pend_build.push_back(ub);
+      pend_probe.push_back(up);
+      cur.slots += cap;
+      cur.nslot++;
+      if (npass > 1) flush();
+    }
+  }
+  flush();
+  S.waves = (int32_t)waves.size();
+
+  // ---- join waves
+  const uint64_t hit_cap = 1 << 20;
+  uint32_t max_nslot = 1;
+  uint64_t max_slots = 64;
+  for (const Wave &w : waves) { max_nslot = std::max(max_nslot, w.nslot); max_slots = std::max(max_slots, w.slots); }
+  const size_t nu = std::max<size_t>(1, units.size());
+  CK(D.units.ensure(sizeof(UnitDesc) * nu));
+  CK(D.ufilt.ensure(8 * nu));
+  CK(D.uhits.ensure(8 * nu));
+  CK(D.keys.ensure(8 * max_slots));
+  CK(D.cnt.ensure(8 * max_slots));
+  CK(D.zero.ensure(8 * max_nslot));
+  CK(D.zhit.ensure(4 * max_nslot));
+  CK(D.hits.ensure(sizeof(HitRec) * hit_cap));
+  CK(D.nhits.ensure(8));
+  CK(D.nrecs.ensure(8));
+  if (!units.empty())
+    CK(cudaMemcpyAsync(D.units.p, units.data(), sizeof(UnitDesc) * units.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(D.ufilt.p, 0, 8 * nu, st));
+  CK(cudaMemsetAsync(D.uhits.p, 0, 8 * nu, st));
+  CK(cudaMemsetAsync(D.nhits.p, 0, 8, st));
+  CK(cudaMemsetAsync(D.err.p, 0, 16, st));
+  JoinTable jt{};
+  jt.keys = D.keys.as<unsigned long long>();
+  jt.cnt = D.cnt.as<unsigned long long>();
+  jt.zero = D.zero.as<unsigned long long>();
+  jt.zero_hit = D.zhit.as<unsigned int>();
+  jt.hits = D.hits.as<HitRec>();
+  jt.nhits = D.nhits.as<unsigned long long>();
+  jt.hit_cap = hit_cap;
+  jt.err = D.err.as<int>();
+  const UnitDesc *udev = D.units.as<UnitDesc>();
+  EnumArgs A = P.base;
+  double hot_ms = 0;
+  const double t_join0 = now_s();
+
+  // Recovery of hits [h_from, h_to): re-enumerate those batches, emit the pairs whose key is a hit
+  // key, confirm exactly on the host.  Uses its own buffers so waves can resume afterwards.
+  int64_t recovered_hh = 0;
+  auto recover = [&](uint64_t h_from, uint64_t h_to) -> int {
+    if (h_to <= h_from) return MSP_OK;
+    std::vector<HitRec> hv(h_to - h_from);
+    CK(cudaMemcpy(hv.data(), D.hits.as<HitRec>() + h_from, sizeof(HitRec) * hv.size(), cudaMemcpyDeviceToHost));
+    std::map<uint32_t, std::vector<uint64_t>> byg;
+    for (const HitRec &h : hv) byg[h.gid].push_back(h.key);
+    std::vector<UnitDesc> ru;
+    std::vector<unsigned long long> himg;
+    uint64_t tb = 0, slots = 0;
+    for (auto &kv : byg) {
+      const uint32_t g = kv.first;
+      std::vector<uint64_t> ks = kv.second;
+      std::sort(ks.begin(), ks.end());
+      ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
+      const uint32_t l2 = std::max<uint32_t>(6, pow2ceil(4 * ks.size()));
+      const uint64_t cap = 1ull << l2;
+      himg.resize(slots + cap, 0);
+      bool has_zero = false;
+      for (uint64_t k : ks) {
+        if (k == 0) { has_zero = true; continue; }
+        uint32_t sl = (uint32_t)((k * kGolden) >> (64 - l2));
+        while (himg[slots + sl]) sl = (sl + 1) & (uint32_t)(cap - 1);
+        himg[slots + sl] = k;
+      }
+      for (int side = 0; side < 2; ++side) {
+        UnitDesc u = make_unit(P, g, side, tb);
+        u.region_base = (uint32_t)slots;
+        u.region_log2 = l2;
+        u.flags = has_zero ? 1u : 0u;
+        tb += P.tiles[2 * g + side];
+        ru.push_back(u);
+      }
+      slots += cap;
+    }
+    CK(D.rkeys.ensure(8 * std::max<uint64_t>(slots, 1)));
+    CK(D.runits.ensure(sizeof(UnitDesc) * ru.size()));
+    CK(D.rfilt.ensure(8 * ru.size()));
+    CK(D.rhits.ensure(8 * ru.size()));
+    CK(cudaMemcpyAsync(D.rkeys.p, himg.data(), 8 * slots, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(D.runits.p, ru.data(), sizeof(UnitDesc) * ru.size(), cudaMemcpyHostToDevice, st));
+    JoinTable rj = jt;
+    rj.keys = D.rkeys.as<unsigned long long>();
+    EnumArgs RA = P.base;
+    uint64_t rec_cap = std::max<uint64_t>(4096, 4 * hv.size());
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      CK(D.recs.ensure(sizeof(PairRec) * rec_cap));
+      CK(cudaMemsetAsync(D.nrecs.p, 0, 8, st));
+      rj.recs = D.recs.as<PairRec>();
+      rj.nrecs = D.nrecs.as<unsigned long long>();
+      rj.rec_cap = rec_cap;
+      set_enum_range(RA, D.runits.as<UnitDesc>(), ru.size(), tb, D.num_sms);
+      RA.unit_filtered = D.rfilt.as<unsigned long long>();
+      RA.unit_hits = D.rhits.as<unsigned long long>();
+      launch_enum(P.mc, SINK_RECOVER, RA, rj, D.num_sms, st);
+      ++S.kernel_launches;
+      CK(cudaGetLastError());
+      unsigned long long nr = 0;
+      CK(cudaMemcpyAsync(&nr, D.nrecs.p, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (nr > rec_cap) { rec_cap = nr; continue; }
+      std::vector<PairRec> recs(nr);
+      if (nr) CK(cudaMemcpy(recs.data(), D.recs.p, sizeof(PairRec) * nr, cudaMemcpyDeviceToHost));
+      int64_t hh = 0;
+      const int rc2 = confirm(pr, P, recs, sols, hh);
+      if (rc2) return rc2;
+      recovered_hh += hh;
+      return MSP_OK;
+    }
+    set_err("hit recovery buffer overflow");
+    return MSP_INTERNAL;
+  };
+
+  uint64_t hits_done = 0;
+  bool stopped_early = false;
+  const size_t sync_every = (deadline || opt->mode == MSP_MODE_FIRST) ? 16 : waves.size() + 1;
+  for (size_t wi = 0; wi < waves.size(); ++wi) {
+    const Wave &w = waves[wi];
+    CK(cudaMemsetAsync(D.keys.p, 0, 8 * w.slots, st));
+    CK(cudaMemsetAsync(D.cnt.p, 0, 8 * w.slots, st));
+    CK(cudaMemsetAsync(D.zero.p, 0, 8 * w.nslot, st));
+    CK(cudaMemsetAsync(D.zhit.p, 0, 4 * w.nslot, st));
+    if (profile) CK(cudaEventRecord(D.pev[0], st));
+    set_enum_range(A, udev + w.ub0, w.ub1 - w.ub0, w.build_tiles, D.num_sms);
+    A.unit_filtered = D.ufilt.as<unsigned long long>() + w.ub0;
+    A.unit_hits = D.uhits.as<unsigned long long>() + w.ub0;
+    if (launch_enum(P.mc, SINK_BUILD, A, jt, D.num_sms, st)) { set_err("unsupported m"); return MSP_INTERNAL; }
+    set_enum_range(A, udev + w.up0, w.up1 - w.up0, w.probe_tiles, D.num_sms);
+    A.unit_filtered = D.ufilt.as<unsigned long long>() + w.up0;
+    A.unit_hits = D.uhits.as<unsigned long long>() + w.up0;
+    launch_enum(P.mc, SINK_PROBE, A, jt, D.num_sms, st);
+    S.kernel_launches += 2;
+    if (profile) {
+      CK(cudaEventRecord(D.pev[1], st));
+      CK(cudaEventSynchronize(D.pev[1]));
+      hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
+      S.hot_launches += 2;
+      S.hot_pairs += (int64_t)w.pairs;
+    }
+    if (wi % sync_every == sync_every - 1 || wi + 1 == waves.size()) {
+      unsigned long long nh = 0;
+      CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaGetLastError());
+      if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
+      if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
+      if (opt->mode == MSP_MODE_FIRST && nh > hits_done) {
+        rc = recover(hits_done, nh);
+        if (rc) return rc;
+        hits_done = nh;
+        if (!sols.empty()) { S.waves = (int32_t)(wi + 1); stopped_early = true; break; }
+      }
+    }
+  }
+  CK(cudaEventRecord(D.ev[2], st));
+  std::vector<unsigned long long> uf(units.size()), uh(units.size());
+  unsigned long long nh = 0;
+  int err = 0;
+  if (!units.empty()) {
+    CK(cudaMemcpyAsync(uf.data(), D.ufilt.p, 8 * units.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(uh.data(), D.uhits.p, 8 * units.size(), cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  S.t_validate = now_s() - t_join0;
+  S.dev_ms_tables = elapsed_ms(D.ev[0], D.ev[1]);
+  S.dev_ms_join = elapsed_ms(D.ev[1], D.ev[2]);
+  S.dev_ms_hot = hot_ms;
+  if (err) { set_err("join table region overflow (err=%d)", err); return MSP_INTERNAL; }
+  for (size_t i = 0; i < units.size(); ++i) { S.filtered_residuals += (int64_t)uf[i]; S.hash_hits += (int64_t)uh[i]; }
+  if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
+  if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
+  if (!stopped_early) {
+    rc = recover(hits_done, nh);
+    if (rc) return rc;
+    if (opt->mode == MSP_MODE_ALL && recovered_hh != S.hash_hits) {
+      set_err("internal error: recovered hash hits %lld != join hash hits %lld", (long long)recovered_hh,
+              (long long)S.hash_hits);
+      return MSP_INTERNAL;
+    }
+  }
+  CK(cudaEventRecord(D.ev[3], st));
+  CK(cudaEventSynchronize(D.ev[3]));
+  S.dev_ms_total = elapsed_ms(D.ev[0], D.ev[3]);
+  S.exact_hits = (int64_t)sols.size();
+  S.t_enumerate = S.t_build;  // the plan replaces the heap stream
+  if (opt->mode == MSP_MODE_FIRST && sols.size() > 1) sols.resize(1);
+  return emit();
+}
+
+}  // namespace
+}  // namespace msp
+
+// ====================================================================== C-ABI
+
+extern "C" {
+
+int msp_solve(const msp_problem *prob, const msp_options *opt, msp_result *res) {
+  try {
+    int rc = msp::solve_impl(prob, opt, res);
+    if (rc && res) { free(res->xbits); res->xbits = nullptr; res->n_solutions = 0; }
+    return rc;
+  } catch (const std::exception &e) {
+    msp::set_err("exception: %s", e.what());
+    return MSP_INTERNAL;
+  }
+}
+
+void msp_result_free(msp_result *res) {
+  if (!res) return;
+  free(res->xbits);
+  res->xbits = nullptr;
+  res->n_solutions = 0;
+}
+
+int msp_join_alpha(const msp_problem *prob, const msp_options *opt, uint64_t alpha, msp_result *res) {
+  if (!opt) { msp::set_err("null options"); return MSP_INVALID_ARGUMENT; }
+  msp_options o = *opt;
+  o.alpha_lo = alpha;
+  o.alpha_hi = alpha + 1;
+  o.mode = MSP_MODE_ALL;
+  o.flags |= MSP_FLAG_FORCE_TABLE_PATH;
+  return msp_solve(prob, &o, res);
+}
+
+int64_t msp_alpha_plan(const msp_problem *prob, int32_t device, int64_t max_batches, uint64_t *alpha,
+                       uint64_t *beta, uint64_t *n_left, uint64_t *n_right) {
+  using namespace msp;
+  Device *D = nullptr;
+  int rc = get_device(device, &D);
+  if (rc) return -rc;
+  std::lock_guard<std::mutex> lk(D->mu);
+  if (cudaSetDevice(D->dev) != cudaSuccess) return -MSP_CUDA_ERROR;
+  Plan P;
+  rc = check_instance(prob, P);
+  if (rc) return -rc;
+  int64_t launches = 0;
+  rc = build_plan(*D, prob, P, 0, 0, D->stream, launches);
+  if (rc) return -rc;
+  for (uint32_t g = 0; g < P.G && (int64_t)g < max_batches; ++g) {
+    alpha[g] = P.alpha[g];
+    beta[g] = P.target - P.alpha[g];
+    n_left[g] = P.nl[g];
+    n_right[g] = P.nr[g];
+  }
+  return P.G;
+}
+
+int msp_build_tables(const msp_problem *prob, int32_t device, uint64_t **weights, uint32_t **masks,
+                     uint64_t **contribs, int64_t **run_end) {
+  using namespace msp;
+  Device *D = nullptr;
+  int rc = get_device(device, &D);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(D->mu);
+  CK(cudaSetDevice(D->dev));
+  Plan P;
+  rc = check_instance(prob, P);
+  if (rc) return rc;
+  int64_t launches = 0;
+  rc = build_plan(*D, prob, P, 0, 0, D->stream, launches);
+  if (rc) return rc;
+  const int m = P.m;
+  for (int t = 0; t < 4; ++t) {
+    const size_t sz = (size_t)1 << P.b[t];
+    std::vector<uint32_t> comp(sz * P.sw);
+    CK(cudaMemcpy(weights[t], table_w(*D, P, t), 8 * sz, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(masks[t], table_m(*D, P, t), 4 * sz, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(comp.data(), D->comp[t].p, 4 * sz * P.sw, cudaMemcpyDeviceToHost));
+    for (size_t e = 0; e < sz; ++e) {
+      contribs[t][e * m] = weights[t][e];
+      for (int c = 0; c < P.mc; ++c)
+        contribs[t][e * m + 1 + c] = (comp[e * P.sw + (c >> 1)] >> (16 * (c & 1))) & 0xFFFFu;
+    }
+    int64_t end = (int64_t)sz;
+    for (int64_t i = (int64_t)sz - 1; i >= 0; --i) {
+      if (i + 1 < (int64_t)sz && weights[t][i] != weights[t][i + 1]) end = i + 1;
+      run_end[t][i] = end;
+    }
+  }
+  return MSP_OK;
+}
+
+void msp_release(int32_t device) {
+  std::lock_guard<std::mutex> lk(msp::g_devices_mu);
+  auto it = msp::g_devices.find(device);
+  if (it == msp::g_devices.end()) return;
+  {
+    std::lock_guard<std::mutex> lk2(it->second->mu);
+    cudaSetDevice(device);
+    it->second->release_all();
+  }
+}
+
+const char *msp_last_error(void) { return msp::g_err.c_str(); }
+int32_t msp_version(void) { return 1; }
+
+}  // extern "C"

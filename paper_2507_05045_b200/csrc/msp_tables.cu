@@ -1,0 +1,264 @@
+// msp_tables.cu -- K1 quarter tables (merge-doubling) and K2/K3 alpha plan kernels.
+//
+// K1 replaces build_quarter_tables (enumerate1d.py:86-135): each block's power set is grown one
+// column at a time by merging the sorted list L with L + a_col, the new column taking the next
+// mask bit and ties taking the old half first.  That reproduces numpy's lexsort((masks, key))
+// order exactly (ascending weight for A,B; descending for C,D; ties by mask ascending), so table
+// indices equal the reference's.  Companion rows are then packed two u16 per u32 word.
+//
+// K2/K3 replace the heap stream (fastenum.py:87-147): with dense per-weight runs, the left count
+// of alpha is sum_w |A_w| * |B_{alpha-w}| (histogram convolution) and every batch is the union
+// of rectangles A-run(alpha - w_B) x B-run(w_B) -- no heap needed.
+#include <cstdint>
+#include "msp_common.cuh"
+#include "msp_kernels.h"
+
+namespace msp {
+
+// ------------------------------------------------------------------ merge-doubling
+
+__device__ __forceinline__ uint32_t lb_asc(const uint64_t *a, uint32_t n, uint64_t x) {  // #a[i] < x
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (a[mid] < x) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+__device__ __forceinline__ uint32_t ub_asc(const uint64_t *a, uint32_t n, uint64_t x) {  // #a[i] <= x
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (a[mid] <= x) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+__device__ __forceinline__ uint32_t gt_desc(const uint64_t *a, uint32_t n, uint64_t x) { // #a[i] > x
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (a[mid] > x) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+__device__ __forceinline__ uint32_t ge_desc(const uint64_t *a, uint32_t n, uint64_t x) { // #a[i] >= x
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (a[mid] >= x) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+
+__global__ void k_merge_step(MergeArgs args) {
+  const MergeStep s = args.s[blockIdx.y];
+  if (s.n == 0) return;
+  const uint32_t total = 2 * s.n;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    if (i < s.n) {  // old element: after every new element strictly before it
+      const uint64_t v = s.sw[i];
+      uint32_t before;
+      if (s.asc) before = v >= s.a ? lb_asc(s.sw, s.n, v - s.a) : 0;
+      else before = v < s.a ? s.n : gt_desc(s.sw, s.n, v - s.a);
+      s.dw[i + before] = v;
+      s.dm[i + before] = s.sm[i];
+    } else {        // new element: after every old element before-or-equal (old half first on ties)
+      const uint32_t q = i - s.n;
+      const uint64_t v = s.sw[q] + s.a;
+      const uint32_t before = s.asc ? ub_asc(s.sw, s.n, v) : ge_desc(s.sw, s.n, v);
+      s.dw[q + before] = v;
+      s.dm[q + before] = s.sm[q] | (1u << s.bit);
+    }
+  }
+}
+
+// Companion rows 1..m-1 of every entry, packed P16 (two u16 per word, low half = lower row).
+__global__ void k_pack(PackArgs args) {
+  const PackTable t = args.t[blockIdx.y];
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < t.size; e += gridDim.x * blockDim.x) {
+    const uint32_t mk = t.mask[e];
+    uint32_t words[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = 1; r < args.m; ++r) {
+      uint32_t s = 0;
+      for (int b = 0; b < t.b; ++b)
+        if ((mk >> b) & 1u) s += (uint32_t)args.a[(size_t)r * args.n + t.start + b];
+      const int j = r - 1;
+      words[j >> 1] |= (s & 0xFFFFu) << (16 * (j & 1));
+    }
+    for (int k = 0; k < args.sw; ++k) t.comp[(size_t)e * args.sw + k] = words[k];
+  }
+}
+
+// Dense run bounds per weight (the _run_ends information, enumerate1d.py:138-145, keyed by weight).
+__global__ void k_runs(RunArgs args) {
+  const RunTable t = args.t[blockIdx.y];
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < t.size; e += gridDim.x * blockDim.x) {
+    const uint32_t w = (uint32_t)t.w[e];
+    if (e == 0 || t.w[e - 1] != t.w[e]) t.run_start[w] = e;
+    if (e + 1 == t.size || t.w[e + 1] != t.w[e]) t.run_end[w] = e + 1;
+  }
+}
+
+// Block-wide exclusive scan of one u32 per thread (blockDim.x multiple of 32, <= 1024).
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t &total) {
+  __shared__ uint32_t warp_sums[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_sums[lane] = s;  // inclusive
+  }
+  __syncthreads();
+  const uint32_t base = wid ? warp_sums[wid - 1] : 0;
+  total = warp_sums[nw - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+// Distinct-weight run lists of B (y=0) and D (y=1), in ascending weight order.
+__global__ void k_yruns(YRunArgs args) {
+  const YRunTable t = args.t[blockIdx.x];
+  uint32_t base = 0;
+  for (uint32_t w0 = 0; w0 <= t.S; w0 += blockDim.x) {
+    const uint32_t w = w0 + threadIdx.x;
+    const uint32_t len = w <= t.S ? t.run_end[w] - t.run_start[w] : 0;
+    uint32_t tot;
+    const uint32_t pos = block_excl_scan(len > 0, tot);
+    if (len > 0) {
+      t.out_w[base + pos] = w;
+      t.out_start[base + pos] = t.run_start[w];
+      t.out_len[base + pos] = len;
+    }
+    base += tot;
+  }
+  if (threadIdx.x == 0) *t.out_n = base;
+}
+
+// hl[alpha] = sum_r |A_{alpha - w_r}| |B_r| (left) and hr[beta] = sum_r |C_{beta - w_r}| |D_r|.
+__global__ void k_conv(ConvArgs args) {
+  const ConvSide s = args.s[blockIdx.y];
+  const uint32_t ny = *s.ny;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= s.vmax; v += gridDim.x * blockDim.x) {
+    unsigned long long acc = 0;
+    for (uint32_t r = 0; r < ny; ++r) {
+      const uint32_t wy = s.yw[r];
+      if (wy > v) continue;
+      const uint32_t wx = v - wy;
+      if (wx > s.SX) continue;
+      acc += (unsigned long long)(s.x_end[wx] - s.x_start[wx]) * s.ylen[r];
+    }
+    s.out[v] = acc;
+  }
+}
+
+// Batches: alpha ascending with hl[alpha] > 0 and hr[t - alpha] > 0, restricted to the band.
+__global__ void k_groups(GroupArgs g) {
+  uint32_t base = 0;
+  for (uint64_t a0 = 0; a0 <= g.amax; a0 += blockDim.x) {
+    const uint64_t al = a0 + threadIdx.x;
+    bool ok = al <= g.amax && al >= g.alpha_lo && al < g.alpha_hi && g.hl[al] > 0 && al <= g.target;
+    uint64_t be = ok ? g.target - al : 0;
+    ok = ok && be <= g.bmax && g.hr[be] > 0;
+    uint32_t tot;
+    const uint32_t pos = block_excl_scan(ok, tot);
+    if (ok && base + pos < g.max_groups) {
+      g.alpha[base + pos] = al;
+      g.nl[base + pos] = g.hl[al];
+      g.nr[base + pos] = g.hr[be];
+    }
+    base += tot;
+  }
+  if (threadIdx.x == 0) *g.count = base;
+}
+
+// Per (batch, side): exclusive prefix over Y runs of the warp-tile counts of each rectangle.
+__global__ void k_tile_prefix(PrefixArgs p) {
+  const uint32_t g = blockIdx.x;
+  if (g >= *p.count) return;
+  const int side = blockIdx.y;
+  const PrefixSide s = p.s[side];
+  const uint32_t ny = *s.ny;
+  const uint64_t xw_total = side == 0 ? p.alpha[g] : p.target - p.alpha[g];
+  uint32_t *out = p.prefix + s.off + (size_t)g * s.stride;
+  uint64_t base = 0;
+  for (uint32_t r0 = 0; r0 < ny; r0 += blockDim.x) {
+    const uint32_t r = r0 + threadIdx.x;
+    uint32_t tiles = 0;
+    if (r < ny) {
+      const uint32_t wy = s.yw[r];
+      if (wy <= xw_total && xw_total - wy <= s.SX) {
+        const uint32_t wx = (uint32_t)(xw_total - wy);
+        const uint32_t xl = s.x_end[wx] - s.x_start[wx], yl = s.ylen[r];
+        if (xl) {
+          const uint32_t L = xl > yl ? xl : yl, Q = xl > yl ? yl : xl;
+          tiles = ((L + 31) / 32) * ((Q + kTQ - 1) / kTQ);
+        }
+      }
+    }
+    uint32_t tot;
+    const uint32_t pos = block_excl_scan(tiles, tot);
+    if (r < ny) out[r] = (uint32_t)(base + pos);
+    base += tot;
+  }
+  if (threadIdx.x == 0) {
+    out[ny] = (uint32_t)base;
+    p.tiles[(size_t)g * 2 + side] = base;
+    if (base > 0xFFFFFFFFull) atomicOr(p.err, 2);
+  }
+}
+
+// n <= 12 branch (solver.py:197-211, oracle.py:27-75): every assignment, x_1 = MSB of enc.
+__global__ void k_brute(BruteArgs b) {
+  const uint64_t total = 1ull << b.n;
+  for (uint64_t enc = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; enc < total;
+       enc += (uint64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
+    for (int i = 0; i < b.m && ok; ++i) {
+      unsigned long long s = 0;
+      for (int j = 0; j < b.n; ++j)
+        if ((enc >> (b.n - 1 - j)) & 1) s += b.a[(size_t)i * b.n + j];
+      ok = s == b.d[i];
+    }
+    if (ok) {
+      const unsigned long long k = atomicAdd(b.count, 1ull);
+      if (k < b.cap) b.out[k] = enc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ launch wrappers
+
+void launch_merge_step(const MergeArgs &a, uint32_t max_n, cudaStream_t st) {
+  const uint32_t threads = 256;
+  uint32_t blocks = (2 * max_n + threads - 1) / threads;
+  if (blocks > 4096) blocks = 4096;
+  k_merge_step<<<dim3(blocks, 4), threads, 0, st>>>(a);
+}
+void launch_pack(const PackArgs &a, uint32_t max_size, cudaStream_t st) {
+  uint32_t blocks = (max_size + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  k_pack<<<dim3(blocks, 4), 256, 0, st>>>(a);
+}
+void launch_runs(const RunArgs &a, uint32_t max_size, cudaStream_t st) {
+  uint32_t blocks = (max_size + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  k_runs<<<dim3(blocks, 4), 256, 0, st>>>(a);
+}
+void launch_yruns(const YRunArgs &a, cudaStream_t st) { k_yruns<<<2, 1024, 0, st>>>(a); }
+void launch_conv(const ConvArgs &a, uint32_t vmax, cudaStream_t st) {
+  uint32_t blocks = (vmax + 256) / 256;
+  if (blocks > 4096) blocks = 4096;
+  k_conv<<<dim3(blocks, 2), 256, 0, st>>>(a);
+}
+void launch_groups(const GroupArgs &a, cudaStream_t st) { k_groups<<<1, 1024, 0, st>>>(a); }
+void launch_tile_prefix(const PrefixArgs &a, uint32_t max_groups, cudaStream_t st) {
+  if (max_groups) k_tile_prefix<<<dim3(max_groups, 2), 256, 0, st>>>(a);
+}
+void launch_brute(const BruteArgs &a, cudaStream_t st) {
+  const uint64_t total = 1ull << a.n;
+  uint32_t blocks = (uint32_t)((total + 255) / 256);
+  if (blocks > 8192) blocks = 8192;
+  k_brute<<<blocks, 256, 0, st>>>(a);
+}
+
+}  // namespace msp

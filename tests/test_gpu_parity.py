@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path through the C-ABI against reference-generated goldens and the oracle.
+
+Bit-exact bar (integer work): identical quarter tables, batch headers, solution sets and every
+deterministic SolveStats counter (batches, candidates_left/right, filtered_residuals, hash_hits,
+exact_hits, peak_*), plus the row-1 candidate pair count.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import STAT_KEYS, inst_from, load_golden, seeded_instance
+
+pytestmark = pytest.mark.gpu
+
+import paper_2507_05045_b200 as msb  # noqa: E402
+from paper_2507_05045_b200 import _native  # noqa: E402
+from oracle import oracle as O  # noqa: E402  (checker only)
+
+
+def _solve_all(inst, **kw):
+    return msb.solve(inst, msb.SolverConfig(mode="all", **kw))
+
+
+def _strings(sols):
+    return [msb.solution_to_string(x) for x in sols]
+
+
+def test_tables_match_reference():
+    for rec in load_golden("tables.json"):
+        inst = inst_from(rec["instance"])
+        try:
+            got = _native.build_tables(inst.a, inst.d)
+        except RuntimeError:
+            continue  # outside the packed-16 mode (none of the goldens are)
+        for mine, ref in zip(got, rec["tables"]):
+            assert mine["weights"].tolist() == ref["weights"], rec["name"]
+            assert mine["masks"].tolist() == ref["masks"], rec["name"]
+            assert mine["contribs"].tolist() == ref["contribs"], rec["name"]
+            assert mine["run_end"].tolist() == ref["run_end"], rec["name"]
+
+
+def test_tables_match_oracle_large():
+    for (m, s) in ((6, 4), (7, 1), (8, 1)):
+        inst = msb.generate_instance(m, 100, s)
+        got = _native.build_tables(inst.a, inst.d)
+        ref = O.build_tables(inst.a)
+        for mine, r in zip(got, ref):
+            assert np.array_equal(mine["weights"], r["weights"])
+            assert np.array_equal(mine["masks"].astype(np.uint64), r["masks"])
+            assert np.array_equal(mine["contribs"], r["contribs"])
+            assert np.array_equal(mine["run_end"], r["run_end"])
+
+
+def test_plan_matches_reference_streams():
+    for rec in load_golden("streams.json"):
+        inst = inst_from(rec["instance"])
+        if inst.n < 4:
+            continue
+        plan = _native.alpha_plan(inst.a, inst.d)
+        ref = [(b[0], b[1], len(b[2]), len(b[3])) for b in rec["batches"]]
+        assert plan == ref, rec["name"]
+
+
+def test_plan_counts_all_configs():
+    counts = load_golden("plan_counts.json")
+    for key, ref in counts.items():
+        m, s = map(int, key.split(","))
+        inst = msb.generate_instance(m, 100, s)
+        plan = _native.alpha_plan(inst.a, inst.d)
+        assert len(plan) == ref["batches"], key
+        assert sum(p[2] for p in plan) == ref["candidates_left"], key
+        assert sum(p[3] for p in plan) == ref["candidates_right"], key
+        assert sum(p[2] * p[3] for p in plan) == ref["row1_candidate_pairs"], key
+
+
+@pytest.mark.parametrize("fixture", ["solves_small.json", "solves_medium.json"])
+def test_full_solves_match_reference(fixture):
+    for rec in load_golden(fixture):
+        inst = inst_from(rec["instance"])
+        res = _solve_all(inst)
+        assert _strings(res.solutions) == rec["solutions"], rec["name"]
+        assert res.verdict == rec["verdict"], rec["name"]
+        assert res.stats.fallback == rec["fallback"], rec["name"]
+        if rec["fallback"] == "none":
+            for k in STAT_KEYS:
+                assert getattr(res.stats, k) == rec["stats"][k], (rec["name"], k)
+            assert res.stats.engine == "cuda"
+
+
+def test_per_batch_join_matches_reference():
+    """msp_join_alpha on single batches vs the reference's per-batch validate_chunked stats."""
+    for rec in load_golden("solves_medium.json"):
+        if "batches" not in rec:
+            continue
+        inst = inst_from(rec["instance"])
+        batches = rec["batches"]
+        picks = batches[:: max(1, len(batches) // 25)] + [max(batches, key=lambda b: b[1] + b[2])]
+        picks += [b for b in batches if b[5] > 0]
+        for alpha, nl, nr, filt, hh, eh, sols in picks:
+            opts = _native.make_options(mode="all")
+            rc, xb, st = _native.solve_raw(inst.a, inst.d, opts, alpha=alpha)
+            assert rc == 0, _native.last_error()
+            assert (st["batches"], st["candidates_left"], st["candidates_right"]) == (1, nl, nr)
+            assert (st["filtered_residuals"], st["hash_hits"], st["exact_hits"]) == (filt, hh, eh), (rec["name"], alpha)
+            got = sorted("".join(map(str, r)) for r in xb.tolist())
+            assert got == sols
+
+
+@pytest.mark.parametrize("fixture", ["alpha_groups_8_100_1.json", "alpha_groups_9_100_1.json"])
+def test_alpha_groups_large_configs(fixture):
+    g = load_golden(fixture)
+    inst = inst_from(g["instance"])
+    for grp in g["groups"]:
+        opts = _native.make_options(mode="all")
+        rc, xb, st = _native.solve_raw(inst.a, inst.d, opts, alpha=grp["alpha"])
+        assert rc == 0, _native.last_error()
+        assert st["candidates_left"] == grp["n_left"] and st["candidates_right"] == grp["n_right"]
+        assert st["filtered_residuals"] == grp["filtered"], grp["alpha"]
+        assert st["hash_hits"] == grp["hash_hits"] and st["exact_hits"] == grp["exact_hits"]
+        assert sorted("".join(map(str, r)) for r in xb.tolist()) == grp["solutions"]
+
+
+def test_random_instances_match_oracle():
+    for seed in range(30):
+        m = 2 + seed % 5
+        inst = seeded_instance(3000 + seed, m=m, n=13 + seed % 12, k=3 + seed % 40,
+                               d_mode="half" if seed % 3 else "random")
+        res = _solve_all(inst)
+        ref = O.solve(inst.a, inst.d, mode="all")
+        assert res.solutions == ref.solutions, seed
+        for k in STAT_KEYS:
+            assert getattr(res.stats, k) == ref.stats[k], (seed, k)
+
+
+def test_small_waves_force_multi_pass_join():
+    """A tiny wave budget forces batches to split into hash-range passes: results unchanged."""
+    inst = msb.generate_instance(6, 100, 4)
+    ref = _solve_all(inst)
+    tiny = _solve_all(inst, wave_keys=4096)
+    assert tiny.solutions == ref.solutions
+    for k in STAT_KEYS:
+        assert getattr(tiny.stats, k) == getattr(ref.stats, k), k
+    assert tiny.stats.waves > ref.stats.waves
+
+
+def test_first_mode():
+    for (m, s) in ((4, 11), (5, 1), (6, 4)):
+        inst = msb.generate_instance(m, 100, s)
+        full = _solve_all(inst)
+        first = msb.solve(inst, msb.SolverConfig(mode="first"))
+        assert first.feasible == full.feasible
+        if full.feasible:
+            assert first.solutions[0] in full.solutions
+
+
+@pytest.mark.slow
+def test_m7_s1_full_against_reference():
+    rec = load_golden("solve_7_100_1.json")
+    inst = inst_from(rec["instance"])
+    res = _solve_all(inst)
+    assert _strings(res.solutions) == rec["solutions"]
+    for k in STAT_KEYS:
+        assert getattr(res.stats, k) == rec["stats"][k], k
+    ref_rows = rec["batches"]
+    assert res.stats.row1_candidate_pairs == sum(b[1] * b[2] for b in ref_rows)
