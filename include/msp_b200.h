@@ -106,6 +106,9 @@ int64_t msp_alpha_plan(const msp_problem *prob, int32_t device, int64_t max_batc
 /* Join of the single batch alpha (msp_solve restricted to [alpha, alpha+1)). */
 int msp_join_alpha(const msp_problem *prob, const msp_options *opt, uint64_t alpha, msp_result *res);
 
+/* INT32 ops/s of the FNV fold instruction mix on `device` (roofline denominator), or < 0 on error. */
+double msp_int32_peak(int32_t device);
+
 /* Free the cached per-device workspace. */
 void msp_release(int32_t device);
 const char *msp_last_error(void);

@@ -35,7 +35,7 @@ NVCC_FLAGS = [
 
 EXPORTED_SYMBOLS = (
     "msp_solve", "msp_result_free", "msp_build_tables", "msp_alpha_plan", "msp_join_alpha",
-    "msp_release", "msp_last_error", "msp_version",
+    "msp_release", "msp_last_error", "msp_version", "msp_int32_peak",
 )
 
 
@@ -137,6 +137,8 @@ def load(path: str | None = None):
     L.msp_last_error.restype = C.c_char_p
     L.msp_last_error.argtypes = []
     L.msp_version.restype = C.c_int32
+    L.msp_int32_peak.restype = C.c_double
+    L.msp_int32_peak.argtypes = [C.c_int32]
     _lib = L
     return L
 

@@ -55,29 +55,38 @@ struct UnitDesc {
   uint64_t h0;               // FNV state after coordinate 0 (= alpha on both sides)
   uint32_t xw_total;         // alpha (left) / beta (right): X weight = xw_total - Y weight
   uint32_t side;             // 0 left (A x B), 1 right (C x D)
-  uint32_t prefix_off;       // offset of the unit's Y-run tile prefix (nY + 1 u32)
+  uint32_t rect_base;        // first rectangle of this (batch, side) in the rectangle list
   uint32_t gid;              // batch index within the solve
-  uint32_t slot;             // wave-local batch slot (counters, zero-key counts)
-  uint32_t region_base;      // join table / hit-set region (slots)
-  uint32_t region_log2;      // log2 capacity of the region
+  uint32_t slot;             // wave-local batch slot (global-table zero-key counts)
+  uint32_t region_base;      // global table / hit-set region base, or wave bucket base
+  uint32_t region_log2;      // log2 capacity of the region, or bucket bits of the batch
   uint32_t pass, npass;      // hash-range pass filter (npass == 1: all keys)
   uint32_t count_filter;     // count overshooting right pairs in this unit
-  uint32_t flags;            // bit0: hit set contains key 0
-  uint32_t pad;
+  uint32_t flags;            // bit0: hit set contains key 0; bit1: probe role (partitioned join)
+  uint32_t nrect;            // rectangles of this (batch, side)
+};
+
+// One nonempty rectangle X-run(w_x) x Y-run(w_y) of a batch side, oriented for the warp tile:
+// the longer run goes across lanes.  tile_off = warp tiles before it within its (batch, side).
+struct RectDesc {
+  uint32_t lane_start, loop_start, L, Q;
+  uint32_t tile_off;
+  uint32_t lane_is_x;
+  uint32_t nl, nq;
 };
 
 struct EnumArgs {
   TableDev tab[4];
   YRuns yr[2];               // [0] = B runs, [1] = D runs
-  const uint32_t *prefix;    // tile prefixes of all (batch, side)
+  const RectDesc *rects;     // rectangle lists of all (batch, side)
   const UnitDesc *units;
   uint32_t nunits;
   uint64_t total_tiles;
   uint64_t chunk_tiles;      // tiles per warp work item
   uint64_t nchunks;
   uint32_t dpack[8];         // d rows 1..m-1 packed, +0x8000 guard per half (right side)
-  unsigned long long *unit_filtered;  // per unit
-  unsigned long long *unit_hits;      // per unit
+  unsigned long long *batch_filtered; // per batch (gid)
+  unsigned long long *batch_hits;     // per batch (gid)
 };
 
 __device__ __forceinline__ uint32_t pass_of(uint64_t key, uint32_t npass) {

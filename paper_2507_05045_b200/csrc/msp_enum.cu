@@ -14,61 +14,13 @@
 // Work decomposition: a batch is a union of rectangles X-run(alpha - w) x Y-run(w).  A warp tile is
 // 32 entries of the rectangle's longer run (one per lane, companion vector in registers) x up to
 // kTQ entries of the shorter run (warp-uniform loads, broadcast).  Each warp takes a contiguous
-// chunk of tiles; rectangles are located by binary search over per-batch Y-run tile prefixes.
+// chunk of tiles through the compacted rectangle lists (k_rects).
 #include <cstdint>
 #include "msp_common.cuh"
 #include "msp_kernels.h"
+#include "msp_tile.cuh"
 
 namespace msp {
-
-__device__ __forceinline__ uint32_t find_unit(const UnitDesc *u, uint32_t n, uint64_t T) {
-  uint32_t lo = 0, hi = n;  // last u with tile_base <= T
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (u[mid].tile_base <= T) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ uint32_t find_run(const uint32_t *P, uint32_t ny, uint32_t t) {
-  uint32_t lo = 0, hi = ny;  // last r in [0, ny) with P[r] <= t  (P[ny] = total > t)
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(P + mid) <= t) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-struct Rect {
-  const uint32_t *lane_comp, *loop_comp;
-  uint32_t lane_start, loop_start, L, Q, nl, nq;
-  bool lane_is_x;
-};
-
-__device__ __forceinline__ void set_rect(const EnumArgs &A, const UnitDesc &d, uint32_t r, Rect &R) {
-  const YRuns &yr = A.yr[d.side];
-  const TableDev &X = A.tab[d.side ? 2 : 0];
-  const TableDev &Y = A.tab[d.side ? 3 : 1];
-  const uint32_t wy = __ldg(yr.w + r), ys = __ldg(yr.start + r), yl = __ldg(yr.len + r);
-  const uint32_t wx = d.xw_total - wy;
-  const uint32_t xs = __ldg(X.run_start + wx), xl = __ldg(X.run_end + wx) - xs;
-  R.lane_is_x = xl >= yl;
-  if (R.lane_is_x) {
-    R.lane_comp = X.comp; R.loop_comp = Y.comp;
-    R.lane_start = xs; R.L = xl; R.loop_start = ys; R.Q = yl;
-  } else {
-    R.lane_comp = Y.comp; R.loop_comp = X.comp;
-    R.lane_start = ys; R.L = yl; R.loop_start = xs; R.Q = xl;
-  }
-  R.nl = (R.L + 31) >> 5;
-  R.nq = (R.Q + kTQ - 1) / kTQ;
-}
-
-__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 // ---------------------------------------------------------------- sinks (global hash table)
 
@@ -88,7 +40,7 @@ __device__ __forceinline__ bool table_find(const JoinTable &jt, const UnitDesc &
 
 template <int KIND>
 __device__ __forceinline__ void sink(const JoinTable &jt, const UnitDesc &d, uint64_t key, bool ok,
-                                     const Rect &R, uint32_t lidx, uint32_t qidx, const EnumArgs &A,
+                                     const RectDesc &R, uint32_t lidx, uint32_t qidx, const EnumArgs &A,
                                      unsigned long long &hits) {
   if (!ok) return;
   if (d.npass > 1 && pass_of(key, d.npass) != d.pass) return;
@@ -140,9 +92,9 @@ __device__ __forceinline__ void sink(const JoinTable &jt, const UnitDesc &d, uin
       const unsigned long long i = atomicAdd(jt.nrecs, 1ull);
       if (i < jt.rec_cap) {
         const uint32_t xi = R.lane_is_x ? lidx : qidx, yi = R.lane_is_x ? qidx : lidx;
-        const TableDev &X = A.tab[d.side ? 2 : 0];
-        const TableDev &Y = A.tab[d.side ? 3 : 1];
-        jt.recs[i] = PairRec{d.gid, d.side, xi, yi, __ldg(X.mask + xi), __ldg(Y.mask + yi), key};
+        const uint32_t *xm = d.side ? A.tab[2].mask : A.tab[0].mask;
+        const uint32_t *ym = d.side ? A.tab[3].mask : A.tab[1].mask;
+        jt.recs[i] = PairRec{d.gid, d.side, xi, yi, __ldg(xm + xi), __ldg(ym + yi), key};
       }
     }
   }
@@ -153,90 +105,40 @@ __device__ __forceinline__ void sink(const JoinTable &jt, const UnitDesc &d, uin
 template <int MC, int KIND>
 __global__ void __launch_bounds__(256) k_enum(const EnumArgs A, const JoinTable jt) {
   constexpr int NW = words_for(MC);
-  constexpr int SW = stride_for(MC);
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-
   uint32_t dg[NW > 0 ? NW : 1];
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
 
+  __shared__ __align__(16) uint32_t ybuf_all[8][kTQ * 8];
   for (uint64_t chunk = wid; chunk < A.nchunks; chunk += nwarps) {
-    uint64_t T = chunk * A.chunk_tiles;
-    const uint64_t Tend = min(T + A.chunk_tiles, A.total_tiles);
-    uint32_t u = find_unit(A.units, A.nunits, T);
-    UnitDesc d = A.units[u];
-    const uint32_t *P = A.prefix + d.prefix_off;
-    uint32_t ny = A.yr[d.side].n;
-    uint32_t tl = (uint32_t)(T - d.tile_base);
-    uint32_t r = find_run(P, ny, tl);
-    Rect R;
-    set_rect(A, d, r, R);
-    uint32_t local = tl - __ldg(P + r);
-    uint32_t lc = local / R.nq, qc = local - lc * R.nq;
+    TileWalker W;
+    W.init(A, chunk * A.chunk_tiles, min(chunk * A.chunk_tiles + A.chunk_tiles, A.total_tiles));
     unsigned long long filt = 0, hits = 0;
-
-    while (true) {
-      // ---------------- one warp tile: 32 lane entries x up to kTQ loop entries
-      const uint32_t loff = lc * 32 + lane;
-      const bool lok = loff < R.L;
-      const uint32_t lidx = R.lane_start + (lok ? loff : 0);
-      uint32_t lv[SW];
-      load_vec<SW>(R.lane_comp, lidx, lv);
-      const uint32_t q0 = qc * kTQ, q1 = min(R.Q, q0 + kTQ);
-      const uint32_t h0lo = (uint32_t)d.h0, h0hi = (uint32_t)(d.h0 >> 32);
-      const bool right = d.side != 0, cf = d.count_filter != 0;
-      for (uint32_t q = q0; q < q1; ++q) {
-        const uint32_t qidx = R.loop_start + q;
-        uint32_t yv[SW];
-        load_vec<SW>(R.loop_comp, qidx, yv);
-        uint32_t lo = h0lo, hi = h0hi;
-        bool ok = lok;
-        if (right) {
-          uint32_t g[NW > 0 ? NW : 1];
-          uint32_t acc = 0xFFFFFFFFu;
-#pragma unroll
-          for (int k = 0; k < NW; ++k) { g[k] = dg[k] - (lv[k] + yv[k]); acc &= g[k]; }
-          const bool fit = (acc & 0x80008000u) == 0x80008000u;
-          if (lok && !fit && cf) ++filt;
-          ok = ok && fit;
-#pragma unroll
-          for (int c = 0; c < MC; ++c) fnv_step(lo, hi, (g[c >> 1] >> (16 * (c & 1))) & 0x7FFFu);
-        } else {
-#pragma unroll
-          for (int c = 0; c < MC; ++c)
-            fnv_step(lo, hi, ((lv[c >> 1] + yv[c >> 1]) >> (16 * (c & 1))) & 0xFFFFu);
-        }
-        const uint64_t key = ((uint64_t)hi << 32) | lo;
-        sink<KIND>(jt, d, key, ok, R, lidx, qidx, A, hits);
-      }
-      // ---------------- advance to the next tile of the chunk
-      if (++T >= Tend) break;
-      if (++qc < R.nq) continue;
-      qc = 0;
-      if (++lc < R.nl) continue;
-      lc = 0;
-      if (u + 1 < A.nunits && T >= A.units[u + 1].tile_base) {
+    TileCursor<stride_for(MC)> C;
+    C.ybuf = ybuf_all[threadIdx.x >> 5];
+    while (W.valid()) {
+      begin_tile<MC>(A, W, lane, C);
+      while (C.q < C.q1)
+        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
+          sink<KIND>(jt, W.d, key, ok, W.R, lidx, qidx, A, hits);
+        });
+      uint32_t old;
+      if (W.advance(A, old)) {
         const unsigned long long f = warp_sum(filt), h = warp_sum(hits);
         if (lane == 0) {
-          if (f) atomicAdd(A.unit_filtered + u, f);
-          if (h) atomicAdd(A.unit_hits + u, h);
+          if (f) atomicAdd(A.batch_filtered + A.units[old].gid, f);
+          if (h) atomicAdd(A.batch_hits + A.units[old].gid, h);
         }
         filt = hits = 0;
-        while (u + 1 < A.nunits && T >= A.units[u + 1].tile_base) ++u;
-        d = A.units[u];
-        P = A.prefix + d.prefix_off;
-        ny = A.yr[d.side].n;
       }
-      tl = (uint32_t)(T - d.tile_base);
-      r = find_run(P, ny, tl);
-      set_rect(A, d, r, R);
     }
     const unsigned long long f = warp_sum(filt), h = warp_sum(hits);
     if (lane == 0) {
-      if (f) atomicAdd(A.unit_filtered + u, f);
-      if (h) atomicAdd(A.unit_hits + u, h);
+      if (f) atomicAdd(A.batch_filtered + W.d.gid, f);
+      if (h) atomicAdd(A.batch_hits + W.d.gid, h);
     }
   }
 }

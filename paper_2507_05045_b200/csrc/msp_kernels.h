@@ -40,14 +40,15 @@ struct GroupArgs {
   uint64_t *alpha; unsigned long long *nl, *nr; uint32_t *count; uint32_t max_groups;
 };
 
-struct PrefixSide {
-  const uint32_t *x_start, *x_end; uint32_t SX;
-  const uint32_t *yw, *ylen; const uint32_t *ny;
-  size_t off, stride;
+struct RectSide {
+  const uint32_t *x_start, *x_end; uint32_t SX;  // X table dense runs (A or C)
+  const uint32_t *yw, *ys, *ylen; const uint32_t *ny;  // Y runs (B or D)
 };
-struct PrefixArgs {
-  PrefixSide s[2]; const uint64_t *alpha; uint64_t target; const uint32_t *count;
-  uint32_t *prefix; unsigned long long *tiles; int *err;
+struct RectArgs {
+  RectSide s[2]; const uint64_t *alpha; uint64_t target; const uint32_t *count;
+  unsigned long long *tiles; uint32_t *nrect;  // count mode outputs, per (batch, side)
+  const uint32_t *rect_base; RectDesc *rects;  // write mode (rects != nullptr)
+  int *err;
 };
 
 struct BruteArgs {
@@ -72,8 +73,27 @@ void launch_runs(const RunArgs &a, uint32_t max_size, cudaStream_t st);
 void launch_yruns(const YRunArgs &a, cudaStream_t st);
 void launch_conv(const ConvArgs &a, uint32_t vmax, cudaStream_t st);
 void launch_groups(const GroupArgs &a, cudaStream_t st);
-void launch_tile_prefix(const PrefixArgs &a, uint32_t max_groups, cudaStream_t st);
+void launch_rects(const RectArgs &a, uint32_t max_groups, cudaStream_t st);
 void launch_brute(const BruteArgs &a, cudaStream_t st);
+
+// Partitioned join (msp_part.cu).  Buckets of one wave, per role (0 = build, 1 = probe).
+constexpr int kMaxWaveBuckets = 512;   // buckets per role per wave
+constexpr int kScatterWarpsHost = 16;  // warps per k_scatter CTA (must match msp_part.cu)
+constexpr int kJoinSlotsLog2 = 14;     // shared-memory join table: 16K (key, count) slots
+constexpr uint32_t kBucketTarget = 1u << (kJoinSlotsLog2 - 1);  // mean build keys per bucket
+struct PartArgs {
+  unsigned long long *scratch;
+  const uint32_t *start[2];   // bucket region start in scratch
+  const uint32_t *cap[2];     // bucket region capacity
+  uint32_t *fill[2];          // keys written (reset by k_join)
+  const uint32_t *gid;        // batch of each bucket
+  uint32_t nb;                // buckets per role
+  unsigned int *batch_ovf;    // per batch: a bucket overflowed -> re-join with the global table
+  HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;
+  unsigned long long *batch_hits;
+};
+cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int num_sms, cudaStream_t st);
+cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 
 enum SinkKind { SINK_BUILD = 0, SINK_PROBE = 1, SINK_RECOVER = 2 };
 // Enumerate every pair of the launch's units, hash it, and hand the key to the sink.

@@ -1,0 +1,311 @@
+// msp_part.cu -- K4/K5 as a radix-partitioned shared-memory hash join (the default join path).
+//
+// Same semantics as fastval._join_pairs (fastval.py:47-108): every left key is joined with every
+// unfiltered right key of the same batch and all full-64-bit-hash-equal pairs are counted
+// (hash_hits) and reported for exact confirmation.  Instead of bucket chains in DRAM, one wave of
+// batches is joined in two launches:
+//
+//   k_scatter  enumerate + hash (msp_tile.cuh), stage 4096 keys per CTA round in shared memory,
+//              counting-sort them by bucket (top bits of the key within the batch), reserve space
+//              per bucket with one global atomic, and write bucket-contiguous runs into an
+//              L2-resident scratch.  Right pairs that overshoot d are counted, not written.
+//   k_join     one CTA per bucket: insert the build side's keys (the smaller side of the batch)
+//              into a 16K-slot (key, count) table in shared memory, stream the probe side's keys
+//              through it, count hash hits, record each hit key once for recovery.
+//
+// The per-bucket capacity is sized from the exact batch counts (mean + 7 sigma); a bucket that
+// overflows (duplicate-heavy instances) marks its batch, which the host re-joins with the global
+// table path (msp_enum.cu), so results never depend on the partitioning.
+#include <cstdint>
+#include "msp_common.cuh"
+#include "msp_kernels.h"
+#include "msp_tile.cuh"
+
+namespace msp {
+
+constexpr int kScatterWarps = 16;
+constexpr int kWarpStage = 512;                         // keys a warp stages per round
+constexpr int kStage = kScatterWarps * kWarpStage;      // keys staged per CTA round
+constexpr uint32_t kOvf = 0x80000000u;
+
+size_t scatter_smem_bytes() {
+  return (size_t)kStage * (8 + 8 + 2 + 2 + 2) + (size_t)2 * kMaxWaveBuckets * 4 * 3 + 64;
+}
+
+template <int MC>
+__global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A, const PartArgs S) {
+  constexpr int NW = words_for(MC);
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long *skey = reinterpret_cast<unsigned long long *>(smem);
+  unsigned long long *sorted = skey + kStage;
+  uint16_t *sbkt = reinterpret_cast<uint16_t *>(sorted + kStage);
+  uint16_t *rank = sbkt + kStage;
+  uint16_t *sortb = rank + kStage;
+  uint32_t *hist = reinterpret_cast<uint32_t *>(sortb + kStage);
+  uint32_t *off = hist + 2 * kMaxWaveBuckets;
+  uint32_t *abase = off + 2 * kMaxWaveBuckets;
+  __shared__ uint32_t warp_tot[kScatterWarps];
+  __shared__ uint8_t ovf[2 * kMaxWaveBuckets];
+  __shared__ __align__(16) uint32_t ybuf_all[kScatterWarps][kTQ * 8];
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t nbw = S.nb;             // buckets per role in this wave
+  const uint32_t nent = 2 * nbw;         // (role, bucket) histogram entries
+  uint32_t dg[NW > 0 ? NW : 1];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
+  for (uint32_t i = tid; i < 2 * kMaxWaveBuckets; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  unsigned long long *mykey = skey + warp * kWarpStage;
+  uint16_t *mybk = sbkt + warp * kWarpStage;
+  uint16_t *myrank = rank + warp * kWarpStage;
+
+  for (uint64_t chunk = blockIdx.x; chunk < A.nchunks; chunk += gridDim.x) {
+    const uint64_t wT = (chunk * kScatterWarps + warp) * A.chunk_tiles;
+    TileWalker W;
+    W.init(A, min(wT, A.total_tiles), min(wT + A.chunk_tiles, A.total_tiles));
+    TileCursor<stride_for(MC)> C;
+    C.ybuf = ybuf_all[warp];
+    bool have = W.valid();
+    if (have) begin_tile<MC>(A, W, lane, C);
+    unsigned long long filt = 0;
+    while (true) {
+      // ---- fill: append valid keys densely (ballot + popc) and rank them within their bucket,
+      //      until the warp's stage is full
+      uint32_t cnt = 0;
+      while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
+        const uint32_t bbase = ((W.d.flags >> 1) & 1u) * nbw + W.d.region_base;
+        const uint32_t bits = W.d.region_log2;
+        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
+          const uint32_t m = __ballot_sync(0xffffffffu, ok);
+          if (ok) {
+            const uint32_t pos = cnt + __popc(m & lt_mask);
+            const uint32_t b = bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u);
+            mykey[pos] = key;
+            mybk[pos] = (uint16_t)b;
+            myrank[pos] = (uint16_t)atomicAdd(hist + b, 1u);
+          }
+          cnt += __popc(m);
+        });
+        if (C.q >= C.q1) {
+          uint32_t old;
+          if (W.advance(A, old)) {
+            const unsigned long long f = warp_sum(filt);
+            if (lane == 0 && f) atomicAdd(A.batch_filtered + A.units[old].gid, f);
+            filt = 0;
+          }
+          have = W.valid();
+          if (have) begin_tile<MC>(A, W, lane, C);
+        }
+      }
+      if (!__syncthreads_or(cnt > 0)) break;
+      // ---- exclusive scan over (role, bucket) counts + one global reservation per bucket; the
+      //      thread's kPer reservations are independent atomics issued back to back
+      constexpr int kPer = 2 * kMaxWaveBuckets / (kScatterWarps * 32);
+      const uint32_t j0 = tid * kPer;
+      uint32_t hv[kPer], local = 0;
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        hv[k] = j0 + k < nent ? hist[j0 + k] : 0u;
+        hist[j0 + k] = 0u;  // ready for the next fill
+        local += hv[k];
+      }
+      uint32_t incl = local;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      if (lane == 31) warp_tot[warp] = incl;
+      uint32_t gres[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const uint32_t j = j0 + k, role = j >= nbw;
+        gres[k] = hv[k] ? atomicAdd((role ? S.fill[1] : S.fill[0]) + (j - role * nbw), hv[k]) : 0u;
+      }
+      __syncthreads();
+      uint32_t run = incl - local;
+      for (uint32_t w = 0; w < warp; ++w) run += warp_tot[w];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const uint32_t j = j0 + k;
+        if (j < nent) {
+          off[j] = run;
+          ovf[j] = 0;
+          if (hv[k]) {
+            const uint32_t role = j >= nbw, b = j - role * nbw;
+            if (gres[k] + hv[k] > __ldg((role ? S.cap[1] : S.cap[0]) + b)) {
+              ovf[j] = 1;
+              atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+            } else {
+              abase[j] = __ldg((role ? S.start[1] : S.start[0]) + b) + gres[k] - run;
+            }
+          }
+        }
+        run += hv[k];
+      }
+      uint32_t total = 0;
+      for (int w = 0; w < kScatterWarps; ++w) total += warp_tot[w];
+      __syncthreads();
+      // ---- reorder into bucket-sorted runs (each warp its own staged keys)
+      for (uint32_t j = lane; j < cnt; j += 32) {
+        const uint16_t b = mybk[j];
+        const uint32_t pos = off[b] + myrank[j];
+        sorted[pos] = mykey[j];
+        sortb[pos] = b;
+      }
+      __syncthreads();
+      // ---- coalesced write-out of the runs
+      for (uint32_t pos = tid; pos < total; pos += blockDim.x) {
+        const uint16_t b = sortb[pos];
+        if (!ovf[b]) S.scratch[abase[b] + pos] = sorted[pos];
+      }
+      __syncthreads();
+    }
+    const unsigned long long f = warp_sum(filt);
+    if (lane == 0 && f) atomicAdd(A.batch_filtered + W.d.gid, f);
+  }
+}
+
+constexpr int kJoinThreads = 1024;
+constexpr int kJoinSlots = 1 << kJoinSlotsLog2;
+
+size_t join_smem_bytes() { return (size_t)kJoinSlots * 12 + 64; }
+
+__global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned long long *tk = reinterpret_cast<unsigned long long *>(smem);
+  uint32_t *tc = reinterpret_cast<uint32_t *>(tk + kJoinSlots);
+  __shared__ unsigned int zb, zhit;
+  __shared__ unsigned long long bhits[kJoinThreads / 32];
+  const uint32_t tid = threadIdx.x;
+  constexpr uint32_t mask = kJoinSlots - 1;
+
+  for (uint32_t b = blockIdx.x; b < S.nb; b += gridDim.x) {
+    for (uint32_t i = tid; i < kJoinSlots; i += kJoinThreads) { tk[i] = 0ull; tc[i] = 0u; }
+    if (tid == 0) { zb = 0; zhit = 0; }
+    __syncthreads();
+    const uint32_t gid = __ldg(S.gid + b);
+    const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
+    const unsigned long long *bk = S.scratch + __ldg(S.start[0] + b);
+    constexpr int U = 8;  // keys prefetched per thread before the table operations
+    for (uint32_t base = 0; base < nbuild; base += kJoinThreads * U) {
+      unsigned long long kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = base + u * kJoinThreads + tid;
+        kv[u] = i < nbuild ? bk[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long k = kv[u];
+        if (base + u * kJoinThreads + tid >= nbuild) continue;
+        if (k == 0) { atomicAdd(&zb, 1u); continue; }
+        uint32_t s = (uint32_t)((k * kGolden) >> (64 - kJoinSlotsLog2));
+        for (uint32_t p = 0; p <= mask; ++p) {
+          const unsigned long long old = atomicCAS(tk + s, 0ull, k);
+          if (old == 0ull) break;
+          if (old == k) { atomicAdd(tc + s, 1u); break; }
+          s = (s + 1) & mask;
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
+    const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
+    unsigned long long hits = 0;
+    for (uint32_t base = 0; base < nprobe; base += kJoinThreads * U) {
+      unsigned long long kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = base + u * kJoinThreads + tid;
+        kv[u] = i < nprobe ? pk[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long k = kv[u];
+        if (base + u * kJoinThreads + tid >= nprobe) continue;
+        if (k == 0) {
+          if (zb) {
+            hits += zb;
+            if (atomicExch(&zhit, 1u) == 0u) {
+              const unsigned long long h = atomicAdd(S.nhits, 1ull);
+              if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, 0ull};
+            }
+          }
+          continue;
+        }
+        uint32_t s = (uint32_t)((k * kGolden) >> (64 - kJoinSlotsLog2));
+        for (uint32_t p = 0; p <= mask; ++p) {
+          const unsigned long long t = tk[s];
+          if (t == k) {
+            const uint32_t c = tc[s];
+            hits += (c & ~kOvf) + 1;
+            if (!(c & kOvf) && !(atomicOr(tc + s, kOvf) & kOvf)) {
+              const unsigned long long h = atomicAdd(S.nhits, 1ull);
+              if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
+            }
+            break;
+          }
+          if (t == 0ull) break;
+          s = (s + 1) & mask;
+        }
+      }
+    }
+    hits = warp_sum(hits);
+    if ((tid & 31) == 0) bhits[tid >> 5] = hits;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < kJoinThreads / 32; ++w) t += bhits[w];
+      if (t) atomicAdd(S.batch_hits + gid, t);
+      S.fill[0][b] = 0;
+      S.fill[1][b] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+template <int MC>
+static cudaError_t launch_scatter_mc(const EnumArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
+  static bool configured = false;
+  const size_t sm = scatter_smem_bytes();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_scatter<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_scatter<MC><<<grid, kScatterWarps * 32, sm, st>>>(a, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int num_sms, cudaStream_t st) {
+  if (args.nchunks == 0) return cudaSuccess;
+  const uint64_t cap = (uint64_t)num_sms;
+  const int grid = (int)(args.nchunks < cap ? args.nchunks : cap);
+  switch (mc) {
+#define MSP_CASE(N) case N: return launch_scatter_mc<N>(args, p, grid, st);
+    MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
+    MSP_CASE(8) MSP_CASE(9) MSP_CASE(10) MSP_CASE(11) MSP_CASE(12) MSP_CASE(13) MSP_CASE(14)
+    MSP_CASE(15)
+#undef MSP_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st) {
+  static bool configured = false;
+  const size_t sm = join_smem_bytes();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (p.nb == 0) return cudaSuccess;
+  const uint32_t grid = p.nb < (uint32_t)num_sms ? p.nb : (uint32_t)num_sms;
+  k_join<<<grid, kJoinThreads, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace msp

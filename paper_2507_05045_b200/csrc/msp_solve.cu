@@ -1,13 +1,14 @@
 // msp_solve.cu -- host orchestration and the C-ABI of libmsp_b200.so.
 //
 // One msp_solve call = the reference's table path (solver.py:213-245) on one GPU:
-//   K1 quarter tables -> K2 plan (runs, convolution, batch list, tile prefixes) -> one host sync
+//   K1 quarter tables -> K2 plan (runs, convolution, batch list, rectangle lists) -> one host sync
 //   -> join waves (build / probe launches over the global hash table) -> hit recovery -> exact
 //   confirmation on the host (validate.py:285-313) -> solution bit vectors.
 // All arithmetic on the hot path runs in the kernels of msp_tables.cu / msp_enum.cu; the host only
 // plans waves and confirms the (rare) full-hash hits exactly, as the reference does on its CPU.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -74,17 +75,19 @@ struct Device {
   DBuf a, d;
   DBuf tw[4], tm[4], tw2[4], tm2[4], comp[4], rs[4], re[4];
   DBuf yw[2], ys[2], yl[2], yn;
-  DBuf hl, hr, galpha, gnl, gnr, gcount, prefix, tiles, err;
+  DBuf hl, hr, galpha, gnl, gnr, gcount, rects, nrect, rbase, tiles, err;
   DBuf units, ufilt, uhits;
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
   DBuf rkeys, runits, rfilt, rhits;
+  DBuf bfilt, bhits, bovf, scratch, bk, fill;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
-    DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &prefix, &tiles, &err,
+    DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
-                   &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits};
+                   &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
+                   &bfilt, &bhits, &bovf, &scratch, &bk, &fill};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
                                   comp[i].release(); rs[i].release(); re[i].release(); }
@@ -134,7 +137,7 @@ struct Plan {
   uint32_t ny[2] = {0, 0};
   uint32_t G = 0;
   std::vector<uint64_t> alpha, nl, nr, tiles;  // tiles[2g + side]
-  size_t stride[2] = {0, 0}, off[2] = {0, 0};
+  std::vector<uint32_t> rect_base, nrect;      // [2g + side]
   EnumArgs base{};
   int merge_w_cur[4] = {0, 0, 0, 0};  // which ping-pong buffer holds the final table
 };
@@ -267,39 +270,47 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   P.ny[1] = hdr[3];
   P.alpha.resize(P.G); P.nl.resize(P.G); P.nr.resize(P.G); P.tiles.assign(2 * (size_t)P.G, 0);
   if (P.G == 0) return MSP_OK;
-  // ---- tile prefixes per (batch, side)
-  P.stride[0] = P.ny[0] + 1;
-  P.stride[1] = P.ny[1] + 1;
-  P.off[0] = 0;
-  P.off[1] = (size_t)P.G * P.stride[0];
-  const size_t npre = P.off[1] + (size_t)P.G * P.stride[1];
-  if (npre > 0xFFFFFFFFull) { set_err("tile prefix table too large"); return MSP_UNSUPPORTED; }
-  CK(D.prefix.ensure(4 * npre));
+  // ---- rectangle lists per (batch, side): count pass, one sync, write pass
   CK(D.tiles.ensure(16 * (size_t)P.G));
+  CK(D.nrect.ensure(8 * (size_t)P.G));
+  CK(D.rbase.ensure(8 * (size_t)P.G));
   CK(D.err.ensure(16));
   CK(cudaMemsetAsync(D.err.p, 0, 16, st));
-  PrefixArgs pp{};
+  RectArgs ra2{};
   for (int s = 0; s < 2; ++s) {
     const int X = s ? 2 : 0;
-    pp.s[s] = PrefixSide{D.rs[X].as<uint32_t>(), D.re[X].as<uint32_t>(), P.S[X], D.yw[s].as<uint32_t>(),
-                         D.yl[s].as<uint32_t>(), D.yn.as<uint32_t>() + s, P.off[s], P.stride[s]};
+    ra2.s[s] = RectSide{D.rs[X].as<uint32_t>(), D.re[X].as<uint32_t>(), P.S[X], D.yw[s].as<uint32_t>(),
+                        D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), D.yn.as<uint32_t>() + s};
   }
-  pp.alpha = D.galpha.as<uint64_t>();
-  pp.target = P.target;
-  pp.count = D.gcount.as<uint32_t>();
-  pp.prefix = D.prefix.as<uint32_t>();
-  pp.tiles = D.tiles.as<unsigned long long>();
-  pp.err = D.err.as<int>();
-  launch_tile_prefix(pp, P.G, st);
+  ra2.alpha = D.galpha.as<uint64_t>();
+  ra2.target = P.target;
+  ra2.count = D.gcount.as<uint32_t>();
+  ra2.tiles = D.tiles.as<unsigned long long>();
+  ra2.nrect = D.nrect.as<uint32_t>();
+  ra2.err = D.err.as<int>();
+  launch_rects(ra2, P.G, st);
   ++launches;
   int err = 0;
+  std::vector<uint32_t> nrect(2 * (size_t)P.G);
   CK(cudaMemcpyAsync(P.alpha.data(), D.galpha.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.nl.data(), D.gnl.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.nr.data(), D.gnr.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.tiles.data(), D.tiles.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(nrect.data(), D.nrect.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (err) { set_err("tile count of one batch side exceeds 2^32"); return MSP_UNSUPPORTED; }
+  P.rect_base.assign(2 * (size_t)P.G, 0);
+  P.nrect = nrect;
+  uint64_t nrt = 0;
+  for (size_t i = 0; i < 2 * (size_t)P.G; ++i) { P.rect_base[i] = (uint32_t)nrt; nrt += nrect[i]; }
+  if (nrt > 0xFFFFFFFFull) { set_err("rectangle list too large"); return MSP_UNSUPPORTED; }
+  CK(D.rects.ensure(sizeof(RectDesc) * std::max<uint64_t>(nrt, 1)));
+  CK(cudaMemcpyAsync(D.rbase.p, P.rect_base.data(), 8 * (size_t)P.G, cudaMemcpyHostToDevice, st));
+  ra2.rect_base = D.rbase.as<uint32_t>();
+  ra2.rects = D.rects.as<RectDesc>();
+  launch_rects(ra2, P.G, st);
+  ++launches;
   // ---- launch-invariant enumeration arguments
   EnumArgs &A = P.base;
   for (int t = 0; t < 4; ++t)
@@ -307,7 +318,7 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
                         D.re[t].as<uint32_t>(), P.S[t], 1u << P.b[t]};
   for (int s = 0; s < 2; ++s)
     A.yr[s] = YRuns{D.yw[s].as<uint32_t>(), D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), P.ny[s]};
-  A.prefix = D.prefix.as<uint32_t>();
+  A.rects = D.rects.as<RectDesc>();
   for (int k = 0; k < 8; ++k) {
     const int c0 = 2 * k + 1, c1 = 2 * k + 2;  // rows c0, c1 (1-based companion rows)
     const uint32_t lo = (c0 < m ? (uint32_t)pr->d[c0] : 0u) + 0x8000u;
@@ -332,7 +343,8 @@ UnitDesc make_unit(const Plan &P, uint32_t g, int side, uint64_t tile_base) {
   u.h0 = fnv_step64(kFnvOffset, P.alpha[g]);
   u.xw_total = (uint32_t)(side == 0 ? P.alpha[g] : P.target - P.alpha[g]);
   u.side = side;
-  u.prefix_off = (uint32_t)(P.off[side] + (size_t)g * P.stride[side]);
+  u.rect_base = P.rect_base[2 * (size_t)g + side];
+  u.nrect = P.nrect[2 * (size_t)g + side];
   u.gid = g;
   u.npass = 1;
   return u;
@@ -513,111 +525,39 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   S.row1_pairs_hi = (uint64_t)(row1 >> 64);
   if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
 
-  // ---- wave plan (global-table join): build on the smaller side of each batch
-  const uint64_t slot_budget = opt->wave_keys ? std::max<uint64_t>(1024, opt->wave_keys) : (1ull << 22);
-  std::vector<UnitDesc> units;
-  std::vector<Wave> waves;
-  Wave cur;
-  uint64_t tb_build = 0, tb_probe = 0;
-  std::vector<UnitDesc> pend_build, pend_probe;
-  auto flush = [&]() {
-    if (pend_build.empty()) return;
-    cur.ub0 = units.size();
-    units.insert(units.end(), pend_build.begin(), pend_build.end());
-    cur.ub1 = units.size();
-    cur.up0 = units.size();
-    units.insert(units.end(), pend_probe.begin(), pend_probe.end());
-    cur.up1 = units.size();
-    cur.build_tiles = tb_build;
-    cur.probe_tiles = tb_probe;
-    waves.push_back(cur);
-    cur = Wave();
-    pend_build.clear();
-    pend_probe.clear();
-    tb_build = tb_probe = 0;
-  };
-  for (uint32_t g = 0; g < P.G; ++g) {
-    const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
-    const uint64_t nb = bside ? P.nr[g] : P.nl[g];
-    const uint64_t need = 1ull << std::max<uint32_t>(6, pow2ceil(2 * nb));
-    uint32_t npass = 1;
-    uint64_t cap = need;
-    if (need > slot_budget) {
-      npass = (uint32_t)((2 * nb + slot_budget - 1) / slot_budget);
-      do {
-        ++npass;
-        cap = 1ull << std::max<uint32_t>(6, pow2ceil((uint64_t)(2.2 * (double)nb / npass) + 64));
-      } while (cap > slot_budget);
-      flush();
-    }
-    for (uint32_t p = 0; p < npass; ++p) {
-      if (npass == 1 && cur.slots + cap > slot_budget) flush();
-      UnitDesc ub = make_unit(P, g, bside, tb_build);
-      UnitDesc up = make_unit(P, g, 1 - bside, tb_probe);
-      for (UnitDesc *u : {&ub, &up}) {
-        u->slot = cur.nslot;
-        u->region_base = (uint32_t)cur.slots;
-        u->region_log2 = pow2ceil(cap);
-        u->pass = p;
-        u->npass = npass;
-        u->count_filter = (u->side == 1 && p == 0);
-      }
-      tb_build += P.tiles[2 * g + bside];
-      tb_probe += P.tiles[2 * g + 1 - bside];
-      cur.pairs += P.nl[g] + P.nr[g];
-      pend_build.push_back(ub);
-      pend_probe.push_back(up);
-      cur.slots += cap;
-      cur.nslot++;
-      if (npass > 1) flush();
-    }
-  }
-  flush();
-  S.waves = (int32_t)waves.size();
-
-  // ---- join waves
+  // ---- per-batch counters, hit list
+  const size_t G1 = std::max<size_t>(1, P.G);
+  CK(D.bfilt.ensure(8 * G1));
+  CK(D.bhits.ensure(8 * G1));
+  CK(D.bovf.ensure(4 * G1));
+  CK(cudaMemsetAsync(D.bfilt.p, 0, 8 * G1, st));
+  CK(cudaMemsetAsync(D.bhits.p, 0, 8 * G1, st));
+  CK(cudaMemsetAsync(D.bovf.p, 0, 4 * G1, st));
   const uint64_t hit_cap = 1 << 20;
-  uint32_t max_nslot = 1;
-  uint64_t max_slots = 64;
-  for (const Wave &w : waves) { max_nslot = std::max(max_nslot, w.nslot); max_slots = std::max(max_slots, w.slots); }
-  const size_t nu = std::max<size_t>(1, units.size());
-  CK(D.units.ensure(sizeof(UnitDesc) * nu));
-  CK(D.ufilt.ensure(8 * nu));
-  CK(D.uhits.ensure(8 * nu));
-  CK(D.keys.ensure(8 * max_slots));
-  CK(D.cnt.ensure(8 * max_slots));
-  CK(D.zero.ensure(8 * max_nslot));
-  CK(D.zhit.ensure(4 * max_nslot));
   CK(D.hits.ensure(sizeof(HitRec) * hit_cap));
   CK(D.nhits.ensure(8));
   CK(D.nrecs.ensure(8));
-  if (!units.empty())
-    CK(cudaMemcpyAsync(D.units.p, units.data(), sizeof(UnitDesc) * units.size(), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(D.ufilt.p, 0, 8 * nu, st));
-  CK(cudaMemsetAsync(D.uhits.p, 0, 8 * nu, st));
   CK(cudaMemsetAsync(D.nhits.p, 0, 8, st));
   CK(cudaMemsetAsync(D.err.p, 0, 16, st));
   JoinTable jt{};
-  jt.keys = D.keys.as<unsigned long long>();
-  jt.cnt = D.cnt.as<unsigned long long>();
-  jt.zero = D.zero.as<unsigned long long>();
-  jt.zero_hit = D.zhit.as<unsigned int>();
   jt.hits = D.hits.as<HitRec>();
   jt.nhits = D.nhits.as<unsigned long long>();
   jt.hit_cap = hit_cap;
   jt.err = D.err.as<int>();
-  const UnitDesc *udev = D.units.as<UnitDesc>();
   EnumArgs A = P.base;
+  A.batch_filtered = D.bfilt.as<unsigned long long>();
+  A.batch_hits = D.bhits.as<unsigned long long>();
   double hot_ms = 0;
   const double t_join0 = now_s();
+  uint64_t hits_done = 0;
+  bool stopped = false;
+  std::vector<uint8_t> dropped(P.G, 0);  // batches whose partitioned join overflowed
 
-  // Recovery of hits [h_from, h_to): re-enumerate those batches, emit the pairs whose key is a hit
-  // key, confirm exactly on the host.  Uses its own buffers so waves can resume afterwards.
+  // Recovery of a set of hit keys: re-enumerate those batches, emit the pairs whose key is a hit
+  // key, confirm exactly on the host (validate.py:285-313).  Own buffers: waves can resume after.
   int64_t recovered_hh = 0;
-  auto recover = [&](uint64_t h_from, uint64_t h_to) -> int {
-    if (h_to <= h_from) return MSP_OK;
-    std::vector<HitRec> hv(h_to - h_from);
-    CK(cudaMemcpy(hv.data(), D.hits.as<HitRec>() + h_from, sizeof(HitRec) * hv.size(), cudaMemcpyDeviceToHost));
+  auto recover = [&](const std::vector<HitRec> &hv) -> int {
+    if (hv.empty()) return MSP_OK;
     std::map<uint32_t, std::vector<uint64_t>> byg;
     for (const HitRec &h : hv) byg[h.gid].push_back(h.key);
     std::vector<UnitDesc> ru;
@@ -650,13 +590,15 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
     CK(D.rkeys.ensure(8 * std::max<uint64_t>(slots, 1)));
     CK(D.runits.ensure(sizeof(UnitDesc) * ru.size()));
-    CK(D.rfilt.ensure(8 * ru.size()));
-    CK(D.rhits.ensure(8 * ru.size()));
+    CK(D.rfilt.ensure(8 * P.G));
+    CK(D.rhits.ensure(8 * P.G));
     CK(cudaMemcpyAsync(D.rkeys.p, himg.data(), 8 * slots, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(D.runits.p, ru.data(), sizeof(UnitDesc) * ru.size(), cudaMemcpyHostToDevice, st));
     JoinTable rj = jt;
     rj.keys = D.rkeys.as<unsigned long long>();
     EnumArgs RA = P.base;
+    RA.batch_filtered = D.rfilt.as<unsigned long long>();
+    RA.batch_hits = D.rhits.as<unsigned long long>();
     uint64_t rec_cap = std::max<uint64_t>(4096, 4 * hv.size());
     for (int attempt = 0; attempt < 2; ++attempt) {
       CK(D.recs.ensure(sizeof(PairRec) * rec_cap));
@@ -665,8 +607,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       rj.nrecs = D.nrecs.as<unsigned long long>();
       rj.rec_cap = rec_cap;
       set_enum_range(RA, D.runits.as<UnitDesc>(), ru.size(), tb, D.num_sms);
-      RA.unit_filtered = D.rfilt.as<unsigned long long>();
-      RA.unit_hits = D.rhits.as<unsigned long long>();
       launch_enum(P.mc, SINK_RECOVER, RA, rj, D.num_sms, st);
       ++S.kernel_launches;
       CK(cudaGetLastError());
@@ -685,55 +625,276 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     set_err("hit recovery buffer overflow");
     return MSP_INTERNAL;
   };
-
-  uint64_t hits_done = 0;
-  bool stopped_early = false;
-  const size_t sync_every = (deadline || opt->mode == MSP_MODE_FIRST) ? 16 : waves.size() + 1;
-  for (size_t wi = 0; wi < waves.size(); ++wi) {
-    const Wave &w = waves[wi];
-    CK(cudaMemsetAsync(D.keys.p, 0, 8 * w.slots, st));
-    CK(cudaMemsetAsync(D.cnt.p, 0, 8 * w.slots, st));
-    CK(cudaMemsetAsync(D.zero.p, 0, 8 * w.nslot, st));
-    CK(cudaMemsetAsync(D.zhit.p, 0, 4 * w.nslot, st));
-    if (profile) CK(cudaEventRecord(D.pev[0], st));
-    set_enum_range(A, udev + w.ub0, w.ub1 - w.ub0, w.build_tiles, D.num_sms);
-    A.unit_filtered = D.ufilt.as<unsigned long long>() + w.ub0;
-    A.unit_hits = D.uhits.as<unsigned long long>() + w.ub0;
-    if (launch_enum(P.mc, SINK_BUILD, A, jt, D.num_sms, st)) { set_err("unsupported m"); return MSP_INTERNAL; }
-    set_enum_range(A, udev + w.up0, w.up1 - w.up0, w.probe_tiles, D.num_sms);
-    A.unit_filtered = D.ufilt.as<unsigned long long>() + w.up0;
-    A.unit_hits = D.uhits.as<unsigned long long>() + w.up0;
-    launch_enum(P.mc, SINK_PROBE, A, jt, D.num_sms, st);
-    S.kernel_launches += 2;
-    if (profile) {
-      CK(cudaEventRecord(D.pev[1], st));
-      CK(cudaEventSynchronize(D.pev[1]));
-      hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
-      S.hot_launches += 2;
-      S.hot_pairs += (int64_t)w.pairs;
+  auto fetch_hits = [&](uint64_t from, uint64_t to, std::vector<HitRec> &out) -> int {
+    out.clear();
+    if (to <= from) return MSP_OK;
+    std::vector<HitRec> hv(to - from);
+    CK(cudaMemcpy(hv.data(), D.hits.as<HitRec>() + from, sizeof(HitRec) * hv.size(), cudaMemcpyDeviceToHost));
+    for (const HitRec &h : hv) if (!dropped[h.gid]) out.push_back(h);
+    return MSP_OK;
+  };
+  // Sync point: deadline, hit-list capacity and (first mode) early recovery.
+  auto checkpoint = [&](bool &stop_now) -> int {
+    unsigned long long nh = 0;
+    CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
+    if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
+    if (opt->mode == MSP_MODE_FIRST && nh > hits_done) {
+      std::vector<HitRec> hv;
+      int r2 = fetch_hits(hits_done, nh, hv);
+      if (r2) return r2;
+      r2 = recover(hv);
+      if (r2) return r2;
+      hits_done = nh;
+      if (!sols.empty()) stop_now = true;
     }
-    if (wi % sync_every == sync_every - 1 || wi + 1 == waves.size()) {
-      unsigned long long nh = 0;
-      CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      CK(cudaGetLastError());
-      if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
-      if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
-      if (opt->mode == MSP_MODE_FIRST && nh > hits_done) {
-        rc = recover(hits_done, nh);
-        if (rc) return rc;
-        hits_done = nh;
-        if (!sols.empty()) { S.waves = (int32_t)(wi + 1); stopped_early = true; break; }
+    return MSP_OK;
+  };
+  const bool periodic = deadline || opt->mode == MSP_MODE_FIRST;
+
+  // ---- classify batches: partitioned shared-memory join (default) or global-table join
+  const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : (10ull << 20);
+  std::vector<uint32_t> part_b, global_b;
+  for (uint32_t g = 0; g < P.G; ++g) {
+    const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
+    const uint64_t nbk = 1ull << pow2ceil((nb + kBucketTarget - 1) / kBucketTarget);
+    if ((opt->flags & MSP_FLAG_JOIN_GLOBAL) || nbk > (uint64_t)kMaxWaveBuckets || nb + np > key_budget)
+      global_b.push_back(g);
+    else
+      part_b.push_back(g);
+  }
+
+  // ---- partitioned waves
+  {
+    struct PWave { size_t u0, u1, b0, nb; uint64_t tiles, scratch, pairs; };
+    std::vector<PWave> pw;
+    std::vector<UnitDesc> units;
+    std::vector<uint32_t> bstart[2], bcap[2], bgid;
+    PWave cur{0, 0, 0, 0, 0, 0, 0};
+    uint64_t cur_keys = 0;
+    auto flush = [&]() {
+      if (cur.nb == 0) return;
+      cur.u1 = units.size();
+      pw.push_back(cur);
+      cur = PWave{units.size(), units.size(), bgid.size(), 0, 0, 0, 0};
+      cur_keys = 0;
+    };
+    for (uint32_t g : part_b) {
+      const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
+      const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
+      const uint32_t bits = pow2ceil((nb + kBucketTarget - 1) / kBucketTarget);
+      const uint32_t NB = 1u << bits;
+      if (cur.nb + NB > (uint32_t)kMaxWaveBuckets || cur_keys + nb + np > key_budget) flush();
+      const double mb = (double)nb / NB, mp = (double)np / NB;
+      const uint32_t cb = (uint32_t)(mb + 7.0 * std::sqrt(mb) + 16), cp = (uint32_t)(mp + 7.0 * std::sqrt(mp) + 16);
+      for (uint32_t k = 0; k < NB; ++k) {
+        bstart[0].push_back((uint32_t)cur.scratch); bcap[0].push_back(cb); cur.scratch += cb;
+        bstart[1].push_back((uint32_t)cur.scratch); bcap[1].push_back(cp); cur.scratch += cp;
+        bgid.push_back(g);
+      }
+      for (int side = 0; side < 2; ++side) {
+        UnitDesc u = make_unit(P, g, side, cur.tiles);
+        u.region_base = cur.nb;
+        u.region_log2 = bits;
+        u.flags = (side == bside ? 0u : 1u) << 1;  // role: 0 build, 1 probe
+        u.count_filter = side == 1;
+        cur.tiles += P.tiles[2 * g + side];
+        units.push_back(u);
+      }
+      cur.nb += NB;
+      cur.pairs += P.nl[g] + P.nr[g];
+      cur_keys += nb + np;
+    }
+    flush();
+    S.waves += (int32_t)pw.size();
+    if (!pw.empty()) {
+      uint64_t max_scratch = 0;
+      for (const PWave &w : pw) max_scratch = std::max(max_scratch, w.scratch);
+      const size_t nbt = bgid.size();
+      CK(D.scratch.ensure(8 * max_scratch));
+      CK(D.units.ensure(sizeof(UnitDesc) * units.size()));
+      CK(D.bk.ensure(4 * 5 * nbt));
+      CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
+      CK(cudaMemsetAsync(D.fill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+      std::vector<uint32_t> bkimg;
+      bkimg.reserve(5 * nbt);
+      for (auto *v : {&bstart[0], &bstart[1], &bcap[0], &bcap[1], &bgid}) bkimg.insert(bkimg.end(), v->begin(), v->end());
+      CK(cudaMemcpyAsync(D.bk.p, bkimg.data(), 4 * bkimg.size(), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(D.units.p, units.data(), sizeof(UnitDesc) * units.size(), cudaMemcpyHostToDevice, st));
+      const uint32_t *bkd = D.bk.as<uint32_t>();
+      PartArgs pa{};
+      pa.scratch = D.scratch.as<unsigned long long>();
+      pa.fill[0] = D.fill.as<uint32_t>();
+      pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
+      pa.batch_ovf = D.bovf.as<unsigned int>();
+      pa.hits = D.hits.as<HitRec>();
+      pa.nhits = D.nhits.as<unsigned long long>();
+      pa.hit_cap = hit_cap;
+      pa.batch_hits = D.bhits.as<unsigned long long>();
+      for (size_t wi = 0; wi < pw.size(); ++wi) {
+        const PWave &w = pw[wi];
+        pa.start[0] = bkd + w.b0;
+        pa.start[1] = bkd + nbt + w.b0;
+        pa.cap[0] = bkd + 2 * nbt + w.b0;
+        pa.cap[1] = bkd + 3 * nbt + w.b0;
+        pa.gid = bkd + 4 * nbt + w.b0;
+        pa.nb = (uint32_t)w.nb;
+        set_enum_range(A, D.units.as<UnitDesc>() + w.u0, w.u1 - w.u0, w.tiles, D.num_sms);
+        // the scatter CTA walks 4 warps x chunk_tiles tiles per work item
+        A.chunk_tiles = std::max<uint64_t>(1, std::min<uint64_t>(256, w.tiles / ((uint64_t)D.num_sms * kScatterWarpsHost * 3)));
+        A.nchunks = (w.tiles + kScatterWarpsHost * A.chunk_tiles - 1) / (kScatterWarpsHost * A.chunk_tiles);
+        if (profile) CK(cudaEventRecord(D.pev[0], st));
+        CK(launch_scatter(P.mc, A, pa, D.num_sms, st));
+        CK(launch_join(pa, D.num_sms, st));
+        S.kernel_launches += 2;
+        if (profile) {
+          CK(cudaEventRecord(D.pev[1], st));
+          CK(cudaEventSynchronize(D.pev[1]));
+          hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
+          S.hot_launches += 2;
+          S.hot_pairs += (int64_t)w.pairs;
+        }
+        if (periodic && (wi % 16 == 15 || wi + 1 == pw.size())) {
+          bool stop_now = false;
+          rc = checkpoint(stop_now);
+          if (rc) return rc;
+          if (stop_now) { stopped = true; break; }
+        }
       }
     }
   }
+
+  // ---- overflowed partitioned batches are re-joined with the global table
+  unsigned long long n_v2_hits = 0;
+  if (!stopped && !part_b.empty()) {
+    std::vector<uint32_t> ovf(P.G);
+    CK(cudaMemcpyAsync(ovf.data(), D.bovf.p, 4 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&n_v2_hits, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint32_t g = 0; g < P.G; ++g) {
+      if (!ovf[g]) continue;
+      dropped[g] = 1;
+      global_b.push_back(g);
+      CK(cudaMemsetAsync(D.bfilt.as<unsigned long long>() + g, 0, 8, st));
+      CK(cudaMemsetAsync(D.bhits.as<unsigned long long>() + g, 0, 8, st));
+    }
+    std::sort(global_b.begin(), global_b.end());
+  }
+
+  // ---- global-table waves (huge batches by hash-range passes; overflow fallback)
+  if (!stopped && !global_b.empty()) {
+    const uint64_t slot_budget = opt->wave_keys ? std::max<uint64_t>(1024, 2 * opt->wave_keys) : (1ull << 23);
+    std::vector<UnitDesc> units;
+    std::vector<Wave> waves;
+    Wave cur;
+    uint64_t tb_build = 0, tb_probe = 0;
+    std::vector<UnitDesc> pend_build, pend_probe;
+    auto flush = [&]() {
+      if (pend_build.empty()) return;
+      cur.ub0 = units.size();
+      units.insert(units.end(), pend_build.begin(), pend_build.end());
+      cur.ub1 = units.size();
+      cur.up0 = units.size();
+      units.insert(units.end(), pend_probe.begin(), pend_probe.end());
+      cur.up1 = units.size();
+      cur.build_tiles = tb_build;
+      cur.probe_tiles = tb_probe;
+      waves.push_back(cur);
+      cur = Wave();
+      pend_build.clear();
+      pend_probe.clear();
+      tb_build = tb_probe = 0;
+    };
+    for (uint32_t g : global_b) {
+      const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
+      const uint64_t nb = bside ? P.nr[g] : P.nl[g];
+      const uint64_t need = 1ull << std::max<uint32_t>(6, pow2ceil(2 * nb));
+      uint32_t npass = 1;
+      uint64_t cap = need;
+      if (need > slot_budget) {
+        npass = (uint32_t)((2 * nb + slot_budget - 1) / slot_budget);
+        do {
+          ++npass;
+          cap = 1ull << std::max<uint32_t>(6, pow2ceil((uint64_t)(2.2 * (double)nb / npass) + 64));
+        } while (cap > slot_budget);
+        flush();
+      }
+      for (uint32_t p = 0; p < npass; ++p) {
+        if (npass == 1 && cur.slots + cap > slot_budget) flush();
+        UnitDesc ub = make_unit(P, g, bside, tb_build);
+        UnitDesc up = make_unit(P, g, 1 - bside, tb_probe);
+        for (UnitDesc *u : {&ub, &up}) {
+          u->slot = cur.nslot;
+          u->region_base = (uint32_t)cur.slots;
+          u->region_log2 = pow2ceil(cap);
+          u->pass = p;
+          u->npass = npass;
+          u->count_filter = (u->side == 1 && p == 0);
+        }
+        tb_build += P.tiles[2 * g + bside];
+        tb_probe += P.tiles[2 * g + 1 - bside];
+        cur.pairs += P.nl[g] + P.nr[g];
+        pend_build.push_back(ub);
+        pend_probe.push_back(up);
+        cur.slots += cap;
+        cur.nslot++;
+        if (npass > 1) flush();
+      }
+    }
+    flush();
+    S.waves += (int32_t)waves.size();
+    uint32_t max_nslot = 1;
+    uint64_t max_slots = 64;
+    for (const Wave &w : waves) { max_nslot = std::max(max_nslot, w.nslot); max_slots = std::max(max_slots, w.slots); }
+    CK(D.units.ensure(sizeof(UnitDesc) * std::max<size_t>(1, units.size())));
+    CK(D.keys.ensure(8 * max_slots));
+    CK(D.cnt.ensure(8 * max_slots));
+    CK(D.zero.ensure(8 * max_nslot));
+    CK(D.zhit.ensure(4 * max_nslot));
+    CK(cudaMemcpyAsync(D.units.p, units.data(), sizeof(UnitDesc) * units.size(), cudaMemcpyHostToDevice, st));
+    jt.keys = D.keys.as<unsigned long long>();
+    jt.cnt = D.cnt.as<unsigned long long>();
+    jt.zero = D.zero.as<unsigned long long>();
+    jt.zero_hit = D.zhit.as<unsigned int>();
+    const UnitDesc *udev = D.units.as<UnitDesc>();
+    for (size_t wi = 0; wi < waves.size(); ++wi) {
+      const Wave &w = waves[wi];
+      CK(cudaMemsetAsync(D.keys.p, 0, 8 * w.slots, st));
+      CK(cudaMemsetAsync(D.cnt.p, 0, 8 * w.slots, st));
+      CK(cudaMemsetAsync(D.zero.p, 0, 8 * w.nslot, st));
+      CK(cudaMemsetAsync(D.zhit.p, 0, 4 * w.nslot, st));
+      if (profile) CK(cudaEventRecord(D.pev[0], st));
+      set_enum_range(A, udev + w.ub0, w.ub1 - w.ub0, w.build_tiles, D.num_sms);
+      if (launch_enum(P.mc, SINK_BUILD, A, jt, D.num_sms, st)) { set_err("unsupported m"); return MSP_INTERNAL; }
+      set_enum_range(A, udev + w.up0, w.up1 - w.up0, w.probe_tiles, D.num_sms);
+      launch_enum(P.mc, SINK_PROBE, A, jt, D.num_sms, st);
+      S.kernel_launches += 2;
+      if (profile) {
+        CK(cudaEventRecord(D.pev[1], st));
+        CK(cudaEventSynchronize(D.pev[1]));
+        hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
+        S.hot_launches += 2;
+        S.hot_pairs += (int64_t)w.pairs;
+      }
+      if (periodic && (wi % 16 == 15 || wi + 1 == waves.size())) {
+        bool stop_now = false;
+        rc = checkpoint(stop_now);
+        if (rc) return rc;
+        if (stop_now) { stopped = true; break; }
+      }
+    }
+  }
+
+  // ---- totals
   CK(cudaEventRecord(D.ev[2], st));
-  std::vector<unsigned long long> uf(units.size()), uh(units.size());
+  std::vector<unsigned long long> bf(P.G), bh(P.G);
   unsigned long long nh = 0;
   int err = 0;
-  if (!units.empty()) {
-    CK(cudaMemcpyAsync(uf.data(), D.ufilt.p, 8 * units.size(), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(uh.data(), D.uhits.p, 8 * units.size(), cudaMemcpyDeviceToHost, st));
+  if (P.G) {
+    CK(cudaMemcpyAsync(bf.data(), D.bfilt.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(bh.data(), D.bhits.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
@@ -743,11 +904,22 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   S.dev_ms_join = elapsed_ms(D.ev[1], D.ev[2]);
   S.dev_ms_hot = hot_ms;
   if (err) { set_err("join table region overflow (err=%d)", err); return MSP_INTERNAL; }
-  for (size_t i = 0; i < units.size(); ++i) { S.filtered_residuals += (int64_t)uf[i]; S.hash_hits += (int64_t)uh[i]; }
+  for (uint32_t g = 0; g < P.G; ++g) { S.filtered_residuals += (int64_t)bf[g]; S.hash_hits += (int64_t)bh[g]; }
   if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
   if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
-  if (!stopped_early) {
-    rc = recover(hits_done, nh);
+  if (!stopped) {
+    // hits recorded by the partitioned join of dropped batches are superseded by their re-join
+    std::vector<HitRec> hv;
+    rc = fetch_hits(hits_done, n_v2_hits > hits_done ? n_v2_hits : hits_done, hv);
+    if (rc) return rc;
+    std::vector<HitRec> tail(0);
+    if (nh > std::max<uint64_t>(hits_done, n_v2_hits)) {
+      const uint64_t from = std::max<uint64_t>(hits_done, n_v2_hits);
+      std::vector<HitRec> t2(nh - from);
+      CK(cudaMemcpy(t2.data(), D.hits.as<HitRec>() + from, sizeof(HitRec) * t2.size(), cudaMemcpyDeviceToHost));
+      hv.insert(hv.end(), t2.begin(), t2.end());
+    }
+    rc = recover(hv);
     if (rc) return rc;
     if (opt->mode == MSP_MODE_ALL && recovered_hh != S.hash_hits) {
       set_err("internal error: recovered hash hits %lld != join hash hits %lld", (long long)recovered_hh,

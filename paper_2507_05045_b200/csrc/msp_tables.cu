@@ -171,39 +171,60 @@ __global__ void k_groups(GroupArgs g) {
   if (threadIdx.x == 0) *g.count = base;
 }
 
-// Per (batch, side): exclusive prefix over Y runs of the warp-tile counts of each rectangle.
-__global__ void k_tile_prefix(PrefixArgs p) {
+// Per (batch, side): the nonempty rectangles X-run(xw_total - w) x Y-run(w) over the Y runs w,
+// oriented for the warp tile (longer run across lanes) with their warp-tile offsets.  Count mode
+// (rects == nullptr) only produces the per-(batch, side) tile and rectangle totals the host needs
+// to plan waves; write mode fills the compacted rectangle list at rect_base[2g + side].
+__global__ void k_rects(RectArgs p) {
   const uint32_t g = blockIdx.x;
   if (g >= *p.count) return;
   const int side = blockIdx.y;
-  const PrefixSide s = p.s[side];
+  const RectSide s = p.s[side];
   const uint32_t ny = *s.ny;
   const uint64_t xw_total = side == 0 ? p.alpha[g] : p.target - p.alpha[g];
-  uint32_t *out = p.prefix + s.off + (size_t)g * s.stride;
-  uint64_t base = 0;
+  const bool write = p.rects != nullptr;
+  RectDesc *out = write ? p.rects + p.rect_base[(size_t)g * 2 + side] : nullptr;
+  uint64_t tbase = 0;
+  uint32_t rbase = 0;
   for (uint32_t r0 = 0; r0 < ny; r0 += blockDim.x) {
     const uint32_t r = r0 + threadIdx.x;
-    uint32_t tiles = 0;
+    uint32_t tiles = 0, xs = 0, xl = 0, ys = 0, yl = 0;
     if (r < ny) {
       const uint32_t wy = s.yw[r];
       if (wy <= xw_total && xw_total - wy <= s.SX) {
         const uint32_t wx = (uint32_t)(xw_total - wy);
-        const uint32_t xl = s.x_end[wx] - s.x_start[wx], yl = s.ylen[r];
+        xs = s.x_start[wx];
+        xl = s.x_end[wx] - xs;
+        ys = s.ys[r];
+        yl = s.ylen[r];
         if (xl) {
           const uint32_t L = xl > yl ? xl : yl, Q = xl > yl ? yl : xl;
           tiles = ((L + 31) / 32) * ((Q + kTQ - 1) / kTQ);
         }
       }
     }
-    uint32_t tot;
-    const uint32_t pos = block_excl_scan(tiles, tot);
-    if (r < ny) out[r] = (uint32_t)(base + pos);
-    base += tot;
+    uint32_t ttot, rtot;
+    const uint32_t tpos = block_excl_scan(tiles, ttot);
+    const uint32_t rpos = block_excl_scan(tiles > 0, rtot);
+    if (write && tiles) {
+      RectDesc R;
+      R.lane_is_x = xl >= yl;
+      R.lane_start = R.lane_is_x ? xs : ys;
+      R.loop_start = R.lane_is_x ? ys : xs;
+      R.L = R.lane_is_x ? xl : yl;
+      R.Q = R.lane_is_x ? yl : xl;
+      R.tile_off = (uint32_t)(tbase + tpos);
+      R.nl = (R.L + 31) / 32;
+      R.nq = (R.Q + kTQ - 1) / kTQ;
+      out[rbase + rpos] = R;
+    }
+    tbase += ttot;
+    rbase += rtot;
   }
-  if (threadIdx.x == 0) {
-    out[ny] = (uint32_t)base;
-    p.tiles[(size_t)g * 2 + side] = base;
-    if (base > 0xFFFFFFFFull) atomicOr(p.err, 2);
+  if (!write && threadIdx.x == 0) {
+    p.tiles[(size_t)g * 2 + side] = tbase;
+    p.nrect[(size_t)g * 2 + side] = rbase;
+    if (tbase > 0xFFFFFFFFull) atomicOr(p.err, 2);
   }
 }
 
@@ -251,8 +272,8 @@ void launch_conv(const ConvArgs &a, uint32_t vmax, cudaStream_t st) {
   k_conv<<<dim3(blocks, 2), 256, 0, st>>>(a);
 }
 void launch_groups(const GroupArgs &a, cudaStream_t st) { k_groups<<<1, 1024, 0, st>>>(a); }
-void launch_tile_prefix(const PrefixArgs &a, uint32_t max_groups, cudaStream_t st) {
-  if (max_groups) k_tile_prefix<<<dim3(max_groups, 2), 256, 0, st>>>(a);
+void launch_rects(const RectArgs &a, uint32_t max_groups, cudaStream_t st) {
+  if (max_groups) k_rects<<<dim3(max_groups, 2), 256, 0, st>>>(a);
 }
 void launch_brute(const BruteArgs &a, cudaStream_t st) {
   const uint64_t total = 1ull << a.n;

@@ -145,6 +145,20 @@ def test_small_waves_force_multi_pass_join():
     assert tiny.stats.waves > ref.stats.waves
 
 
+def test_global_table_join_path_matches():
+    """The fallback global-hash-table join gives identical results to the partitioned join."""
+    for (m, s) in ((4, 11), (5, 1), (6, 4)):
+        inst = msb.generate_instance(m, 100, s)
+        ref = _solve_all(inst)
+        opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_JOIN_GLOBAL)
+        rc, xb, st = _native.solve_raw(inst.a, inst.d, opts)
+        assert rc == 0, _native.last_error()
+        got = sorted((tuple(int(v) for v in r) for r in xb), key=msb.solution_encoding)
+        assert got == ref.solutions
+        for k in STAT_KEYS:
+            assert st[k] == getattr(ref.stats, k), k
+
+
 def test_first_mode():
     for (m, s) in ((4, 11), (5, 1), (6, 4)):
         inst = msb.generate_instance(m, 100, s)
