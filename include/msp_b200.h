@@ -109,6 +109,10 @@ int msp_join_alpha(const msp_problem *prob, const msp_options *opt, uint64_t alp
 /* INT32 ops/s of the FNV fold instruction mix on `device` (roofline denominator), or < 0 on error. */
 double msp_int32_peak(int32_t device);
 
+/* sizeof(msp_problem), sizeof(msp_options), sizeof(msp_stats), sizeof(msp_result) -> out[0..3]
+ * (lets bindings check their struct mirrors without a GPU). */
+void msp_abi_sizes(int32_t *out);
+
 /* Free the cached per-device workspace. */
 void msp_release(int32_t device);
 const char *msp_last_error(void);

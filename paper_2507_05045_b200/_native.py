@@ -35,7 +35,7 @@ NVCC_FLAGS = [
 
 EXPORTED_SYMBOLS = (
     "msp_solve", "msp_result_free", "msp_build_tables", "msp_alpha_plan", "msp_join_alpha",
-    "msp_release", "msp_last_error", "msp_version", "msp_int32_peak",
+    "msp_release", "msp_last_error", "msp_version", "msp_int32_peak", "msp_abi_sizes",
 )
 
 
@@ -139,6 +139,8 @@ def load(path: str | None = None):
     L.msp_version.restype = C.c_int32
     L.msp_int32_peak.restype = C.c_double
     L.msp_int32_peak.argtypes = [C.c_int32]
+    L.msp_abi_sizes.restype = None
+    L.msp_abi_sizes.argtypes = [C.POINTER(C.c_int32)]
     _lib = L
     return L
 

@@ -1041,6 +1041,12 @@ void msp_release(int32_t device) {
 }
 
 const char *msp_last_error(void) { return msp::g_err.c_str(); }
+void msp_abi_sizes(int32_t *out) {
+  out[0] = (int32_t)sizeof(msp_problem);
+  out[1] = (int32_t)sizeof(msp_options);
+  out[2] = (int32_t)sizeof(msp_stats);
+  out[3] = (int32_t)sizeof(msp_result);
+}
 int32_t msp_version(void) { return 1; }
 
 }  // extern "C"
