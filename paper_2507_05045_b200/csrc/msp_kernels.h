@@ -77,7 +77,7 @@ void launch_rects(const RectArgs &a, uint32_t max_groups, cudaStream_t st);
 void launch_brute(const BruteArgs &a, cudaStream_t st);
 
 // Partitioned join (msp_part.cu).  Buckets of one wave, per role (0 = build, 1 = probe).
-constexpr int kMaxWaveBuckets = 512;   // buckets per role per wave
+constexpr int kMaxWaveBuckets = 1024;  // buckets per role per wave
 constexpr int kScatterWarpsHost = 16;  // warps per k_scatter CTA (must match msp_part.cu)
 constexpr int kJoinSlotsLog2 = 14;     // shared-memory join table: 16K (key, count) slots
 constexpr uint32_t kBucketTarget = 1u << (kJoinSlotsLog2 - 1);  // mean build keys per bucket
@@ -93,6 +93,17 @@ struct PartArgs {
   unsigned long long *batch_hits;
 };
 cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int num_sms, cudaStream_t st);
+// Huge batches, level 2: re-partition coarse bucket regions (already hashed keys) into fine buckets.
+struct RescatterSrc {
+  const unsigned long long *keys;  // coarse bucket region
+  const uint32_t *fill;            // keys written into it (device counter)
+  uint32_t cap, role;              // region capacity; 0 build, 1 probe
+  uint32_t fine_base, fbits;       // first fine bucket (per role) and fine bits of this source
+  uint32_t coarse_bits, pad;       // key bits already consumed by the coarse level
+  uint64_t in_base;                // first input slot of this source
+};
+struct RescatterArgs { const RescatterSrc *src; uint32_t nsrc; uint64_t total; };
+cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st);
 cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 
 enum SinkKind { SINK_BUILD = 0, SINK_PROBE = 1, SINK_RECOVER = 2 };

@@ -27,39 +27,135 @@ constexpr int kScatterWarps = 16;
 constexpr int kWarpStage = 512;                         // keys a warp stages per round
 constexpr int kStage = kScatterWarps * kWarpStage;      // keys staged per CTA round
 constexpr uint32_t kOvf = 0x80000000u;
+constexpr int kHistEntries = 2 * kMaxWaveBuckets;       // (role, bucket)
 
 size_t scatter_smem_bytes() {
-  return (size_t)kStage * (8 + 8 + 2 + 2 + 2) + (size_t)2 * kMaxWaveBuckets * 4 * 3 + 64;
+  return (size_t)kStage * (8 + 8 + 2 + 2 + 2) + (size_t)kHistEntries * 4 * 3 + 64;
+}
+
+// Shared-memory views of one CTA's staging area.
+struct Stage {
+  unsigned long long *skey, *sorted;
+  uint16_t *sbkt, *rank, *sortb;
+  uint32_t *hist, *off, *abase;
+  uint8_t *ovf;
+  uint32_t *warp_tot;
+};
+
+__device__ __forceinline__ Stage stage_views(unsigned char *smem, uint8_t *ovf, uint32_t *warp_tot) {
+  Stage g;
+  g.skey = reinterpret_cast<unsigned long long *>(smem);
+  g.sorted = g.skey + kStage;
+  g.sbkt = reinterpret_cast<uint16_t *>(g.sorted + kStage);
+  g.rank = g.sbkt + kStage;
+  g.sortb = g.rank + kStage;
+  g.hist = reinterpret_cast<uint32_t *>(g.sortb + kStage);
+  g.off = g.hist + kHistEntries;
+  g.abase = g.off + kHistEntries;
+  g.ovf = ovf;
+  g.warp_tot = warp_tot;
+  return g;
+}
+
+// Append one warp-step of keys densely to the warp's stage (ballot + popc) and rank each key
+// within its (role, bucket) with one shared-memory atomic.
+__device__ __forceinline__ void stage_key(const Stage &g, uint32_t warp, uint32_t lane_lt, uint32_t &cnt,
+                                          uint64_t key, uint32_t b, bool ok) {
+  const uint32_t m = __ballot_sync(0xffffffffu, ok);
+  if (ok) {
+    const uint32_t pos = warp * kWarpStage + cnt + __popc(m & lane_lt);
+    g.skey[pos] = key;
+    g.sbkt[pos] = (uint16_t)b;
+    g.rank[pos] = (uint16_t)atomicAdd(g.hist + b, 1u);
+  }
+  cnt += __popc(m);
+}
+
+// After a __syncthreads: scan the round's bucket counts, reserve one global range per nonempty
+// bucket (the thread's kPer reservations are independent atomics issued back to back), reorder the
+// staged keys into bucket-sorted runs and write the runs out coalesced.  Ends synchronised, with
+// the histogram zeroed for the next round.
+__device__ __forceinline__ void flush_round(const Stage &g, const PartArgs &S, uint32_t cnt) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nbw = S.nb, nent = 2 * nbw;
+  constexpr int kPer = kHistEntries / (kScatterWarps * 32);
+  const uint32_t j0 = tid * kPer;
+  uint32_t hv[kPer], local = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    hv[k] = j0 + k < nent ? g.hist[j0 + k] : 0u;
+    g.hist[j0 + k] = 0u;  // ready for the next fill
+    local += hv[k];
+  }
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  if (lane == 31) g.warp_tot[warp] = incl;
+  uint32_t gres[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t j = j0 + k, role = j >= nbw;
+    gres[k] = hv[k] ? atomicAdd((role ? S.fill[1] : S.fill[0]) + (j - role * nbw), hv[k]) : 0u;
+  }
+  __syncthreads();
+  uint32_t run = incl - local;
+  for (uint32_t w = 0; w < warp; ++w) run += g.warp_tot[w];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t j = j0 + k;
+    if (j < nent) {
+      g.off[j] = run;
+      g.ovf[j] = 0;
+      if (hv[k]) {
+        const uint32_t role = j >= nbw, b = j - role * nbw;
+        if (gres[k] + hv[k] > __ldg((role ? S.cap[1] : S.cap[0]) + b)) {
+          g.ovf[j] = 1;
+          atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+        } else {
+          g.abase[j] = __ldg((role ? S.start[1] : S.start[0]) + b) + gres[k] - run;
+        }
+      }
+    }
+    run += hv[k];
+  }
+  uint32_t total = 0;
+  for (int w = 0; w < kScatterWarps; ++w) total += g.warp_tot[w];
+  __syncthreads();
+  for (uint32_t j = lane; j < cnt; j += 32) {  // each warp reorders its own staged keys
+    const uint32_t i = warp * kWarpStage + j;
+    const uint16_t b = g.sbkt[i];
+    const uint32_t pos = g.off[b] + g.rank[i];
+    g.sorted[pos] = g.skey[i];
+    g.sortb[pos] = b;
+  }
+  __syncthreads();
+  for (uint32_t pos = tid; pos < total; pos += blockDim.x) {
+    const uint16_t b = g.sortb[pos];
+    if (!g.ovf[b]) S.scratch[g.abase[b] + pos] = g.sorted[pos];
+  }
+  __syncthreads();
 }
 
 template <int MC>
 __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A, const PartArgs S) {
   constexpr int NW = words_for(MC);
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long *skey = reinterpret_cast<unsigned long long *>(smem);
-  unsigned long long *sorted = skey + kStage;
-  uint16_t *sbkt = reinterpret_cast<uint16_t *>(sorted + kStage);
-  uint16_t *rank = sbkt + kStage;
-  uint16_t *sortb = rank + kStage;
-  uint32_t *hist = reinterpret_cast<uint32_t *>(sortb + kStage);
-  uint32_t *off = hist + 2 * kMaxWaveBuckets;
-  uint32_t *abase = off + 2 * kMaxWaveBuckets;
   __shared__ uint32_t warp_tot[kScatterWarps];
-  __shared__ uint8_t ovf[2 * kMaxWaveBuckets];
-  __shared__ __align__(16) uint32_t ybuf_all[kScatterWarps][kTQ * 8];
+  __shared__ uint8_t ovf[kHistEntries];
+  __shared__ __align__(16) uint32_t ybuf_all[kScatterWarps][kTQ * stride_for(MC)];
+  const Stage g = stage_views(smem, ovf, warp_tot);
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const uint32_t nbw = S.nb;             // buckets per role in this wave
-  const uint32_t nent = 2 * nbw;         // (role, bucket) histogram entries
+  const uint32_t nbw = S.nb;
   uint32_t dg[NW > 0 ? NW : 1];
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
-  for (uint32_t i = tid; i < 2 * kMaxWaveBuckets; i += blockDim.x) hist[i] = 0;
+  for (uint32_t i = tid; i < kHistEntries; i += blockDim.x) g.hist[i] = 0;
   __syncthreads();
-  unsigned long long *mykey = skey + warp * kWarpStage;
-  uint16_t *mybk = sbkt + warp * kWarpStage;
-  uint16_t *myrank = rank + warp * kWarpStage;
 
   for (uint64_t chunk = blockIdx.x; chunk < A.nchunks; chunk += gridDim.x) {
     const uint64_t wT = (chunk * kScatterWarps + warp) * A.chunk_tiles;
@@ -71,22 +167,12 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A
     if (have) begin_tile<MC>(A, W, lane, C);
     unsigned long long filt = 0;
     while (true) {
-      // ---- fill: append valid keys densely (ballot + popc) and rank them within their bucket,
-      //      until the warp's stage is full
       uint32_t cnt = 0;
       while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
         const uint32_t bbase = ((W.d.flags >> 1) & 1u) * nbw + W.d.region_base;
         const uint32_t bits = W.d.region_log2;
         step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
-          const uint32_t m = __ballot_sync(0xffffffffu, ok);
-          if (ok) {
-            const uint32_t pos = cnt + __popc(m & lt_mask);
-            const uint32_t b = bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u);
-            mykey[pos] = key;
-            mybk[pos] = (uint16_t)b;
-            myrank[pos] = (uint16_t)atomicAdd(hist + b, 1u);
-          }
-          cnt += __popc(m);
+          stage_key(g, warp, lt_mask, cnt, key, bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u), ok);
         });
         if (C.q >= C.q1) {
           uint32_t old;
@@ -100,71 +186,52 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A
         }
       }
       if (!__syncthreads_or(cnt > 0)) break;
-      // ---- exclusive scan over (role, bucket) counts + one global reservation per bucket; the
-      //      thread's kPer reservations are independent atomics issued back to back
-      constexpr int kPer = 2 * kMaxWaveBuckets / (kScatterWarps * 32);
-      const uint32_t j0 = tid * kPer;
-      uint32_t hv[kPer], local = 0;
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        hv[k] = j0 + k < nent ? hist[j0 + k] : 0u;
-        hist[j0 + k] = 0u;  // ready for the next fill
-        local += hv[k];
-      }
-      uint32_t incl = local;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-      }
-      if (lane == 31) warp_tot[warp] = incl;
-      uint32_t gres[kPer];
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const uint32_t j = j0 + k, role = j >= nbw;
-        gres[k] = hv[k] ? atomicAdd((role ? S.fill[1] : S.fill[0]) + (j - role * nbw), hv[k]) : 0u;
-      }
-      __syncthreads();
-      uint32_t run = incl - local;
-      for (uint32_t w = 0; w < warp; ++w) run += warp_tot[w];
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const uint32_t j = j0 + k;
-        if (j < nent) {
-          off[j] = run;
-          ovf[j] = 0;
-          if (hv[k]) {
-            const uint32_t role = j >= nbw, b = j - role * nbw;
-            if (gres[k] + hv[k] > __ldg((role ? S.cap[1] : S.cap[0]) + b)) {
-              ovf[j] = 1;
-              atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
-            } else {
-              abase[j] = __ldg((role ? S.start[1] : S.start[0]) + b) + gres[k] - run;
-            }
-          }
-        }
-        run += hv[k];
-      }
-      uint32_t total = 0;
-      for (int w = 0; w < kScatterWarps; ++w) total += warp_tot[w];
-      __syncthreads();
-      // ---- reorder into bucket-sorted runs (each warp its own staged keys)
-      for (uint32_t j = lane; j < cnt; j += 32) {
-        const uint16_t b = mybk[j];
-        const uint32_t pos = off[b] + myrank[j];
-        sorted[pos] = mykey[j];
-        sortb[pos] = b;
-      }
-      __syncthreads();
-      // ---- coalesced write-out of the runs
-      for (uint32_t pos = tid; pos < total; pos += blockDim.x) {
-        const uint16_t b = sortb[pos];
-        if (!ovf[b]) S.scratch[abase[b] + pos] = sorted[pos];
-      }
-      __syncthreads();
+      flush_round(g, S, cnt);
     }
     const unsigned long long f = warp_sum(filt);
     if (lane == 0 && f) atomicAdd(A.batch_filtered + W.d.gid, f);
+  }
+}
+
+// Level 2 of the huge-batch path: stream already-hashed keys back from coarse bucket regions
+// (HBM) and re-partition them into fine buckets (L2 scratch) for k_join.  Each CTA round takes
+// kStage consecutive input slots; slots past a region's fill are empty.
+__global__ void __launch_bounds__(kScatterWarps * 32) k_rescatter(const RescatterArgs R, const PartArgs S) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t warp_tot[kScatterWarps];
+  __shared__ uint8_t ovf[kHistEntries];
+  const Stage g = stage_views(smem, ovf, warp_tot);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint32_t nbw = S.nb;
+  for (uint32_t i = tid; i < kHistEntries; i += blockDim.x) g.hist[i] = 0;
+  __syncthreads();
+  for (uint64_t chunk = blockIdx.x; chunk * kStage < R.total; chunk += gridDim.x) {
+    const uint64_t base = chunk * kStage + (uint64_t)warp * kWarpStage;
+    uint32_t s = 0;
+    {
+      uint32_t lo = 0, hi = R.nsrc;  // last source with in_base <= base
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (R.src[mid].in_base <= base) lo = mid; else hi = mid;
+      }
+      s = lo;
+    }
+    uint32_t cnt = 0;
+#pragma unroll 4
+    for (int k = 0; k < kWarpStage / 32; ++k) {
+      const uint64_t idx = base + (uint64_t)k * 32 + lane;
+      uint32_t sl = s;
+      while (sl + 1 < R.nsrc && idx >= R.src[sl + 1].in_base) ++sl;
+      const RescatterSrc &src = R.src[sl];
+      const uint64_t local = idx - src.in_base;
+      const bool ok = idx < R.total && local < min(*src.fill, src.cap);
+      const uint64_t key = ok ? src.keys[local] : 0ull;
+      const uint32_t fb = src.fbits ? (uint32_t)((key << src.coarse_bits) >> (64 - src.fbits)) : 0u;
+      stage_key(g, warp, lt_mask, cnt, key, src.role * nbw + src.fine_base + fb, ok);
+    }
+    __syncthreads();
+    flush_round(g, S, cnt);
   }
 }
 
@@ -292,6 +359,21 @@ cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int 
 #undef MSP_CASE
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st) {
+  static bool configured = false;
+  const size_t sm = scatter_smem_bytes();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_rescatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const uint64_t chunks = (r.total + kStage - 1) / kStage;
+  if (!chunks) return cudaSuccess;
+  const int grid = (int)(chunks < (uint64_t)num_sms ? chunks : (uint64_t)num_sms);
+  k_rescatter<<<grid, kScatterWarps * 32, sm, st>>>(r, p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st) {

@@ -81,13 +81,15 @@ struct Device {
   DBuf bout, bcnt;
   DBuf rkeys, runits, rfilt, rhits;
   DBuf bfilt, bhits, bovf, scratch, bk, fill;
+  DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
     DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
-                   &bfilt, &bhits, &bovf, &scratch, &bk, &fill};
+                   &bfilt, &bhits, &bovf, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
+                   &cfill, &cbk, &hunits, &l2bk, &l2src};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
                                   comp[i].release(); rs[i].release(); re[i].release(); }
@@ -653,15 +655,18 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     return MSP_OK;
   };
   const bool periodic = deadline || opt->mode == MSP_MODE_FIRST;
+  bool fill_zeroed = false;  // wave fill counters (reset by k_join after each bucket)
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
   const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : (10ull << 20);
-  std::vector<uint32_t> part_b, global_b;
+  std::vector<uint32_t> part_b, huge_b, global_b;
   for (uint32_t g = 0; g < P.G; ++g) {
     const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
     const uint64_t nbk = 1ull << pow2ceil((nb + kBucketTarget - 1) / kBucketTarget);
-    if ((opt->flags & MSP_FLAG_JOIN_GLOBAL) || nbk > (uint64_t)kMaxWaveBuckets || nb + np > key_budget)
+    if (opt->flags & MSP_FLAG_JOIN_GLOBAL)
       global_b.push_back(g);
+    else if (nbk > (uint64_t)kMaxWaveBuckets || nb + np > key_budget)
+      huge_b.push_back(g);
     else
       part_b.push_back(g);
   }
@@ -718,6 +723,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(D.bk.ensure(4 * 5 * nbt));
       CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
       CK(cudaMemsetAsync(D.fill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+      fill_zeroed = true;
       std::vector<uint32_t> bkimg;
       bkimg.reserve(5 * nbt);
       for (auto *v : {&bstart[0], &bstart[1], &bcap[0], &bcap[1], &bgid}) bkimg.insert(bkimg.end(), v->begin(), v->end());
@@ -766,9 +772,164 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
   }
 
+  // ---- huge batches: two-level partitioned join.  Level 1 hashes the batch once and partitions
+  //      each side into <= 1024 coarse buckets in HBM (one k_scatter launch per side, so each
+  //      side's region indices stay 32-bit); level 2 streams coarse buckets back, re-partitions
+  //      them into fine buckets in the L2 scratch and joins them (k_rescatter + k_join).
+  if (!stopped && !huge_b.empty()) {
+    constexpr uint64_t kCoarseTarget = 2ull << 20;  // build keys per coarse bucket
+    CK(D.cfill.ensure(4 * 2 * kMaxWaveBuckets));
+    for (size_t hi_ = 0; hi_ < huge_b.size() && !stopped; ++hi_) {
+      const uint32_t g = huge_b[hi_];
+      const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
+      const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
+      uint32_t cbits = pow2ceil((nb + kCoarseTarget - 1) / kCoarseTarget);
+      cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, 10));
+      const uint32_t NC = 1u << cbits;
+      const double mb = (double)nb / NC, mp = (double)np / NC;
+      const uint64_t cb = (uint64_t)(mb + 7.0 * std::sqrt(mb) + 16), cp = (uint64_t)(mp + 7.0 * std::sqrt(mp) + 16);
+      if (cb * NC > 0xFFFFFFF0ull || cp * NC > 0xFFFFFFF0ull) {
+        set_err("batch side too large for 32-bit coarse regions");
+        return MSP_UNSUPPORTED;
+      }
+      // coarse bucket arrays: start[0] | start[1] | cap[0] | cap[1] | gid
+      std::vector<uint32_t> cbk(5 * (size_t)NC);
+      for (uint32_t c = 0; c < NC; ++c) {
+        cbk[c] = (uint32_t)(c * cb);
+        cbk[NC + c] = (uint32_t)(c * cp);
+        cbk[2 * NC + c] = (uint32_t)cb;
+        cbk[3 * NC + c] = (uint32_t)cp;
+        cbk[4 * NC + c] = g;
+      }
+      CK(D.cscratch[0].ensure(8 * cb * NC));
+      CK(D.cscratch[1].ensure(8 * cp * NC));
+      CK(D.cbk.ensure(4 * cbk.size()));
+      CK(cudaMemcpyAsync(D.cbk.p, cbk.data(), 4 * cbk.size(), cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(D.cfill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+      UnitDesc lu[2];
+      uint64_t ltiles[2];
+      for (int side = 0; side < 2; ++side) {
+        const uint32_t role = side == bside ? 0u : 1u;
+        lu[role] = make_unit(P, g, side, 0);
+        lu[role].region_base = 0;
+        lu[role].region_log2 = cbits;
+        lu[role].flags = role << 1;
+        lu[role].count_filter = side == 1;
+        ltiles[role] = P.tiles[2 * g + side];
+      }
+      CK(D.hunits.ensure(sizeof(UnitDesc) * 2));
+      CK(cudaMemcpyAsync(D.hunits.p, lu, sizeof(UnitDesc) * 2, cudaMemcpyHostToDevice, st));
+      const uint32_t *cbkd = D.cbk.as<uint32_t>();
+      PartArgs c1{};
+      c1.start[0] = cbkd; c1.start[1] = cbkd + NC;
+      c1.cap[0] = cbkd + 2 * NC; c1.cap[1] = cbkd + 3 * NC;
+      c1.gid = cbkd + 4 * NC;
+      c1.fill[0] = D.cfill.as<uint32_t>();
+      c1.fill[1] = D.cfill.as<uint32_t>() + kMaxWaveBuckets;
+      c1.nb = NC;
+      c1.batch_ovf = D.bovf.as<unsigned int>();
+      if (profile) CK(cudaEventRecord(D.pev[0], st));
+      for (int role = 0; role < 2; ++role) {
+        c1.scratch = D.cscratch[role].as<unsigned long long>();
+        set_enum_range(A, D.hunits.as<UnitDesc>() + role, 1, ltiles[role], D.num_sms);
+        A.chunk_tiles = std::max<uint64_t>(1, std::min<uint64_t>(256, ltiles[role] / ((uint64_t)D.num_sms * kScatterWarpsHost * 3)));
+        A.nchunks = (ltiles[role] + kScatterWarpsHost * A.chunk_tiles - 1) / (kScatterWarpsHost * A.chunk_tiles);
+        CK(launch_scatter(P.mc, A, c1, D.num_sms, st));
+        ++S.kernel_launches;
+      }
+      // level 2 waves over the coarse buckets
+      const uint32_t fbits = pow2ceil((uint64_t)std::ceil(mb / kBucketTarget));
+      const uint32_t NF = 1u << fbits;
+      const double fmb = mb / NF, fmp = mp / NF;
+      const uint32_t fcb = (uint32_t)(fmb + 7.0 * std::sqrt(fmb) + 16), fcp = (uint32_t)(fmp + 7.0 * std::sqrt(fmp) + 16);
+      struct L2Wave { size_t s0, ns, b0, nb; uint64_t total, scratch; };
+      std::vector<L2Wave> lw;
+      std::vector<RescatterSrc> srcs;
+      std::vector<uint32_t> fst0, fst1, fcap0, fcap1, fgid;
+      L2Wave cw{0, 0, 0, 0, 0, 0};
+      for (uint32_t c = 0; c < NC; ++c) {
+        if (cw.nb && (cw.nb + NF > (uint32_t)kMaxWaveBuckets || cw.total + cb + cp > key_budget)) {
+          lw.push_back(cw);
+          cw = L2Wave{srcs.size(), 0, fgid.size(), 0, 0, 0};
+        }
+        for (int role = 0; role < 2; ++role) {
+          RescatterSrc r{};
+          r.keys = D.cscratch[role].as<unsigned long long>() + (size_t)c * (role ? cp : cb);
+          r.fill = D.cfill.as<uint32_t>() + role * kMaxWaveBuckets + c;
+          r.cap = (uint32_t)(role ? cp : cb);
+          r.role = role;
+          r.fine_base = (uint32_t)cw.nb;
+          r.fbits = fbits;
+          r.coarse_bits = cbits;
+          r.in_base = cw.total;
+          cw.total += r.cap;
+          srcs.push_back(r);
+          cw.ns++;
+        }
+        for (uint32_t k = 0; k < NF; ++k) {
+          fst0.push_back((uint32_t)cw.scratch); fcap0.push_back(fcb); cw.scratch += fcb;
+          fst1.push_back((uint32_t)cw.scratch); fcap1.push_back(fcp); cw.scratch += fcp;
+          fgid.push_back(g);
+        }
+        cw.nb += NF;
+      }
+      lw.push_back(cw);
+      const size_t nft = fgid.size();
+      uint64_t max_scr = 0;
+      for (const L2Wave &w : lw) max_scr = std::max(max_scr, w.scratch);
+      std::vector<uint32_t> fimg;
+      fimg.reserve(5 * nft);
+      for (auto *v : {&fst0, &fst1, &fcap0, &fcap1, &fgid}) fimg.insert(fimg.end(), v->begin(), v->end());
+      CK(D.scratch.ensure(8 * max_scr));
+      CK(D.l2bk.ensure(4 * fimg.size()));
+      CK(D.l2src.ensure(sizeof(RescatterSrc) * srcs.size()));
+      CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
+      CK(cudaMemcpyAsync(D.l2bk.p, fimg.data(), 4 * fimg.size(), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(D.l2src.p, srcs.data(), sizeof(RescatterSrc) * srcs.size(), cudaMemcpyHostToDevice, st));
+      if (!fill_zeroed) { CK(cudaMemsetAsync(D.fill.p, 0, 4 * 2 * kMaxWaveBuckets, st)); fill_zeroed = true; }
+      const uint32_t *fb = D.l2bk.as<uint32_t>();
+      PartArgs pa{};
+      pa.scratch = D.scratch.as<unsigned long long>();
+      pa.fill[0] = D.fill.as<uint32_t>();
+      pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
+      pa.batch_ovf = D.bovf.as<unsigned int>();
+      pa.hits = D.hits.as<HitRec>();
+      pa.nhits = D.nhits.as<unsigned long long>();
+      pa.hit_cap = hit_cap;
+      pa.batch_hits = D.bhits.as<unsigned long long>();
+      for (size_t wi = 0; wi < lw.size(); ++wi) {
+        const L2Wave &w = lw[wi];
+        pa.start[0] = fb + w.b0;
+        pa.start[1] = fb + nft + w.b0;
+        pa.cap[0] = fb + 2 * nft + w.b0;
+        pa.cap[1] = fb + 3 * nft + w.b0;
+        pa.gid = fb + 4 * nft + w.b0;
+        pa.nb = (uint32_t)w.nb;
+        RescatterArgs ra{D.l2src.as<RescatterSrc>() + w.s0, (uint32_t)w.ns, w.total};
+        CK(launch_rescatter(ra, pa, D.num_sms, st));
+        CK(launch_join(pa, D.num_sms, st));
+        S.kernel_launches += 2;
+      }
+      S.waves += (int32_t)lw.size() + 1;
+      if (profile) {
+        CK(cudaEventRecord(D.pev[1], st));
+        CK(cudaEventSynchronize(D.pev[1]));
+        hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
+        S.hot_launches += 2 + 2 * (int64_t)lw.size();
+        S.hot_pairs += (int64_t)(P.nl[g] + P.nr[g]);
+      }
+      if (periodic) {
+        bool stop_now = false;
+        rc = checkpoint(stop_now);
+        if (rc) return rc;
+        if (stop_now) stopped = true;
+      }
+    }
+  }
+
   // ---- overflowed partitioned batches are re-joined with the global table
   unsigned long long n_v2_hits = 0;
-  if (!stopped && !part_b.empty()) {
+  if (!stopped && (!part_b.empty() || !huge_b.empty())) {
     std::vector<uint32_t> ovf(P.G);
     CK(cudaMemcpyAsync(ovf.data(), D.bovf.p, 4 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&n_v2_hits, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));

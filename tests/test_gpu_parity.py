@@ -145,6 +145,17 @@ def test_small_waves_force_multi_pass_join():
     assert tiny.stats.waves > ref.stats.waves
 
 
+@pytest.mark.parametrize("m,s,wave_keys", [(6, 4, 20000), (6, 1, 60000), (7, 1, 400000)])
+def test_two_level_huge_batch_path(m, s, wave_keys):
+    """A small wave budget routes the big batches through the two-level (coarse HBM + fine L2) join."""
+    inst = msb.generate_instance(m, 100, s)
+    ref = _solve_all(inst)
+    got = _solve_all(inst, wave_keys=wave_keys)
+    assert got.solutions == ref.solutions
+    for k in STAT_KEYS:
+        assert getattr(got.stats, k) == getattr(ref.stats, k), k
+
+
 def test_global_table_join_path_matches():
     """The fallback global-hash-table join gives identical results to the partitioned join."""
     for (m, s) in ((4, 11), (5, 1), (6, 4)):
