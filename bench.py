@@ -186,6 +186,7 @@ def main() -> int:
     ap.add_argument("--ref-frac", type=float, default=0.05, help="CPU sample: fraction of pairs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--wave-keys", type=int, default=0)
+    ap.add_argument("--join", default="auto", choices=("auto", "partitioned", "global"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -221,6 +222,8 @@ def main() -> int:
         lo, hi = band
         if hi != 0 and lo >= hi:
             return [], {"kernel_launches": 0}
+        if args.join == "global":
+            flags |= _native.MSP_FLAG_JOIN_GLOBAL
         return native_solve(inst, "all", None, device=local, alpha_lo=lo, alpha_hi=hi, flags=flags,
                             wave_keys=args.wave_keys, stream=sptr)
 
@@ -252,7 +255,7 @@ def main() -> int:
     value = total_pairs * args.steps / (max_ms * 1e-3)
 
     # ---------------- e2e: the public API from host buffers (H2D instance, D2H solutions) per step
-    cfg = msb.SolverConfig(mode="all", device=local, wave_keys=args.wave_keys)
+    cfg = msb.SolverConfig(mode="all", device=local, wave_keys=args.wave_keys, join=args.join)
     ref_sols = None
     barrier()
     t0 = time.perf_counter()

@@ -45,7 +45,9 @@ enum msp_mode { MSP_MODE_FIRST = 0, MSP_MODE_ALL = 1 };
 enum msp_flags {
   MSP_FLAG_PROFILE = 1u << 0,      /* time the dominant kernel per launch with CUDA events */
   MSP_FLAG_FORCE_TABLE_PATH = 1u << 1, /* never take the n <= brute_force_max_n branch */
-  MSP_FLAG_JOIN_GLOBAL = 1u << 2   /* force the global-hash-table join (fallback path) */
+  MSP_FLAG_JOIN_GLOBAL = 1u << 2,  /* force the global-hash-table join (fallback path) */
+  MSP_FLAG_DIAG_HASH_ONLY = 1u << 3 /* diagnostic timing: global path kernels hash but do not join
+                                       (results invalid; never set in a real solve) */
 };
 
 typedef struct {

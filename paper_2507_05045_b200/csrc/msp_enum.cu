@@ -23,11 +23,19 @@
 namespace msp {
 
 // ---------------------------------------------------------------- sinks (global hash table)
+//
+// The table lives in L2 (<= 8M 64-bit key slots per wave, 64 MB).  Random L2 atomics and loads are
+// throughput-bound only when many are in flight, so a warp step's kU keys are issued as kU
+// independent CAS / loads before any result is inspected; collisions fall to a linear-probe slow
+// path.  Duplicate counts and hit flags live in an epoch-tagged side array that never needs
+// clearing: only the key array is reset per wave.
+
+constexpr unsigned long long kCntMask = (1ull << 39) - 1;
+constexpr unsigned long long kCntFlag = 1ull << 39;
 
 __device__ __forceinline__ bool table_find(const JoinTable &jt, const UnitDesc &d, uint64_t key,
-                                           uint32_t &slot_out) {
+                                           uint32_t s, uint32_t &slot_out) {
   const uint32_t mask = (1u << d.region_log2) - 1;
-  uint32_t s = home_slot(key, d.region_log2);
   const unsigned long long *K = jt.keys + d.region_base;
   for (uint32_t p = 0; p <= mask; ++p) {
     const unsigned long long k = K[s];
@@ -38,63 +46,121 @@ __device__ __forceinline__ bool table_find(const JoinTable &jt, const UnitDesc &
   return false;
 }
 
+__device__ __forceinline__ void count_duplicate(const JoinTable &jt, uint32_t slot) {
+  unsigned long long *c = jt.cnt + slot;
+  unsigned long long old = *c, assumed;
+  do {
+    assumed = old;
+    const unsigned long long nv = (assumed >> 40) == jt.epoch ? assumed + 1 : (jt.epoch << 40) | 1ull;
+    old = atomicCAS(c, assumed, nv);
+  } while (old != assumed);
+}
+
+// hits += multiplicity of the build key in `slot`; the first probe to hit it records (gid, key).
+__device__ __forceinline__ void register_hit(const JoinTable &jt, uint32_t gid, uint32_t slot, uint64_t key,
+                                             unsigned long long &hits) {
+  unsigned long long *c = jt.cnt + slot;
+  unsigned long long cur = *c;
+  const bool valid = (cur >> 40) == jt.epoch;
+  hits += (valid ? (cur & kCntMask) : 0ull) + 1;
+  if (valid && (cur & kCntFlag)) return;
+  unsigned long long assumed;
+  do {
+    assumed = cur;
+    const bool v = (assumed >> 40) == jt.epoch;
+    if (v && (assumed & kCntFlag)) return;  // someone else recorded it
+    const unsigned long long nv = v ? (assumed | kCntFlag) : ((jt.epoch << 40) | kCntFlag);
+    cur = atomicCAS(c, assumed, nv);
+  } while (cur != assumed);
+  const unsigned long long i = atomicAdd(jt.nhits, 1ull);
+  if (i < jt.hit_cap) jt.hits[i] = HitRec{gid, 0u, key};
+}
+
 template <int KIND>
-__device__ __forceinline__ void sink(const JoinTable &jt, const UnitDesc &d, uint64_t key, bool ok,
-                                     const RectDesc &R, uint32_t lidx, uint32_t qidx, const EnumArgs &A,
-                                     unsigned long long &hits) {
-  if (!ok) return;
-  if (d.npass > 1 && pass_of(key, d.npass) != d.pass) return;
+__device__ __forceinline__ void sink_batch(const JoinTable &jt, const UnitDesc &d, const uint64_t (&key)[kU],
+                                           bool (&ok)[kU], const RectDesc &R, const uint32_t (&lidx)[kU],
+                                           const uint32_t (&qidx)[kU], const EnumArgs &A,
+                                           unsigned long long &hits) {
+#pragma unroll
+  for (int u = 0; u < kU; ++u)
+    if (ok[u] && d.npass > 1 && pass_of(key[u], d.npass) != d.pass) ok[u] = false;
   if constexpr (KIND == SINK_BUILD) {
-    if (key == 0) { atomicAdd(jt.zero + d.slot, 1ull); return; }
     const uint32_t mask = (1u << d.region_log2) - 1;
-    uint32_t s = home_slot(key, d.region_log2);
     unsigned long long *K = jt.keys + d.region_base;
-    for (uint32_t p = 0; p <= mask; ++p) {
-      const unsigned long long old = atomicCAS(K + s, 0ull, (unsigned long long)key);
-      if (old == 0) return;                       // fresh key: stored count-1 stays 0
-      if (old == key) { atomicAdd(jt.cnt + d.region_base + s, 1ull); return; }
-      s = (s + 1) & mask;
+    uint32_t s[kU];
+    unsigned long long old[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {  // kU independent CAS in flight
+      s[u] = home_slot(key[u], d.region_log2);
+      old[u] = (ok[u] && key[u] != 0) ? atomicCAS(K + s[u], 0ull, (unsigned long long)key[u]) : 0ull;
     }
-    atomicOr(jt.err, 1);                          // region full: host retries with more passes
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (!ok[u]) continue;
+      if (key[u] == 0) { atomicAdd(jt.zero + d.slot, 1ull); continue; }
+      if (old[u] == 0) continue;                            // fresh key
+      if (old[u] == key[u]) { count_duplicate(jt, d.region_base + s[u]); continue; }
+      uint32_t t = (s[u] + 1) & mask;                       // collision: linear probe
+      bool placed = false;
+      for (uint32_t p = 0; p < mask; ++p) {
+        const unsigned long long o = atomicCAS(K + t, 0ull, (unsigned long long)key[u]);
+        if (o == 0) { placed = true; break; }
+        if (o == key[u]) { count_duplicate(jt, d.region_base + t); placed = true; break; }
+        t = (t + 1) & mask;
+      }
+      if (!placed) atomicOr(jt.err, 1);                     // region full
+    }
   } else if constexpr (KIND == SINK_PROBE) {
-    if (key == 0) {
-      const unsigned long long z = jt.zero[d.slot];
-      if (z) {
-        hits += z;
-        if (atomicExch(jt.zero_hit + d.slot, 1u) == 0u) {
-          const unsigned long long i = atomicAdd(jt.nhits, 1ull);
-          if (i < jt.hit_cap) jt.hits[i] = HitRec{d.gid, 0u, 0ull};
-        }
-      }
-      return;
+    const uint32_t mask = (1u << d.region_log2) - 1;
+    const unsigned long long *K = jt.keys + d.region_base;
+    uint32_t s[kU];
+    unsigned long long t[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {  // kU independent loads in flight
+      s[u] = home_slot(key[u], d.region_log2);
+      t[u] = (ok[u] && key[u] != 0) ? K[s[u]] : 0ull;
     }
-    uint32_t slot;
-    if (table_find(jt, d, key, slot)) {
-      const unsigned long long c = jt.cnt[slot];
-      hits += (c & ~kHitFlag) + 1;
-      if (!(c & kHitFlag)) {
-        const unsigned long long old = atomicOr(jt.cnt + slot, kHitFlag);
-        if (!(old & kHitFlag)) {
-          const unsigned long long i = atomicAdd(jt.nhits, 1ull);
-          if (i < jt.hit_cap) jt.hits[i] = HitRec{d.gid, 0u, key};
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (!ok[u]) continue;
+      if (key[u] == 0) {
+        const unsigned long long z = jt.zero[d.slot];
+        if (z) {
+          hits += z;
+          if (atomicExch(jt.zero_hit + d.slot, 1u) == 0u) {
+            const unsigned long long i = atomicAdd(jt.nhits, 1ull);
+            if (i < jt.hit_cap) jt.hits[i] = HitRec{d.gid, 0u, 0ull};
+          }
         }
+        continue;
       }
-    }
-  } else {  // SINK_RECOVER: emit every pair whose key is in the batch's hit set
-    bool present;
-    if (key == 0) {
-      present = d.flags & 1u;
-    } else {
+      if (t[u] == key[u]) { register_hit(jt, d.gid, d.region_base + s[u], key[u], hits); continue; }
+      if (t[u] == 0) continue;                              // miss
       uint32_t slot;
-      present = table_find(jt, d, key, slot);
+      if (table_find(jt, d, key[u], (s[u] + 1) & mask, slot)) register_hit(jt, d.gid, slot, key[u], hits);
     }
-    if (present) {
-      const unsigned long long i = atomicAdd(jt.nrecs, 1ull);
-      if (i < jt.rec_cap) {
-        const uint32_t xi = R.lane_is_x ? lidx : qidx, yi = R.lane_is_x ? qidx : lidx;
-        const uint32_t *xm = d.side ? A.tab[2].mask : A.tab[0].mask;
-        const uint32_t *ym = d.side ? A.tab[3].mask : A.tab[1].mask;
-        jt.recs[i] = PairRec{d.gid, d.side, xi, yi, __ldg(xm + xi), __ldg(ym + yi), key};
+  } else if constexpr (KIND == SINK_NONE) {  // diagnostic: keep the keys live, touch nothing
+#pragma unroll
+    for (int u = 0; u < kU; ++u) hits ^= ok[u] ? key[u] : 0ull;
+  } else {  // SINK_RECOVER: emit every pair whose key is in the batch's hit set
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (!ok[u]) continue;
+      bool present;
+      if (key[u] == 0) {
+        present = d.flags & 1u;
+      } else {
+        uint32_t slot;
+        present = table_find(jt, d, key[u], home_slot(key[u], d.region_log2), slot);
+      }
+      if (present) {
+        const unsigned long long i = atomicAdd(jt.nrecs, 1ull);
+        if (i < jt.rec_cap) {
+          const uint32_t xi = R.lane_is_x ? lidx[u] : qidx[u], yi = R.lane_is_x ? qidx[u] : lidx[u];
+          const uint32_t *xm = d.side ? A.tab[2].mask : A.tab[0].mask;
+          const uint32_t *ym = d.side ? A.tab[3].mask : A.tab[1].mask;
+          jt.recs[i] = PairRec{d.gid, d.side, xi, yi, __ldg(xm + xi), __ldg(ym + yi), key[u]};
+        }
       }
     }
   }
@@ -103,7 +169,7 @@ __device__ __forceinline__ void sink(const JoinTable &jt, const UnitDesc &d, uin
 // ---------------------------------------------------------------- enumeration kernel
 
 template <int MC, int KIND>
-__global__ void __launch_bounds__(256) k_enum(const EnumArgs A, const JoinTable jt) {
+__global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTable jt) {
   constexpr int NW = words_for(MC);
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -112,7 +178,7 @@ __global__ void __launch_bounds__(256) k_enum(const EnumArgs A, const JoinTable 
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
 
-  __shared__ __align__(16) uint32_t ybuf_all[8][kTQ * 8];
+  __shared__ __align__(16) uint32_t ybuf_all[8][kTQ * stride_for(MC)];
   for (uint64_t chunk = wid; chunk < A.nchunks; chunk += nwarps) {
     TileWalker W;
     W.init(A, chunk * A.chunk_tiles, min(chunk * A.chunk_tiles + A.chunk_tiles, A.total_tiles));
@@ -121,10 +187,17 @@ __global__ void __launch_bounds__(256) k_enum(const EnumArgs A, const JoinTable 
     C.ybuf = ybuf_all[threadIdx.x >> 5];
     while (W.valid()) {
       begin_tile<MC>(A, W, lane, C);
-      while (C.q < C.q1)
-        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
-          sink<KIND>(jt, W.d, key, ok, W.R, lidx, qidx, A, hits);
+      while (C.q < C.q1) {
+        uint64_t kk[kU];
+        bool okk[kU];
+        uint32_t li[kU], qi[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) { okk[u] = false; kk[u] = 0; li[u] = qi[u] = 0; }
+        step_keys<MC>(W, C, dg, filt, [&](int u, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
+          kk[u] = key; okk[u] = ok; li[u] = lidx; qi[u] = qidx;
         });
+        sink_batch<KIND>(jt, W.d, kk, okk, W.R, li, qi, A, hits);
+      }
       uint32_t old;
       if (W.advance(A, old)) {
         const unsigned long long f = warp_sum(filt), h = warp_sum(hits);
@@ -148,6 +221,7 @@ static void launch_mc(SinkKind kind, const EnumArgs &a, const JoinTable &jt, int
   switch (kind) {
     case SINK_BUILD: k_enum<MC, SINK_BUILD><<<grid, 256, 0, st>>>(a, jt); break;
     case SINK_PROBE: k_enum<MC, SINK_PROBE><<<grid, 256, 0, st>>>(a, jt); break;
+    case SINK_NONE: k_enum<MC, SINK_NONE><<<grid, 256, 0, st>>>(a, jt); break;
     default: k_enum<MC, SINK_RECOVER><<<grid, 256, 0, st>>>(a, jt); break;
   }
 }

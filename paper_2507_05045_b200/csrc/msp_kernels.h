@@ -58,8 +58,10 @@ struct BruteArgs {
 
 // Global-hash-table join sinks (build / probe / recover), see msp_enum.cu.
 struct JoinTable {
-  unsigned long long *keys;    // 0 = empty
-  unsigned long long *cnt;     // (count - 1) | kHitFlag
+  unsigned long long *keys;    // 0 = empty (cleared per wave)
+  unsigned long long *cnt;     // epoch-tagged: (epoch << 40) | hit flag << 39 | (count - 1); a
+                               // slot whose tag is not this wave's epoch has count 1, no hit yet
+  unsigned long long epoch;    // 24-bit tag of the current wave (never 0)
   unsigned long long *zero;    // per wave slot: count of key 0
   unsigned int *zero_hit;      // per wave slot
   HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;
@@ -106,7 +108,7 @@ struct RescatterArgs { const RescatterSrc *src; uint32_t nsrc; uint64_t total; }
 cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st);
 cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 
-enum SinkKind { SINK_BUILD = 0, SINK_PROBE = 1, SINK_RECOVER = 2 };
+enum SinkKind { SINK_BUILD = 0, SINK_PROBE = 1, SINK_RECOVER = 2, SINK_NONE = 3 /* diagnostic: hash only */ };
 // Enumerate every pair of the launch's units, hash it, and hand the key to the sink.
 int launch_enum(int mc, SinkKind kind, const EnumArgs &args, const JoinTable &jt, int num_sms,
                 cudaStream_t st);

@@ -82,6 +82,10 @@ struct Device {
   DBuf rkeys, runits, rfilt, rhits;
   DBuf bfilt, bhits, bovf, scratch, bk, fill;
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
+  uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
+  cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
+  cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
+  DBuf scratch2, fill2;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
@@ -89,7 +93,7 @@ struct Device {
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
                    &bfilt, &bhits, &bovf, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
-                   &cfill, &cbk, &hunits, &l2bk, &l2src};
+                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
                                   comp[i].release(); rs[i].release(); re[i].release(); }
@@ -114,6 +118,10 @@ int get_device(int dev, Device **out) {
   CK(cudaDeviceGetAttribute(&D->num_sms, cudaDevAttrMultiProcessorCount, dev));
   for (auto &e : D->ev) CK(cudaEventCreate(&e));
   for (auto &e : D->pev) CK(cudaEventCreate(&e));
+  CK(cudaStreamCreateWithFlags(&D->stream2, cudaStreamNonBlocking));
+  for (auto &e : D->ev_s) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto &e : D->ev_j) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&D->ev_x, cudaEventDisableTiming));
   g_devices[dev] = D;
   *out = D;
   return MSP_OK;
@@ -555,6 +563,46 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   bool stopped = false;
   std::vector<uint8_t> dropped(P.G, 0);  // batches whose partitioned join overflowed
 
+  bool fill_zeroed = false;  // wave fill counters (reset by k_join after each bucket)
+  // Double-buffered waves: wave k scatters into buffer k&1 on `st` while wave k-1 joins on
+  // stream2; ordering is carried by events (scatter k waits for join k-2, join k for scatter k).
+  const bool overlap = !profile;
+  auto join_streams = [&]() -> int {
+    CK(cudaEventRecord(D.ev_x, D.stream2));
+    CK(cudaStreamWaitEvent(st, D.ev_x, 0));
+    return MSP_OK;
+  };
+  auto launch_pair = [&](size_t wi, auto &&scatter_fn, PartArgs &pa) -> int {
+    const int buf = (int)(wi & 1);
+    pa.scratch = (buf ? D.scratch2 : D.scratch).as<unsigned long long>();
+    pa.fill[0] = (buf ? D.fill2 : D.fill).as<uint32_t>();
+    pa.fill[1] = pa.fill[0] + kMaxWaveBuckets;
+    if (!overlap) {
+      CK(scatter_fn(pa, st));
+      CK(launch_join(pa, D.num_sms, st));
+      return MSP_OK;
+    }
+    if (wi >= 2) CK(cudaStreamWaitEvent(st, D.ev_j[buf], 0));
+    CK(scatter_fn(pa, st));
+    CK(cudaEventRecord(D.ev_s[buf], st));
+    CK(cudaStreamWaitEvent(D.stream2, D.ev_s[buf], 0));
+    CK(launch_join(pa, D.num_sms, D.stream2));
+    CK(cudaEventRecord(D.ev_j[buf], D.stream2));
+    return MSP_OK;
+  };
+  auto ensure_wave_buffers = [&](uint64_t scratch_keys) -> int {
+    CK(D.scratch.ensure(8 * scratch_keys));
+    CK(D.scratch2.ensure(8 * scratch_keys));
+    void *f1 = D.fill.p, *f2 = D.fill2.p;
+    CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
+    CK(D.fill2.ensure(4 * 2 * kMaxWaveBuckets));
+    if (f1 != D.fill.p || f2 != D.fill2.p || !fill_zeroed) {
+      CK(cudaMemsetAsync(D.fill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+      CK(cudaMemsetAsync(D.fill2.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+      fill_zeroed = true;
+    }
+    return MSP_OK;
+  };
   // Recovery of a set of hit keys: re-enumerate those batches, emit the pairs whose key is a hit
   // key, confirm exactly on the host (validate.py:285-313).  Own buffers: waves can resume after.
   int64_t recovered_hh = 0;
@@ -637,6 +685,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   };
   // Sync point: deadline, hit-list capacity and (first mode) early recovery.
   auto checkpoint = [&](bool &stop_now) -> int {
+    if (int r0 = join_streams()) return r0;
     unsigned long long nh = 0;
     CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -655,7 +704,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     return MSP_OK;
   };
   const bool periodic = deadline || opt->mode == MSP_MODE_FIRST;
-  bool fill_zeroed = false;  // wave fill counters (reset by k_join after each bucket)
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
   const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : (10ull << 20);
@@ -718,12 +766,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       uint64_t max_scratch = 0;
       for (const PWave &w : pw) max_scratch = std::max(max_scratch, w.scratch);
       const size_t nbt = bgid.size();
-      CK(D.scratch.ensure(8 * max_scratch));
+      rc = ensure_wave_buffers(max_scratch);
+      if (rc) return rc;
       CK(D.units.ensure(sizeof(UnitDesc) * units.size()));
       CK(D.bk.ensure(4 * 5 * nbt));
-      CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
-      CK(cudaMemsetAsync(D.fill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
-      fill_zeroed = true;
       std::vector<uint32_t> bkimg;
       bkimg.reserve(5 * nbt);
       for (auto *v : {&bstart[0], &bstart[1], &bcap[0], &bcap[1], &bgid}) bkimg.insert(bkimg.end(), v->begin(), v->end());
@@ -752,8 +798,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         A.chunk_tiles = std::max<uint64_t>(1, std::min<uint64_t>(256, w.tiles / ((uint64_t)D.num_sms * kScatterWarpsHost * 3)));
         A.nchunks = (w.tiles + kScatterWarpsHost * A.chunk_tiles - 1) / (kScatterWarpsHost * A.chunk_tiles);
         if (profile) CK(cudaEventRecord(D.pev[0], st));
-        CK(launch_scatter(P.mc, A, pa, D.num_sms, st));
-        CK(launch_join(pa, D.num_sms, st));
+        rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_scatter(P.mc, A, p2, D.num_sms, s2); }, pa);
+        if (rc) return rc;
         S.kernel_launches += 2;
         if (profile) {
           CK(cudaEventRecord(D.pev[1], st));
@@ -772,6 +818,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
   }
 
+  rc = join_streams();
+  if (rc) return rc;
+
   // ---- huge batches: two-level partitioned join.  Level 1 hashes the batch once and partitions
   //      each side into <= 1024 coarse buckets in HBM (one k_scatter launch per side, so each
   //      side's region indices stay 32-bit); level 2 streams coarse buckets back, re-partitions
@@ -780,6 +829,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     constexpr uint64_t kCoarseTarget = 2ull << 20;  // build keys per coarse bucket
     CK(D.cfill.ensure(4 * 2 * kMaxWaveBuckets));
     for (size_t hi_ = 0; hi_ < huge_b.size() && !stopped; ++hi_) {
+      rc = join_streams();  // the previous batch's joins still read the wave buffers
+      if (rc) return rc;
       const uint32_t g = huge_b[hi_];
       const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
       const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
@@ -880,13 +931,12 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       std::vector<uint32_t> fimg;
       fimg.reserve(5 * nft);
       for (auto *v : {&fst0, &fst1, &fcap0, &fcap1, &fgid}) fimg.insert(fimg.end(), v->begin(), v->end());
-      CK(D.scratch.ensure(8 * max_scr));
+      rc = ensure_wave_buffers(max_scr);
+      if (rc) return rc;
       CK(D.l2bk.ensure(4 * fimg.size()));
       CK(D.l2src.ensure(sizeof(RescatterSrc) * srcs.size()));
-      CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
       CK(cudaMemcpyAsync(D.l2bk.p, fimg.data(), 4 * fimg.size(), cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(D.l2src.p, srcs.data(), sizeof(RescatterSrc) * srcs.size(), cudaMemcpyHostToDevice, st));
-      if (!fill_zeroed) { CK(cudaMemsetAsync(D.fill.p, 0, 4 * 2 * kMaxWaveBuckets, st)); fill_zeroed = true; }
       const uint32_t *fb = D.l2bk.as<uint32_t>();
       PartArgs pa{};
       pa.scratch = D.scratch.as<unsigned long long>();
@@ -906,8 +956,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         pa.gid = fb + 4 * nft + w.b0;
         pa.nb = (uint32_t)w.nb;
         RescatterArgs ra{D.l2src.as<RescatterSrc>() + w.s0, (uint32_t)w.ns, w.total};
-        CK(launch_rescatter(ra, pa, D.num_sms, st));
-        CK(launch_join(pa, D.num_sms, st));
+        rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_rescatter(ra, p2, D.num_sms, s2); }, pa);
+        if (rc) return rc;
         S.kernel_launches += 2;
       }
       S.waves += (int32_t)lw.size() + 1;
@@ -926,6 +976,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       }
     }
   }
+
+  rc = join_streams();
+  if (rc) return rc;
 
   // ---- overflowed partitioned batches are re-joined with the global table
   unsigned long long n_v2_hits = 0;
@@ -1011,7 +1064,14 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     for (const Wave &w : waves) { max_nslot = std::max(max_nslot, w.nslot); max_slots = std::max(max_slots, w.slots); }
     CK(D.units.ensure(sizeof(UnitDesc) * std::max<size_t>(1, units.size())));
     CK(D.keys.ensure(8 * max_slots));
-    CK(D.cnt.ensure(8 * max_slots));
+    {
+      void *before = D.cnt.p;
+      CK(D.cnt.ensure(8 * max_slots));
+      if (D.cnt.p != before) {  // fresh memory: no stale tag may look like a live epoch
+        CK(cudaMemsetAsync(D.cnt.p, 0, D.cnt.cap, st));
+        D.epoch = 0;
+      }
+    }
     CK(D.zero.ensure(8 * max_nslot));
     CK(D.zhit.ensure(4 * max_nslot));
     CK(cudaMemcpyAsync(D.units.p, units.data(), sizeof(UnitDesc) * units.size(), cudaMemcpyHostToDevice, st));
@@ -1023,14 +1083,19 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     for (size_t wi = 0; wi < waves.size(); ++wi) {
       const Wave &w = waves[wi];
       CK(cudaMemsetAsync(D.keys.p, 0, 8 * w.slots, st));
-      CK(cudaMemsetAsync(D.cnt.p, 0, 8 * w.slots, st));
+      if (++D.epoch >= (1ull << 24)) {  // tag space exhausted: clear and restart
+        CK(cudaMemsetAsync(D.cnt.p, 0, D.cnt.cap, st));
+        D.epoch = 1;
+      }
+      jt.epoch = D.epoch;
       CK(cudaMemsetAsync(D.zero.p, 0, 8 * w.nslot, st));
       CK(cudaMemsetAsync(D.zhit.p, 0, 4 * w.nslot, st));
       if (profile) CK(cudaEventRecord(D.pev[0], st));
       set_enum_range(A, udev + w.ub0, w.ub1 - w.ub0, w.build_tiles, D.num_sms);
-      if (launch_enum(P.mc, SINK_BUILD, A, jt, D.num_sms, st)) { set_err("unsupported m"); return MSP_INTERNAL; }
+      const bool diag = opt->flags & MSP_FLAG_DIAG_HASH_ONLY;
+      if (launch_enum(P.mc, diag ? SINK_NONE : SINK_BUILD, A, jt, D.num_sms, st)) { set_err("unsupported m"); return MSP_INTERNAL; }
       set_enum_range(A, udev + w.up0, w.up1 - w.up0, w.probe_tiles, D.num_sms);
-      launch_enum(P.mc, SINK_PROBE, A, jt, D.num_sms, st);
+      launch_enum(P.mc, diag ? SINK_NONE : SINK_PROBE, A, jt, D.num_sms, st);
       S.kernel_launches += 2;
       if (profile) {
         CK(cudaEventRecord(D.pev[1], st));

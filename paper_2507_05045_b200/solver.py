@@ -64,6 +64,7 @@ class SolverConfig:
     memory_budget_bytes: int = DEFAULT_MEMORY_BUDGET
     device: int = 0
     wave_keys: int = 0
+    join: str = "auto"  # "auto" | "partitioned" | "global": join strategy of the CUDA engine
 
     def validated(self) -> "SolverConfig":
         if self.mode not in _MODES:
@@ -78,6 +79,8 @@ class SolverConfig:
             raise ValueError("worker_count must be >= 0")
         if self.memory_budget_bytes < 1:
             raise ValueError("memory_budget_bytes must be >= 1")
+        if self.join not in ("auto", "partitioned", "global"):
+            raise ValueError(f"unknown join {self.join!r}")
         if self.backend not in _BACKENDS:
             raise ValueError(f"unknown backend {self.backend!r}; choose from {sorted(_BACKENDS)}")
         return self
@@ -208,7 +211,9 @@ def solve(
 
     if time_limit is not None and time_limit <= 0:
         raise SolveTimeout(f"time limit of {time_limit}s exceeded")
-    found, st = native_solve(work, cfg.mode, time_limit, device=cfg.device, wave_keys=cfg.wave_keys)
+    flags = _native.MSP_FLAG_JOIN_GLOBAL if cfg.join == "global" else 0
+    found, st = native_solve(work, cfg.mode, time_limit, device=cfg.device, wave_keys=cfg.wave_keys,
+                             flags=flags)
     stats_from_native(st, stats)
     if stats.fallback == "none":
         stats.engine = "cuda"

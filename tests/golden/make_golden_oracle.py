@@ -22,11 +22,11 @@ from paper_2507_05045_b200.instances import generate_instance  # noqa: E402
 m, seed = int(sys.argv[1]), int(sys.argv[2])
 inst = generate_instance(m, 100, seed)
 t0 = time.time()
-r = O.solve(inst.a, inst.d, mode="all", bucket_bits_cap=30, chunk_pairs=1 << 34, record_batches=True)
+r = O.solve(inst.a, inst.d, mode="all", bucket_bits_cap=26, chunk_pairs=1 << 26, workers=6, record_batches=True)
 assert r.status == 0
 rec = {
     "name": f"gen_{m}_100_{seed}",
-    "source": "oracle/msp_oracle.c (pinned to the reference), bucket_bits_cap=30",
+    "source": "oracle/msp_oracle.c (pinned to the reference), bucket_bits_cap=26, chunk_pairs=2^26",
     "instance": {"a": inst.a.tolist(), "d": inst.d.tolist()},
     "verdict": "feasible" if r.solutions else "infeasible",
     "solutions": ["".join(map(str, x)) for x in r.solutions],
