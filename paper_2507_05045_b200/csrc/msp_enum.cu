@@ -156,7 +156,7 @@ __device__ __forceinline__ void sink_batch(const JoinTable &jt, const UnitDesc &
       if (present) {
         const unsigned long long i = atomicAdd(jt.nrecs, 1ull);
         if (i < jt.rec_cap) {
-          const uint32_t xi = R.lane_is_x ? lidx[u] : qidx[u], yi = R.lane_is_x ? qidx[u] : lidx[u];
+          const uint32_t xi = R.lane_is_x() ? lidx[u] : qidx[u], yi = R.lane_is_x() ? qidx[u] : lidx[u];
           const uint32_t *xm = d.side ? A.tab[2].mask : A.tab[0].mask;
           const uint32_t *ym = d.side ? A.tab[3].mask : A.tab[1].mask;
           jt.recs[i] = PairRec{d.gid, d.side, xi, yi, __ldg(xm + xi), __ldg(ym + yi), key[u]};

@@ -17,6 +17,7 @@
 // overflows (duplicate-heavy instances) marks its batch, which the host re-joins with the global
 // table path (msp_enum.cu), so results never depend on the partitioning.
 #include <cstdint>
+#include <type_traits>
 #include "msp_common.cuh"
 #include "msp_kernels.h"
 #include "msp_tile.cuh"
@@ -139,7 +140,7 @@ __device__ __forceinline__ void flush_round(const Stage &g, const PartArgs &S, u
   __syncthreads();
 }
 
-template <int MC>
+template <int MC, bool ITEMS>
 __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A, const PartArgs S) {
   constexpr int NW = words_for(MC);
   extern __shared__ __align__(16) unsigned char smem[];
@@ -157,39 +158,57 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A
   for (uint32_t i = tid; i < kHistEntries; i += blockDim.x) g.hist[i] = 0;
   __syncthreads();
 
-  for (uint64_t chunk = blockIdx.x; chunk < A.nchunks; chunk += gridDim.x) {
-    const uint64_t wT = (chunk * kScatterWarps + warp) * A.chunk_tiles;
-    TileWalker W;
-    W.init(A, min(wT, A.total_tiles), min(wT + A.chunk_tiles, A.total_tiles));
-    TileCursor<stride_for(MC)> C;
-    C.ybuf = ybuf_all[warp];
-    bool have = W.valid();
-    if (have) begin_tile<MC>(A, W, lane, C);
-    unsigned long long filt = 0;
-    while (true) {
-      uint32_t cnt = 0;
-      while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
-        const uint32_t bbase = ((W.d.flags >> 1) & 1u) * nbw + W.d.region_base;
-        const uint32_t bits = W.d.region_log2;
-        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
-          stage_key(g, warp, lt_mask, cnt, key, bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u), ok);
-        });
-        if (C.q >= C.q1) {
-          uint32_t old;
-          if (W.advance(A, old)) {
-            const unsigned long long f = warp_sum(filt);
-            if (lane == 0 && f) atomicAdd(A.batch_filtered + A.units[old].gid, f);
-            filt = 0;
+  // ITEMS: one-tile work items statically strided over the grid (small waves, balanced);
+  // else: contiguous tile chunks per warp (huge batches: large chunks amortise the search).
+  using Walker = typename std::conditional<ITEMS, ItemWalker, TileWalker>::type;
+  Walker W;
+  uint64_t chunk = (uint64_t)blockIdx.x * kScatterWarps + warp;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kScatterWarps;
+  if constexpr (ITEMS) {
+    W.init(A, chunk, nwarps);
+  } else {
+    W.init(A, min(chunk * A.chunk_tiles, A.total_tiles), min(chunk * A.chunk_tiles + A.chunk_tiles, A.total_tiles));
+  }
+  TileCursor<stride_for(MC)> C;
+  C.ybuf = ybuf_all[warp];
+  bool have;
+  if constexpr (ITEMS) have = W.grab(A, lane); else have = W.valid();
+  if (have) begin_tile<MC>(A, W, lane, C);
+  unsigned long long filt = 0;
+  while (true) {
+    uint32_t cnt = 0;
+    while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
+      const uint32_t bbase = ((W.d.flags >> 1) & 1u) * nbw + W.d.region_base;
+      const uint32_t bits = W.d.region_log2;
+      step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
+        stage_key(g, warp, lt_mask, cnt, key, bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u), ok);
+      });
+      if (C.q >= C.q1) {
+        uint32_t old_gid;
+        bool changed;
+        if constexpr (ITEMS) {
+          changed = W.advance(A, lane, old_gid);
+        } else {
+          uint32_t old_u;
+          changed = W.advance(A, old_u);
+          old_gid = A.units[old_u].gid;
+          if (!W.valid()) {  // next contiguous chunk of this warp
+            chunk += nwarps;
+            changed = true;
+            W.init(A, min(chunk * A.chunk_tiles, A.total_tiles), min(chunk * A.chunk_tiles + A.chunk_tiles, A.total_tiles));
           }
-          have = W.valid();
-          if (have) begin_tile<MC>(A, W, lane, C);
         }
+        if (changed) {
+          const unsigned long long f = warp_sum(filt);
+          if (lane == 0 && f) atomicAdd(A.batch_filtered + old_gid, f);
+          filt = 0;
+        }
+        have = W.valid();
+        if (have) begin_tile<MC>(A, W, lane, C);
       }
-      if (!__syncthreads_or(cnt > 0)) break;
-      flush_round(g, S, cnt);
     }
-    const unsigned long long f = warp_sum(filt);
-    if (lane == 0 && f) atomicAdd(A.batch_filtered + W.d.gid, f);
+    if (!__syncthreads_or(cnt > 0)) break;
+    flush_round(g, S, cnt);
   }
 }
 
@@ -334,23 +353,28 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
   }
 }
 
-template <int MC>
-static cudaError_t launch_scatter_mc(const EnumArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
+template <int MC, bool ITEMS>
+static cudaError_t launch_scatter_mi(const EnumArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
   static bool configured = false;
   const size_t sm = scatter_smem_bytes();
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_scatter<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_scatter<MC, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_scatter<MC><<<grid, kScatterWarps * 32, sm, st>>>(a, p);
+  k_scatter<MC, ITEMS><<<grid, kScatterWarps * 32, sm, st>>>(a, p);
   return cudaGetLastError();
+}
+template <int MC>
+static cudaError_t launch_scatter_mc(const EnumArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
+  return a.items ? launch_scatter_mi<MC, true>(a, p, grid, st) : launch_scatter_mi<MC, false>(a, p, grid, st);
 }
 
 cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int num_sms, cudaStream_t st) {
-  if (args.nchunks == 0) return cudaSuccess;
-  const uint64_t cap = (uint64_t)num_sms;
-  const int grid = (int)(args.nchunks < cap ? args.nchunks : cap);
+  const uint64_t work = args.items ? args.item_hi - args.item_lo : args.nchunks;
+  if (args.items ? args.item_hi <= args.item_lo : args.nchunks == 0) return cudaSuccess;
+  const uint64_t blocks = (work + kScatterWarps - 1) / kScatterWarps;
+  const int grid = (int)(blocks < (uint64_t)num_sms ? blocks : (uint64_t)num_sms);
   switch (mc) {
 #define MSP_CASE(N) case N: return launch_scatter_mc<N>(args, p, grid, st);
     MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)

@@ -75,7 +75,7 @@ struct Device {
   DBuf a, d;
   DBuf tw[4], tm[4], tw2[4], tm2[4], comp[4], rs[4], re[4];
   DBuf yw[2], ys[2], yl[2], yn;
-  DBuf hl, hr, galpha, gnl, gnr, gcount, rects, nrect, rbase, tiles, err;
+  DBuf hl, hr, galpha, gnl, gnr, gcount, rects, nrect, rbase, tiles, err, nitem, ibase, items, ictr;
   DBuf units, ufilt, uhits;
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
@@ -89,7 +89,7 @@ struct Device {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
-    DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err,
+    DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err, &nitem, &ibase, &items, &ictr,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
                    &bfilt, &bhits, &bovf, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
@@ -148,6 +148,7 @@ struct Plan {
   uint32_t G = 0;
   std::vector<uint64_t> alpha, nl, nr, tiles;  // tiles[2g + side]
   std::vector<uint32_t> rect_base, nrect;      // [2g + side]
+  std::vector<uint64_t> item_base;             // [2g + side], + total
   EnumArgs base{};
   int merge_w_cur[4] = {0, 0, 0, 0};  // which ping-pong buffer holds the final table
 };
@@ -190,7 +191,7 @@ int check_instance(const msp_problem *pr, Plan &P) {
 
 // K1 + K2 on the device; ends with the batch list and tile totals on the host.
 int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uint64_t alpha_hi,
-               cudaStream_t st, int64_t &launches) {
+               cudaStream_t st, int64_t &launches, uint64_t item_key_budget = 10ull << 20) {
   const int m = P.m, n = P.n;
   CK(D.a.ensure(sizeof(uint64_t) * m * n));
   CK(D.d.ensure(sizeof(uint64_t) * m));
@@ -283,7 +284,9 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   // ---- rectangle lists per (batch, side): count pass, one sync, write pass
   CK(D.tiles.ensure(16 * (size_t)P.G));
   CK(D.nrect.ensure(8 * (size_t)P.G));
+  CK(D.nitem.ensure(8 * (size_t)P.G));
   CK(D.rbase.ensure(8 * (size_t)P.G));
+  CK(D.ibase.ensure(8 * (2 * (size_t)P.G + 1)));
   CK(D.err.ensure(16));
   CK(cudaMemsetAsync(D.err.p, 0, 16, st));
   RectArgs ra2{};
@@ -297,16 +300,18 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   ra2.count = D.gcount.as<uint32_t>();
   ra2.tiles = D.tiles.as<unsigned long long>();
   ra2.nrect = D.nrect.as<uint32_t>();
+  ra2.nitem = D.nitem.as<uint32_t>();
   ra2.err = D.err.as<int>();
   launch_rects(ra2, P.G, st);
   ++launches;
   int err = 0;
-  std::vector<uint32_t> nrect(2 * (size_t)P.G);
+  std::vector<uint32_t> nrect(2 * (size_t)P.G), nitem(2 * (size_t)P.G);
   CK(cudaMemcpyAsync(P.alpha.data(), D.galpha.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.nl.data(), D.gnl.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.nr.data(), D.gnr.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.tiles.data(), D.tiles.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(nrect.data(), D.nrect.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(nitem.data(), D.nitem.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (err) { set_err("tile count of one batch side exceeds 2^32"); return MSP_UNSUPPORTED; }
@@ -316,9 +321,20 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   for (size_t i = 0; i < 2 * (size_t)P.G; ++i) { P.rect_base[i] = (uint32_t)nrt; nrt += nrect[i]; }
   if (nrt > 0xFFFFFFFFull) { set_err("rectangle list too large"); return MSP_UNSUPPORTED; }
   CK(D.rects.ensure(sizeof(RectDesc) * std::max<uint64_t>(nrt, 1)));
+  P.item_base.assign(2 * (size_t)P.G + 1, 0);
+  for (size_t i = 0; i < 2 * (size_t)P.G; ++i) {
+    const size_t g = i / 2;  // items only for batches the partitioned waves can hold
+    const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
+    const bool fits = nb + np <= item_key_budget && ((nb + kBucketTarget - 1) / kBucketTarget) <= (uint64_t)kMaxWaveBuckets;
+    P.item_base[i + 1] = P.item_base[i] + (fits ? nitem[i] : 0u);
+  }
+  CK(D.items.ensure(8 * std::max<uint64_t>(P.item_base.back(), 1)));
   CK(cudaMemcpyAsync(D.rbase.p, P.rect_base.data(), 8 * (size_t)P.G, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(D.ibase.p, P.item_base.data(), 8 * (2 * (size_t)P.G + 1), cudaMemcpyHostToDevice, st));
   ra2.rect_base = D.rbase.as<uint32_t>();
   ra2.rects = D.rects.as<RectDesc>();
+  ra2.item_base = D.ibase.as<uint64_t>();
+  ra2.items = D.items.as<uint64_t>();
   launch_rects(ra2, P.G, st);
   ++launches;
   // ---- launch-invariant enumeration arguments
@@ -329,6 +345,7 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   for (int s = 0; s < 2; ++s)
     A.yr[s] = YRuns{D.yw[s].as<uint32_t>(), D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), P.ny[s]};
   A.rects = D.rects.as<RectDesc>();
+  A.items = D.items.as<uint64_t>();
   for (int k = 0; k < 8; ++k) {
     const int c0 = 2 * k + 1, c1 = 2 * k + 2;  // rows c0, c1 (1-based companion rows)
     const uint32_t lo = (c0 < m ? (uint32_t)pr->d[c0] : 0u) + 0x8000u;
@@ -515,7 +532,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   if (rc) return rc;
   const double deadline = opt->time_limit_s > 0 ? t0 + opt->time_limit_s : 0;
   CK(cudaEventRecord(D.ev[0], st));
-  rc = build_plan(D, pr, P, opt->alpha_lo, opt->alpha_hi, st, S.kernel_launches);
+  const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : (10ull << 20);
+  rc = build_plan(D, pr, P, opt->alpha_lo, opt->alpha_hi, st, S.kernel_launches, key_budget);
   if (rc) return rc;
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.ev[1], st));
@@ -706,7 +724,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   const bool periodic = deadline || opt->mode == MSP_MODE_FIRST;
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
-  const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : (10ull << 20);
   std::vector<uint32_t> part_b, huge_b, global_b;
   for (uint32_t g = 0; g < P.G; ++g) {
     const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
@@ -719,27 +736,38 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       part_b.push_back(g);
   }
 
+  // ---- dynamic item counters, one per scatter launch of this solve
+  const size_t n_ictr = P.G + 2 * huge_b.size() + 1;
+  CK(D.ictr.ensure(8 * n_ictr));
+  CK(cudaMemsetAsync(D.ictr.p, 0, 8 * n_ictr, st));
+  size_t ictr_next = 0;
+
   // ---- partitioned waves
   {
-    struct PWave { size_t u0, u1, b0, nb; uint64_t tiles, scratch, pairs; };
+    struct PWave { size_t u0, u1, b0, nb; uint64_t tiles, scratch, pairs; uint32_t g0, g1; };
     std::vector<PWave> pw;
     std::vector<UnitDesc> units;
     std::vector<uint32_t> bstart[2], bcap[2], bgid;
-    PWave cur{0, 0, 0, 0, 0, 0, 0};
+    PWave cur{0, 0, 0, 0, 0, 0, 0, 0, 0};
     uint64_t cur_keys = 0;
     auto flush = [&]() {
       if (cur.nb == 0) return;
       cur.u1 = units.size();
       pw.push_back(cur);
-      cur = PWave{units.size(), units.size(), bgid.size(), 0, 0, 0, 0};
+      cur = PWave{units.size(), units.size(), bgid.size(), 0, 0, 0, 0, 0, 0};
       cur_keys = 0;
     };
     for (uint32_t g : part_b) {
+      if (cur.nb == 0) cur.g0 = g;
       const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
       const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
       const uint32_t bits = pow2ceil((nb + kBucketTarget - 1) / kBucketTarget);
       const uint32_t NB = 1u << bits;
-      if (cur.nb + NB > (uint32_t)kMaxWaveBuckets || cur_keys + nb + np > key_budget) flush();
+      if (cur.nb + NB > (uint32_t)kMaxWaveBuckets || cur_keys + nb + np > key_budget ||
+          (cur.nb && g != cur.g1)) {  // waves hold consecutive batches (contiguous item ranges)
+        flush();
+        cur.g0 = g;
+      }
       const double mb = (double)nb / NB, mp = (double)np / NB;
       const uint32_t cb = (uint32_t)(mb + 7.0 * std::sqrt(mb) + 16), cp = (uint32_t)(mp + 7.0 * std::sqrt(mp) + 16);
       for (uint32_t k = 0; k < NB; ++k) {
@@ -757,6 +785,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         units.push_back(u);
       }
       cur.nb += NB;
+      cur.g1 = g + 1;
       cur.pairs += P.nl[g] + P.nr[g];
       cur_keys += nb + np;
     }
@@ -794,9 +823,11 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         pa.gid = bkd + 4 * nbt + w.b0;
         pa.nb = (uint32_t)w.nb;
         set_enum_range(A, D.units.as<UnitDesc>() + w.u0, w.u1 - w.u0, w.tiles, D.num_sms);
-        // the scatter CTA walks 4 warps x chunk_tiles tiles per work item
-        A.chunk_tiles = std::max<uint64_t>(1, std::min<uint64_t>(256, w.tiles / ((uint64_t)D.num_sms * kScatterWarpsHost * 3)));
-        A.nchunks = (w.tiles + kScatterWarpsHost * A.chunk_tiles - 1) / (kScatterWarpsHost * A.chunk_tiles);
+        A.items = D.items.as<uint64_t>();
+        A.item_lo = P.item_base[2 * (size_t)w.g0];
+        A.item_hi = P.item_base[2 * (size_t)w.g1];
+        A.gs_base = 2 * w.g0;
+        A.item_ctr = D.ictr.as<unsigned long long>() + (ictr_next++);
         if (profile) CK(cudaEventRecord(D.pev[0], st));
         rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_scatter(P.mc, A, p2, D.num_sms, s2); }, pa);
         if (rc) return rc;
@@ -883,8 +914,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       for (int role = 0; role < 2; ++role) {
         c1.scratch = D.cscratch[role].as<unsigned long long>();
         set_enum_range(A, D.hunits.as<UnitDesc>() + role, 1, ltiles[role], D.num_sms);
-        A.chunk_tiles = std::max<uint64_t>(1, std::min<uint64_t>(256, ltiles[role] / ((uint64_t)D.num_sms * kScatterWarpsHost * 3)));
-        A.nchunks = (ltiles[role] + kScatterWarpsHost * A.chunk_tiles - 1) / (kScatterWarpsHost * A.chunk_tiles);
+        A.items = nullptr;  // huge batch: contiguous tile chunks
+        A.chunk_tiles = std::max<uint64_t>(1, std::min<uint64_t>(1024, ltiles[role] / ((uint64_t)D.num_sms * kScatterWarpsHost * 8)));
+        A.nchunks = (ltiles[role] + A.chunk_tiles - 1) / A.chunk_tiles;
         CK(launch_scatter(P.mc, A, c1, D.num_sms, st));
         ++S.kernel_launches;
       }

@@ -184,8 +184,9 @@ __global__ void k_rects(RectArgs p) {
   const uint64_t xw_total = side == 0 ? p.alpha[g] : p.target - p.alpha[g];
   const bool write = p.rects != nullptr;
   RectDesc *out = write ? p.rects + p.rect_base[(size_t)g * 2 + side] : nullptr;
-  uint64_t tbase = 0;
+  uint64_t tbase = 0, ibase = 0;
   uint32_t rbase = 0;
+  const size_t gs = (size_t)g * 2 + side;
   for (uint32_t r0 = 0; r0 < ny; r0 += blockDim.x) {
     const uint32_t r = r0 + threadIdx.x;
     uint32_t tiles = 0, xs = 0, xl = 0, ys = 0, yl = 0;
@@ -203,27 +204,39 @@ __global__ void k_rects(RectArgs p) {
         }
       }
     }
-    uint32_t ttot, rtot;
+    uint32_t ttot, rtot, itot;
+    const uint32_t nit = (tiles + kItemTiles - 1) / kItemTiles;
     const uint32_t tpos = block_excl_scan(tiles, ttot);
     const uint32_t rpos = block_excl_scan(tiles > 0, rtot);
+    const uint32_t ipos = block_excl_scan(nit, itot);
     if (write && tiles) {
       RectDesc R;
-      R.lane_is_x = xl >= yl;
-      R.lane_start = R.lane_is_x ? xs : ys;
-      R.loop_start = R.lane_is_x ? ys : xs;
-      R.L = R.lane_is_x ? xl : yl;
-      R.Q = R.lane_is_x ? yl : xl;
+      const bool lx = xl >= yl;
+      R.gs_x = ((uint32_t)(g * 2 + side) << 1) | (lx ? 1u : 0u);
+      R.lane_start = lx ? xs : ys;
+      R.loop_start = lx ? ys : xs;
+      R.L = lx ? xl : yl;
+      R.Q = lx ? yl : xl;
       R.tile_off = (uint32_t)(tbase + tpos);
       R.nl = (R.L + 31) / 32;
       R.nq = (R.Q + kTQ - 1) / kTQ;
       out[rbase + rpos] = R;
+      const uint64_t ridx = p.rect_base[gs] + rbase + rpos;
+      uint64_t *it = p.items + p.item_base[gs] + ibase + ipos;
+      const uint32_t emit = p.item_base[gs + 1] > p.item_base[gs] ? nit : 0u;  // huge batches: none
+      for (uint32_t k = 0; k < emit; ++k) {
+        const uint32_t t0 = k * kItemTiles, nt = min(kItemTiles, tiles - t0);
+        it[k] = ridx | ((uint64_t)t0 << 32) | ((uint64_t)nt << 56);
+      }
     }
     tbase += ttot;
     rbase += rtot;
+    ibase += itot;
   }
   if (!write && threadIdx.x == 0) {
-    p.tiles[(size_t)g * 2 + side] = tbase;
-    p.nrect[(size_t)g * 2 + side] = rbase;
+    p.tiles[gs] = tbase;
+    p.nrect[gs] = rbase;
+    p.nitem[gs] = (uint32_t)ibase;
     if (tbase > 0xFFFFFFFFull) atomicOr(p.err, 2);
   }
 }

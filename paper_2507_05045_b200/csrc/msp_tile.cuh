@@ -85,10 +85,74 @@ struct TileWalker {
     return d.side ? A.tab[3].comp : A.tab[1].comp;
   }
   __device__ __forceinline__ const uint32_t *lane_comp(const EnumArgs &A) const {
-    return R.lane_is_x ? x_comp(A) : y_comp(A);
+    return R.lane_is_x() ? x_comp(A) : y_comp(A);
   }
   __device__ __forceinline__ const uint32_t *loop_comp(const EnumArgs &A) const {
-    return R.lane_is_x ? y_comp(A) : x_comp(A);
+    return R.lane_is_x() ? y_comp(A) : x_comp(A);
+  }
+};
+
+// Walks this launch's work items statically strided over all warps of the grid (warp w takes
+// items w, w + W, w + 2W, ...), prefetching the next item word and rectangle descriptor while the
+// current item is processed: no search, no atomics, no dependent loads on the critical path.
+// Same tile interface as TileWalker.
+struct ItemWalker {
+  uint32_t t, tend, lc, qc;
+  bool ok;
+  UnitDesc d;
+  RectDesc R;
+  uint64_t next_i, stride;
+  uint64_t nit;      // prefetched item word (valid iff next_i < item_hi)
+  RectDesc nrect;
+
+  __device__ __forceinline__ void prefetch(const EnumArgs &A) {
+    if (next_i < A.item_hi) {
+      nit = __ldg(reinterpret_cast<const unsigned long long *>(A.items) + next_i);
+      nrect = load_rect(A.rects + (uint32_t)nit);
+    }
+  }
+  __device__ __forceinline__ void init(const EnumArgs &A, uint64_t warp_id, uint64_t nwarps) {
+    next_i = A.item_lo + warp_id;
+    stride = nwarps;
+    ok = false;
+    prefetch(A);
+  }
+  __device__ __forceinline__ bool grab(const EnumArgs &A, uint32_t) {
+    ok = next_i < A.item_hi;
+    if (!ok) return false;
+    R = nrect;
+    t = (uint32_t)(nit >> 32) & 0xFFFFFFu;
+    tend = t + (uint32_t)(nit >> 56);
+    d = A.units[R.gs() - A.gs_base];
+    lc = t / R.nq;
+    qc = t - lc * R.nq;
+    next_i += stride;
+    prefetch(A);
+    return true;
+  }
+  __device__ __forceinline__ bool valid() const { return ok; }
+  __device__ __forceinline__ const uint32_t *x_comp(const EnumArgs &A) const {
+    return d.side ? A.tab[2].comp : A.tab[0].comp;
+  }
+  __device__ __forceinline__ const uint32_t *y_comp(const EnumArgs &A) const {
+    return d.side ? A.tab[3].comp : A.tab[1].comp;
+  }
+  __device__ __forceinline__ const uint32_t *lane_comp(const EnumArgs &A) const {
+    return R.lane_is_x() ? x_comp(A) : y_comp(A);
+  }
+  __device__ __forceinline__ const uint32_t *loop_comp(const EnumArgs &A) const {
+    return R.lane_is_x() ? y_comp(A) : x_comp(A);
+  }
+  // Next tile; returns true when the unit may have changed (caller flushes per-unit counters).
+  __device__ __forceinline__ bool advance(const EnumArgs &A, uint32_t lane, uint32_t &old_gid) {
+    old_gid = d.gid;
+    if (++t < tend) {
+      if (++qc == R.nq) { qc = 0; ++lc; }
+      return false;
+    }
+    const uint32_t old_gs = R.gs();
+    grab(A, lane);
+    return !ok || R.gs() != old_gs;
   }
 };
 
@@ -105,8 +169,8 @@ struct TileCursor {
   uint32_t *ybuf;  // kTQ * SW words of shared memory owned by this warp
 };
 
-template <int MC>
-__device__ __forceinline__ void begin_tile(const EnumArgs &A, const TileWalker &W, uint32_t lane,
+template <int MC, class Walker>
+__device__ __forceinline__ void begin_tile(const EnumArgs &A, const Walker &W, uint32_t lane,
                                            TileCursor<stride_for(MC)> &C) {
   constexpr int SW = stride_for(MC);
   const RectDesc &R = W.R;
@@ -146,8 +210,8 @@ __device__ __forceinline__ void lds_vec(const uint32_t *p, uint32_t (&v)[SW]) {
 // order.  ok is false for lanes past the run end and for right pairs that overshoot d (counted into
 // `filt` when the unit counts filters).  The kU entries are folded together so each thread carries
 // kU independent FNV chains (the fold itself is a serial dependency chain).
-template <int MC, class Fn>
-__device__ __forceinline__ void step_keys(const TileWalker &W, TileCursor<stride_for(MC)> &C,
+template <int MC, class Walker, class Fn>
+__device__ __forceinline__ void step_keys(const Walker &W, TileCursor<stride_for(MC)> &C,
                                           const uint32_t (&dg)[words_for(MC) > 0 ? words_for(MC) : 1],
                                           unsigned long long &filt, Fn &&fn) {
   constexpr int NW0 = words_for(MC);           // companion words (0 when m == 1)
