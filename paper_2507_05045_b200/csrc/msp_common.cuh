@@ -95,6 +95,7 @@ struct EnumArgs {
   uint64_t item_lo, item_hi; // this launch's item range
   uint32_t gs_base;          // units[gs - gs_base] describes the unit of an item's rectangle
   unsigned long long *item_ctr;  // dynamic item counter of this launch (zeroed per solve)
+  uint32_t diag;             // MSP_FLAG_DIAG_HASH_ONLY: hash without staging (timing only)
   unsigned long long *batch_filtered; // per batch (gid)
   unsigned long long *batch_hits;     // per batch (gid)
 };

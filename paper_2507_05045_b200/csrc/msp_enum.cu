@@ -166,12 +166,78 @@ __device__ __forceinline__ void sink_batch(const JoinTable &jt, const UnitDesc &
   }
 }
 
+// Bulk table operations for one unit's staged keys (one warp): 8 keys per lane are loaded from
+// the warp's shared-memory stage and their CAS / loads are all issued before any result is used,
+// so each warp keeps 256 L2 operations in flight while the other warps keep hashing.
+template <int KIND>
+__device__ __forceinline__ void sink_bulk(const JoinTable &jt, const UnitDesc &d, const unsigned long long *stage,
+                                          uint32_t cnt, uint32_t lane, unsigned long long &hits) {
+  constexpr int V = 8;
+  const uint32_t mask = (1u << d.region_log2) - 1;
+  unsigned long long *K = jt.keys + d.region_base;
+  for (uint32_t j0 = 0; j0 < cnt; j0 += 32 * V) {
+    unsigned long long k[V];
+    uint32_t s[V];
+    unsigned long long r[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const uint32_t j = j0 + u * 32 + lane;
+      k[u] = j < cnt ? stage[j] : 0ull;
+      s[u] = home_slot(k[u], d.region_log2);
+    }
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const bool live = j0 + u * 32 + lane < cnt && k[u] != 0;
+      if constexpr (KIND == SINK_BUILD) r[u] = live ? atomicCAS(K + s[u], 0ull, k[u]) : 0ull;
+      else r[u] = live ? K[s[u]] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      if (j0 + u * 32 + lane >= cnt) continue;
+      if constexpr (KIND == SINK_BUILD) {
+        if (k[u] == 0) { atomicAdd(jt.zero + d.slot, 1ull); continue; }
+        if (r[u] == 0) continue;
+        if (r[u] == k[u]) { count_duplicate(jt, d.region_base + s[u]); continue; }
+        uint32_t t = (s[u] + 1) & mask;
+        bool placed = false;
+        for (uint32_t p = 0; p < mask; ++p) {
+          const unsigned long long o = atomicCAS(K + t, 0ull, k[u]);
+          if (o == 0) { placed = true; break; }
+          if (o == k[u]) { count_duplicate(jt, d.region_base + t); placed = true; break; }
+          t = (t + 1) & mask;
+        }
+        if (!placed) atomicOr(jt.err, 1);
+      } else {
+        if (k[u] == 0) {
+          const unsigned long long z = jt.zero[d.slot];
+          if (z) {
+            hits += z;
+            if (atomicExch(jt.zero_hit + d.slot, 1u) == 0u) {
+              const unsigned long long i = atomicAdd(jt.nhits, 1ull);
+              if (i < jt.hit_cap) jt.hits[i] = HitRec{d.gid, 0u, 0ull};
+            }
+          }
+          continue;
+        }
+        if (r[u] == k[u]) { register_hit(jt, d.gid, d.region_base + s[u], k[u], hits); continue; }
+        if (r[u] == 0) continue;
+        uint32_t slot;
+        if (table_find(jt, d, k[u], (s[u] + 1) & mask, slot)) register_hit(jt, d.gid, slot, k[u], hits);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- enumeration kernel
+
+constexpr uint32_t kEnumStage = 512;  // keys a warp stages before a bulk table pass
 
 template <int MC, int KIND>
 __global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTable jt) {
   constexpr int NW = words_for(MC);
-  const uint32_t lane = threadIdx.x & 31;
+  constexpr bool kBulk = KIND == SINK_BUILD || KIND == SINK_PROBE;
+  const uint32_t lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
   const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t dg[NW > 0 ? NW : 1];
@@ -179,31 +245,59 @@ __global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTab
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
 
   __shared__ __align__(16) uint32_t ybuf_all[8][kTQ * stride_for(MC)];
+  __shared__ unsigned long long stage_all[kBulk ? 8 : 1][kBulk ? kEnumStage : 1];
+  unsigned long long *stage = stage_all[kBulk ? wl : 0];
   for (uint64_t chunk = wid; chunk < A.nchunks; chunk += nwarps) {
     TileWalker W;
     W.init(A, chunk * A.chunk_tiles, min(chunk * A.chunk_tiles + A.chunk_tiles, A.total_tiles));
     unsigned long long filt = 0, hits = 0;
+    uint32_t cnt = 0;
     TileCursor<stride_for(MC)> C;
-    C.ybuf = ybuf_all[threadIdx.x >> 5];
+    C.ybuf = ybuf_all[wl];
     while (W.valid()) {
       begin_tile<MC>(A, W, lane, C);
       while (C.q < C.q1) {
-        uint64_t kk[kU];
-        bool okk[kU];
-        uint32_t li[kU], qi[kU];
+        if constexpr (kBulk) {
+          step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
+            if (ok && W.d.npass > 1 && pass_of(key, W.d.npass) != W.d.pass) ok = false;
+            const uint32_t m = __ballot_sync(0xffffffffu, ok);
+            if (ok) stage[cnt + __popc(m & lt_mask)] = key;
+            cnt += __popc(m);
+          });
+          if (cnt + 32 * kU > kEnumStage) {
+            __syncwarp();
+            sink_bulk<KIND>(jt, W.d, stage, cnt, lane, hits);
+            __syncwarp();
+            cnt = 0;
+          }
+        } else {
+          uint64_t kk[kU];
+          bool okk[kU];
+          uint32_t li[kU], qi[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) { okk[u] = false; kk[u] = 0; li[u] = qi[u] = 0; }
-        step_keys<MC>(W, C, dg, filt, [&](int u, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
-          kk[u] = key; okk[u] = ok; li[u] = lidx; qi[u] = qidx;
-        });
-        sink_batch<KIND>(jt, W.d, kk, okk, W.R, li, qi, A, hits);
+          for (int u = 0; u < kU; ++u) { okk[u] = false; kk[u] = 0; li[u] = qi[u] = 0; }
+          step_keys<MC>(W, C, dg, filt, [&](int u, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
+            kk[u] = key; okk[u] = ok; li[u] = lidx; qi[u] = qidx;
+          });
+          sink_batch<KIND>(jt, W.d, kk, okk, W.R, li, qi, A, hits);
+        }
       }
+      const UnitDesc dprev = W.d;
       uint32_t old;
-      if (W.advance(A, old)) {
+      const bool changed = W.advance(A, old);
+      if constexpr (kBulk) {
+        if ((changed || !W.valid()) && cnt) {  // the stage holds one unit's keys
+          __syncwarp();
+          sink_bulk<KIND>(jt, dprev, stage, cnt, lane, hits);
+          __syncwarp();
+          cnt = 0;
+        }
+      }
+      if (changed) {
         const unsigned long long f = warp_sum(filt), h = warp_sum(hits);
         if (lane == 0) {
-          if (f) atomicAdd(A.batch_filtered + A.units[old].gid, f);
-          if (h) atomicAdd(A.batch_hits + A.units[old].gid, h);
+          if (f) atomicAdd(A.batch_filtered + dprev.gid, f);
+          if (h) atomicAdd(A.batch_hits + dprev.gid, h);
         }
         filt = hits = 0;
       }
@@ -214,6 +308,19 @@ __global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTab
       if (h) atomicAdd(A.batch_hits + W.d.gid, h);
     }
   }
+}
+
+// Table clear with ordinary 16-byte stores so the cleared lines stay resident in L2 for the build
+// (a DMA memset does not leave the 64 MB table in L2; measured 33% L2 hit rate on the CAS).
+__global__ void k_clear(uint4 *p, size_t n16) {
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) p[i] = z;
+}
+
+void launch_clear(void *p, size_t bytes, int num_sms, cudaStream_t st) {
+  const size_t n16 = bytes / 16;
+  if (n16) k_clear<<<num_sms * 4, 512, 0, st>>>(reinterpret_cast<uint4 *>(p), n16);
+  if (bytes % 16) cudaMemsetAsync(reinterpret_cast<char *>(p) + n16 * 16, 0, bytes % 16, st);
 }
 
 template <int MC>

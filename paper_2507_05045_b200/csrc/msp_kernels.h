@@ -109,6 +109,8 @@ struct RescatterArgs { const RescatterSrc *src; uint32_t nsrc; uint64_t total; }
 cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st);
 cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 
+void launch_clear(void *p, size_t bytes, int num_sms, cudaStream_t st);
+
 enum SinkKind { SINK_BUILD = 0, SINK_PROBE = 1, SINK_RECOVER = 2, SINK_NONE = 3 /* diagnostic: hash only */ };
 // Enumerate every pair of the launch's units, hash it, and hand the key to the sink.
 int launch_enum(int mc, SinkKind kind, const EnumArgs &args, const JoinTable &jt, int num_sms,

@@ -122,6 +122,7 @@ __device__ __forceinline__ void flush_round(const Stage &g, const PartArgs &S, u
     }
     run += hv[k];
   }
+#ifndef MSP_SCATTER_DIRECT
   uint32_t total = 0;
   for (int w = 0; w < kScatterWarps; ++w) total += g.warp_tot[w];
   __syncthreads();
@@ -138,6 +139,15 @@ __device__ __forceinline__ void flush_round(const Stage &g, const PartArgs &S, u
     if (!g.ovf[b]) S.scratch[g.abase[b] + pos] = g.sorted[pos];
   }
   __syncthreads();
+#else
+  __syncthreads();
+  for (uint32_t j = lane; j < cnt; j += 32) {  // direct: each key to its final slot
+    const uint32_t i = warp * kWarpStage + j;
+    const uint16_t b = g.sbkt[i];
+    if (!g.ovf[b]) S.scratch[g.abase[b] + g.off[b] + g.rank[i]] = g.skey[i];
+  }
+  __syncthreads();
+#endif
 }
 
 template <int MC, bool ITEMS>
@@ -174,15 +184,21 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A
   bool have;
   if constexpr (ITEMS) have = W.grab(A, lane); else have = W.valid();
   if (have) begin_tile<MC>(A, W, lane, C);
-  unsigned long long filt = 0;
+  unsigned long long filt = 0, diag_acc = 0;
   while (true) {
     uint32_t cnt = 0;
     while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
       const uint32_t bbase = ((W.d.flags >> 1) & 1u) * nbw + W.d.region_base;
       const uint32_t bits = W.d.region_log2;
-      step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
-        stage_key(g, warp, lt_mask, cnt, key, bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u), ok);
-      });
+      if (A.diag) {  // diagnostic timing: hash only, no staging / partition
+        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
+          if (ok) diag_acc ^= key;
+        });
+      } else {
+        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
+          stage_key(g, warp, lt_mask, cnt, key, bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u), ok);
+        });
+      }
       if (C.q >= C.q1) {
         uint32_t old_gid;
         bool changed;
@@ -210,6 +226,7 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A
     if (!__syncthreads_or(cnt > 0)) break;
     flush_round(g, S, cnt);
   }
+  if (diag_acc == 0x123456789ull) A.batch_filtered[0] = diag_acc;  // keep the diagnostic keys live
 }
 
 // Level 2 of the huge-batch path: stream already-hashed keys back from coarse bucket regions

@@ -573,6 +573,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   jt.hit_cap = hit_cap;
   jt.err = D.err.as<int>();
   EnumArgs A = P.base;
+  A.diag = (opt->flags & MSP_FLAG_DIAG_HASH_ONLY) ? 1u : 0u;
   A.batch_filtered = D.bfilt.as<unsigned long long>();
   A.batch_hits = D.bhits.as<unsigned long long>();
   double hot_ms = 0;
@@ -1114,7 +1115,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     const UnitDesc *udev = D.units.as<UnitDesc>();
     for (size_t wi = 0; wi < waves.size(); ++wi) {
       const Wave &w = waves[wi];
-      CK(cudaMemsetAsync(D.keys.p, 0, 8 * w.slots, st));
+      launch_clear(D.keys.p, 8 * w.slots, D.num_sms, st);
       if (++D.epoch >= (1ull << 24)) {  // tag space exhausted: clear and restart
         CK(cudaMemsetAsync(D.cnt.p, 0, D.cnt.cap, st));
         D.epoch = 1;
