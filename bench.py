@@ -295,7 +295,7 @@ def main() -> int:
     achieved_hbm = 8.0 * hot_pairs / (hot_ms * 1e-3) / 1e9 if hot_ms else None
     roofline = {
         "bound": "int32",
-        "kernel": "k_enum (build+probe join waves)",
+        "kernel": "k_scatter + k_join (one partitioned join wave = scatter launch + join launch)",
         "achieved": achieved_int, "peak": int_peak / 1e9 if int_peak > 0 else None,
         "unit": "Gop/s", "frac": (achieved_int / (int_peak / 1e9)) if (achieved_int and int_peak > 0) else None,
         "peak_source": "measured on this GPU: msp_int32_peak (FNV fold instruction mix)",
@@ -304,6 +304,14 @@ def main() -> int:
                        "pairs": hot_pairs},
         "traffic": None,
     }
+    try:  # DRAM bytes per wave from the committed ncu --set full capture (profiles/README.md)
+        with open(os.path.join(HERE, "profiles", "r1_kernels.json")) as fh:
+            tr = json.load(fh)["traffic"]
+        roofline["traffic"] = {"dram_bytes_per_wave": tr["wave_dram_bytes"],
+                               "algorithmic_bytes_per_wave": tr["algorithmic_bytes_per_wave"],
+                               "source": tr["source"]}
+    except (OSError, KeyError, ValueError):
+        pass
     roofline_hbm = {"bound": "hbm", "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_hbm / hbm_peak if achieved_hbm else None,
                     "algorithmic_bytes_per_pair": 8,
