@@ -272,59 +272,135 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_rescatter(const Rescatte
 }
 
 constexpr int kJoinThreads = 1024;
-constexpr int kJoinSlots = 1 << kJoinSlotsLog2;
+constexpr int kJoinSlots = 1 << kJoinSlotsLog2;        // 16K key slots
+constexpr int kJBuckets = kJoinSlots / 4;               // 4K buckets of 4 slots
+constexpr int kStash = 256;                             // keys whose two buckets were both full
+constexpr int kHitWords = (kJoinSlots + kStash) / 32;
 
-size_t join_smem_bytes() { return (size_t)kJoinSlots * 12 + 64; }
+// Shared-memory join table of one bucket: two-choice hashing into 4-slot buckets.  Each slot keeps
+// the full 64-bit key and, in a packed word per bucket, a 16-bit fingerprint, so a probe reads two
+// fingerprint words and two counts and compares four fingerprints per word with one SIMD compare;
+// the full keys are read only on a fingerprint match (~1e-4 of probes plus the true hits).  No
+// probe ever loops, so warps do not diverge on chain lengths.  Only the counts are cleared per
+// bucket (slots past a bucket's count are never read).
+struct JoinSmem {
+  unsigned long long key[kJBuckets][4];
+  unsigned long long fp[kJBuckets];     // four 16-bit fingerprints
+  uint32_t cnt[kJBuckets];              // claims (may exceed 4: failed claims spill over)
+  unsigned long long stash[kStash];
+  uint32_t hitbits[kHitWords];
+  unsigned long long bhits[kJoinThreads / 32];
+  uint32_t nstash, zb, zhit, ovf;
+};
+
+size_t join_smem_bytes() { return sizeof(JoinSmem); }
+
+struct JoinHash { uint32_t b1, b2, fp; };
+__device__ __forceinline__ JoinHash join_hash(unsigned long long k) {
+  const unsigned long long m = k * kGolden;  // odd multiplier: a bijection on 64-bit keys
+  JoinHash h;
+  h.b1 = (uint32_t)(m >> 52);
+  h.b2 = (uint32_t)(m >> 40) & (kJBuckets - 1);
+  if (h.b2 == h.b1) h.b2 ^= 1u;
+  h.fp = (uint32_t)(m >> 24) & 0xFFFFu;
+  return h;
+}
+
+// Lanes of `w` (four 16-bit fingerprints) equal to fp, as a 4-bit mask, restricted to n slots.
+__device__ __forceinline__ uint32_t fp_match(unsigned long long w, uint32_t fp, uint32_t n) {
+  const uint32_t f2 = fp * 0x10001u;
+  const uint32_t lo = __vcmpeq2((uint32_t)w, f2), hi = __vcmpeq2((uint32_t)(w >> 32), f2);
+  const uint32_t m = (lo & 1u) | ((lo >> 15) & 2u) | ((hi & 1u) << 2) | ((hi >> 13) & 8u);
+  return m & ((1u << n) - 1u);
+}
+
+__device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
+  const JoinHash h = join_hash(k);
+  const uint32_t c1 = T.cnt[h.b1], c2 = T.cnt[h.b2];
+  uint32_t b = c1 <= c2 ? h.b1 : h.b2, o = c1 <= c2 ? h.b2 : h.b1;
+  uint32_t s = atomicAdd(&T.cnt[b], 1u);
+  if (s >= 4) { b = o; s = atomicAdd(&T.cnt[b], 1u); }
+  if (s < 4) {
+    T.key[b][s] = k;
+    atomicOr(reinterpret_cast<unsigned long long *>(&T.fp[b]), (unsigned long long)h.fp << (16 * s));
+  } else {
+    const uint32_t i = atomicAdd(&T.nstash, 1u);
+    if (i < (uint32_t)kStash) T.stash[i] = k; else T.ovf = 1u;
+  }
+}
+
+// Multiplicity of k in the table; *first = slot id of its first copy (bucket-major, then stash).
+__device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long long k, uint32_t nstash,
+                                               uint32_t &first) {
+  const JoinHash h = join_hash(k);
+  const uint32_t n1 = min(T.cnt[h.b1], 4u), n2 = min(T.cnt[h.b2], 4u);
+  uint32_t m1 = fp_match(T.fp[h.b1], h.fp, n1), m2 = fp_match(T.fp[h.b2], h.fp, n2);
+  uint32_t c = 0;
+  first = 0xFFFFFFFFu;
+  if (m1 | m2) {  // rare: fingerprint hit, compare full keys
+    while (m1) {
+      const uint32_t s = __ffs(m1) - 1;
+      m1 &= m1 - 1;
+      if (T.key[h.b1][s] == k) { if (!c) first = h.b1 * 4 + s; ++c; }
+    }
+    while (m2) {
+      const uint32_t s = __ffs(m2) - 1;
+      m2 &= m2 - 1;
+      if (T.key[h.b2][s] == k) { if (!c) first = h.b2 * 4 + s; ++c; }
+    }
+  }
+  for (uint32_t i = 0; i < nstash; ++i)
+    if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
+  return c;
+}
 
 __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long *tk = reinterpret_cast<unsigned long long *>(smem);
-  uint32_t *tc = reinterpret_cast<uint32_t *>(tk + kJoinSlots);
-  __shared__ unsigned int zb, zhit;
-  __shared__ unsigned long long bhits[kJoinThreads / 32];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  JoinSmem &T = *reinterpret_cast<JoinSmem *>(smem_raw);
   const uint32_t tid = threadIdx.x;
-  constexpr uint32_t mask = kJoinSlots - 1;
+  constexpr int U = 8;  // keys loaded per thread before the table operations
 
   for (uint32_t b = blockIdx.x; b < S.nb; b += gridDim.x) {
-    for (uint32_t i = tid; i < kJoinSlots; i += kJoinThreads) { tk[i] = 0ull; tc[i] = 0u; }
-    if (tid == 0) { zb = 0; zhit = 0; }
-    __syncthreads();
+    for (uint32_t i = tid; i < (uint32_t)kJBuckets; i += kJoinThreads) { T.cnt[i] = 0u; T.fp[i] = 0ull; }
+    for (uint32_t i = tid; i < (uint32_t)kHitWords; i += kJoinThreads) T.hitbits[i] = 0u;
+    if (tid == 0) { T.nstash = 0; T.zb = 0; T.zhit = 0; T.ovf = 0; }
     const uint32_t gid = __ldg(S.gid + b);
     const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
+    const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
     const unsigned long long *bk = S.scratch + __ldg(S.start[0] + b);
-    constexpr int U = 8;  // keys prefetched per thread before the table operations
-    for (uint32_t base = 0; base < nbuild; base += kJoinThreads * U) {
-      unsigned long long kv[U];
+    const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
+    unsigned long long kv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t i = base + u * kJoinThreads + tid;
-        kv[u] = i < nbuild ? bk[i] : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const unsigned long long k = kv[u];
-        if (base + u * kJoinThreads + tid >= nbuild) continue;
-        if (k == 0) { atomicAdd(&zb, 1u); continue; }
-        uint32_t s = (uint32_t)((k * kGolden) >> (64 - kJoinSlotsLog2));
-        for (uint32_t p = 0; p <= mask; ++p) {
-          const unsigned long long old = atomicCAS(tk + s, 0ull, k);
-          if (old == 0ull) break;
-          if (old == k) { atomicAdd(tc + s, 1u); break; }
-          s = (s + 1) & mask;
-        }
-      }
+    for (int u = 0; u < U; ++u) {  // first build keys in flight across the clear
+      const uint32_t i = u * kJoinThreads + tid;
+      kv[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
     }
     __syncthreads();
-    const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
-    const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
-    unsigned long long hits = 0;
-    for (uint32_t base = 0; base < nprobe; base += kJoinThreads * U) {
-      unsigned long long kv[U];
+    for (uint32_t base = 0; base < nbuild; base += kJoinThreads * U) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint32_t i = base + u * kJoinThreads + tid;
-        kv[u] = i < nprobe ? pk[i] : 0ull;
+        if (base + u * kJoinThreads + tid >= nbuild) continue;
+        if (kv[u] == 0) { atomicAdd(&T.zb, 1u); continue; }
+        join_insert(T, kv[u]);
       }
+      const uint32_t nb2 = base + kJoinThreads * U;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = nb2 + u * kJoinThreads + tid;
+        kv[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {  // first probe keys in flight across the barrier
+      const uint32_t i = u * kJoinThreads + tid;
+      kv[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
+    }
+    __syncthreads();
+    const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
+    const uint32_t zb = T.zb;
+    if (T.ovf && tid == 0) atomicOr(S.batch_ovf + gid, 1u);
+    unsigned long long hits = 0;
+    for (uint32_t base = 0; base < nprobe; base += kJoinThreads * U) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const unsigned long long k = kv[u];
@@ -332,36 +408,36 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
         if (k == 0) {
           if (zb) {
             hits += zb;
-            if (atomicExch(&zhit, 1u) == 0u) {
+            if (atomicExch(&T.zhit, 1u) == 0u) {
               const unsigned long long h = atomicAdd(S.nhits, 1ull);
               if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, 0ull};
             }
           }
           continue;
         }
-        uint32_t s = (uint32_t)((k * kGolden) >> (64 - kJoinSlotsLog2));
-        for (uint32_t p = 0; p <= mask; ++p) {
-          const unsigned long long t = tk[s];
-          if (t == k) {
-            const uint32_t c = tc[s];
-            hits += (c & ~kOvf) + 1;
-            if (!(c & kOvf) && !(atomicOr(tc + s, kOvf) & kOvf)) {
-              const unsigned long long h = atomicAdd(S.nhits, 1ull);
-              if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
-            }
-            break;
+        uint32_t first;
+        const uint32_t c = join_count(T, k, nstash, first);
+        if (c) {
+          hits += c;
+          if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
+            const unsigned long long h = atomicAdd(S.nhits, 1ull);
+            if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
           }
-          if (t == 0ull) break;
-          s = (s + 1) & mask;
         }
+      }
+      const uint32_t nb2 = base + kJoinThreads * U;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = nb2 + u * kJoinThreads + tid;
+        kv[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
       }
     }
     hits = warp_sum(hits);
-    if ((tid & 31) == 0) bhits[tid >> 5] = hits;
+    if ((tid & 31) == 0) T.bhits[tid >> 5] = hits;
     __syncthreads();
     if (tid == 0) {
       unsigned long long t = 0;
-      for (int w = 0; w < kJoinThreads / 32; ++w) t += bhits[w];
+      for (int w = 0; w < kJoinThreads / 32; ++w) t += T.bhits[w];
       if (t) atomicAdd(S.batch_hits + gid, t);
       S.fill[0][b] = 0;
       S.fill[1][b] = 0;
