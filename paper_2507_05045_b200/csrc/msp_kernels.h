@@ -94,8 +94,39 @@ struct PartArgs {
   unsigned int *batch_ovf;    // per batch: a bucket overflowed -> re-join with the global table
   HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;
   unsigned long long *batch_hits;
+  uint32_t sink;              // scratch index of kSinkSlots slots nobody reads: dropped runs land there
 };
-cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int num_sms, cudaStream_t st);
+constexpr uint32_t kSinkSlots = 8192;  // >= keys of one scatter round
+// One (batch, side) unit of a scatter launch, kept in shared memory by k_scatter.
+constexpr int kMaxUnits = 128;         // units per scatter launch (64 batches per wave)
+struct UnitInfo {
+  uint32_t h0lo, h0hi;                 // FNV state after coordinate 0 (alpha)
+  uint32_t ent;                        // first (role, bucket) entry | bucket bits << 12 | side << 16
+  uint32_t gid;                        // batch index within the solve
+};
+// One warp tile: up to 32 lane entries x up to 32 loop entries of one rectangle (16 B, one load).
+struct TileDesc {
+  uint32_t lane0, loop0;               // first lane entry / first loop entry (table indices)
+  uint32_t meta;                       // unit | (lane_n - 1) << 8 | (loop_n - 1) << 13 | lane_is_x << 18
+  uint32_t pad;
+};
+struct TileGenArgs {
+  const RectDesc *rects; uint32_t rect_lo, rect_hi;  // rectangles to expand (global indices)
+  const uint64_t *gs_tile_base;        // by (batch, side): first tile in `out` (nullptr: 0)
+  const uint32_t *gs_unit;             // by (batch, side): unit within its scatter launch, or
+                                       // 0xFFFFFFFF to skip the rectangle (nullptr: unit 0)
+  TileDesc *out;
+};
+void launch_tiles(const TileGenArgs &a, cudaStream_t st);
+struct ScatterArgs {
+  const uint32_t *comp[4];             // companion tables A, B, C, D
+  uint32_t dpack[8];                   // d rows 1..m-1 packed, +0x8000 guard per half
+  const TileDesc *tiles; uint32_t ntiles;
+  const UnitInfo *units; uint32_t nunits;
+  unsigned long long *batch_filtered;  // per batch (gid)
+  uint32_t diag;                       // MSP_FLAG_DIAG_HASH_ONLY: hash without staging
+};
+cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, int num_sms, cudaStream_t st);
 // Huge batches, level 2: re-partition coarse bucket regions (already hashed keys) into fine buckets.
 struct RescatterSrc {
   const unsigned long long *keys;  // coarse bucket region

@@ -25,68 +25,82 @@
 namespace msp {
 
 constexpr int kScatterWarps = 16;
-constexpr int kWarpStage = 512;                         // keys a warp stages per round
+constexpr int kWarpStage = 448;                         // keys a warp stages per round
 constexpr int kStage = kScatterWarps * kWarpStage;      // keys staged per CTA round
-constexpr uint32_t kOvf = 0x80000000u;
 constexpr int kHistEntries = 2 * kMaxWaveBuckets;       // (role, bucket)
+constexpr int kPer = kHistEntries / (kScatterWarps * 32);
 
-size_t scatter_smem_bytes() {
-  return (size_t)kStage * (8 + 8 + 2 + 2 + 2) + (size_t)kHistEntries * 4 * 3 + 64;
+// Reservation of n slots at *p, result left in flight in r (predicated: no-op when n == 0, so no
+// select has to wait for the atomic's return value).
+__device__ __forceinline__ void reserve_async(uint32_t &r, uint32_t *p, uint32_t n) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q atom.global.add.u32 %0, [%1], %2;\n\t}"
+               : "+r"(r)
+               : "l"(p), "r"(n)
+               : "memory");
 }
 
-// Shared-memory views of one CTA's staging area.
+// Shared memory of a scatter CTA (k_scatter / k_rescatter); the producers' loop-vector buffers
+// follow it (k_scatter only).
 struct Stage {
-  unsigned long long *skey, *sorted;
-  uint16_t *sbkt, *rank, *sortb;
-  uint32_t *hist, *off, *abase;
-  uint8_t *ovf;
-  uint32_t *warp_tot;
+  unsigned long long skey[kStage];   // staged keys (warp-private slot ranges)
+  unsigned long long sorted[kStage]; // the round's keys sorted by (role, bucket)
+  uint16_t sbkt[kStage], rank[kStage], sortb[kStage];
+  uint32_t hist[kHistEntries];       // keys per entry in the round being filled
+  uint32_t off[kHistEntries];        // sorted position of each entry's run
+  uint32_t abase[kHistEntries];      // scratch index of sorted position 0 of the run, or kDrop
+  uint32_t est[kHistEntries];        // scratch start of each entry's bucket region
+  uint32_t ecap[kHistEntries];       // its capacity
+  UnitInfo units[kMaxUnits];
+  uint32_t warp_tot[kScatterWarps];
 };
 
-__device__ __forceinline__ Stage stage_views(unsigned char *smem, uint8_t *ovf, uint32_t *warp_tot) {
-  Stage g;
-  g.skey = reinterpret_cast<unsigned long long *>(smem);
-  g.sorted = g.skey + kStage;
-  g.sbkt = reinterpret_cast<uint16_t *>(g.sorted + kStage);
-  g.rank = g.sbkt + kStage;
-  g.sortb = g.rank + kStage;
-  g.hist = reinterpret_cast<uint32_t *>(g.sortb + kStage);
-  g.off = g.hist + kHistEntries;
-  g.abase = g.off + kHistEntries;
-  g.ovf = ovf;
-  g.warp_tot = warp_tot;
-  return g;
+size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kU) * sw * 4; }
+
+__device__ __forceinline__ void stage_init(Stage &g, const PartArgs &S, const UnitInfo *units, uint32_t nunits) {
+  const uint32_t nbw = S.nb;
+  for (uint32_t i = threadIdx.x; i < kHistEntries; i += blockDim.x) g.hist[i] = 0;
+  for (uint32_t j = threadIdx.x; j < 2 * nbw; j += blockDim.x) {
+    const uint32_t role = j >= nbw, b = j - role * nbw;
+    g.est[j] = __ldg((role ? S.start[1] : S.start[0]) + b);
+    g.ecap[j] = __ldg((role ? S.cap[1] : S.cap[0]) + b);
+  }
+  for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) g.units[u] = units[u];
 }
 
 // Append one warp-step of keys densely to the warp's stage (ballot + popc) and rank each key
-// within its (role, bucket) with one shared-memory atomic.
-__device__ __forceinline__ void stage_key(const Stage &g, uint32_t warp, uint32_t lane_lt, uint32_t &cnt,
-                                          uint64_t key, uint32_t b, bool ok) {
+// within its (role, bucket) entry with one shared-memory atomic.
+__device__ __forceinline__ void stage_key(Stage &g, uint32_t warp, uint32_t lane_lt, uint32_t &cnt,
+                                          uint64_t key, uint32_t e, bool ok) {
   const uint32_t m = __ballot_sync(0xffffffffu, ok);
   if (ok) {
     const uint32_t pos = warp * kWarpStage + cnt + __popc(m & lane_lt);
     g.skey[pos] = key;
-    g.sbkt[pos] = (uint16_t)b;
-    g.rank[pos] = (uint16_t)atomicAdd(g.hist + b, 1u);
+    g.sbkt[pos] = (uint16_t)e;
+    g.rank[pos] = (uint16_t)atomicAdd(g.hist + e, 1u);
   }
   cnt += __popc(m);
 }
 
-// After a __syncthreads: scan the round's bucket counts, reserve one global range per nonempty
-// bucket (the thread's kPer reservations are independent atomics issued back to back), reorder the
-// staged keys into bucket-sorted runs and write the runs out coalesced.  Ends synchronised, with
-// the histogram zeroed for the next round.
-__device__ __forceinline__ void flush_round(const Stage &g, const PartArgs &S, uint32_t cnt) {
+// After a __syncthreads: scan the round's entry counts and reserve one scratch range per nonempty
+// entry (global atomics, left in flight), sort each warp's staged keys into bucket-contiguous runs
+// (hiding the atomics' latency), then turn the reservations into run bases and write the runs out
+// coalesced.  The histogram is zeroed for the next fill.
+__device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_t cnt) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nbw = S.nb, nent = 2 * nbw;
-  constexpr int kPer = kHistEntries / (kScatterWarps * 32);
   const uint32_t j0 = tid * kPer;
-  uint32_t hv[kPer], local = 0;
+  uint32_t hv[kPer], gres[kPer], local = 0;
 #pragma unroll
   for (int k = 0; k < kPer; ++k) {
     hv[k] = j0 + k < nent ? g.hist[j0 + k] : 0u;
     g.hist[j0 + k] = 0u;  // ready for the next fill
     local += hv[k];
+  }
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t j = j0 + k, role = j >= nbw;
+    gres[k] = 0u;
+    reserve_async(gres[k], (role ? S.fill[1] : S.fill[0]) + (j - role * nbw), hv[k]);
   }
   uint32_t incl = local;
 #pragma unroll
@@ -95,152 +109,243 @@ __device__ __forceinline__ void flush_round(const Stage &g, const PartArgs &S, u
     if (lane >= (uint32_t)o) incl += y;
   }
   if (lane == 31) g.warp_tot[warp] = incl;
-  uint32_t gres[kPer];
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const uint32_t j = j0 + k, role = j >= nbw;
-    gres[k] = hv[k] ? atomicAdd((role ? S.fill[1] : S.fill[0]) + (j - role * nbw), hv[k]) : 0u;
-  }
   __syncthreads();
-  uint32_t run = incl - local;
-  for (uint32_t w = 0; w < warp; ++w) run += g.warp_tot[w];
+  uint32_t run = incl - local, total = 0;
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const uint32_t j = j0 + k;
-    if (j < nent) {
-      g.off[j] = run;
-      g.ovf[j] = 0;
-      if (hv[k]) {
-        const uint32_t role = j >= nbw, b = j - role * nbw;
-        if (gres[k] + hv[k] > __ldg((role ? S.cap[1] : S.cap[0]) + b)) {
-          g.ovf[j] = 1;
-          atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
-        } else {
-          g.abase[j] = __ldg((role ? S.start[1] : S.start[0]) + b) + gres[k] - run;
-        }
-      }
-    }
-    run += hv[k];
+  for (int w = 0; w < kScatterWarps; ++w) {
+    const uint32_t t = g.warp_tot[w];
+    if ((uint32_t)w < warp) run += t;
+    total += t;
   }
-#ifndef MSP_SCATTER_DIRECT
-  uint32_t total = 0;
-  for (int w = 0; w < kScatterWarps; ++w) total += g.warp_tot[w];
+  uint32_t offs[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) { offs[k] = run; g.off[j0 + k] = run; run += hv[k]; }
   __syncthreads();
-  for (uint32_t j = lane; j < cnt; j += 32) {  // each warp reorders its own staged keys
+  for (uint32_t j = lane; j < cnt; j += 32) {  // each warp sorts its own staged keys
     const uint32_t i = warp * kWarpStage + j;
     const uint16_t b = g.sbkt[i];
     const uint32_t pos = g.off[b] + g.rank[i];
     g.sorted[pos] = g.skey[i];
     g.sortb[pos] = b;
   }
-  __syncthreads();
-  for (uint32_t pos = tid; pos < total; pos += blockDim.x) {
-    const uint16_t b = g.sortb[pos];
-    if (!g.ovf[b]) S.scratch[g.abase[b] + pos] = g.sorted[pos];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const uint32_t j = j0 + k;
+    if (hv[k]) {
+      if (gres[k] + hv[k] > g.ecap[j]) {  // overflow: the run goes to the sink, the batch is re-joined
+        g.abase[j] = S.sink - offs[k];
+        const uint32_t role = j >= nbw;
+        atomicOr(S.batch_ovf + __ldg(S.gid + (j - role * nbw)), 1u);
+      } else {
+        g.abase[j] = g.est[j] + gres[k] - offs[k];
+      }
+    }
   }
   __syncthreads();
-#else
-  __syncthreads();
-  for (uint32_t j = lane; j < cnt; j += 32) {  // direct: each key to its final slot
-    const uint32_t i = warp * kWarpStage + j;
-    const uint16_t b = g.sbkt[i];
-    if (!g.ovf[b]) S.scratch[g.abase[b] + g.off[b] + g.rank[i]] = g.skey[i];
-  }
-  __syncthreads();
-#endif
+  for (uint32_t pos = tid; pos < total; pos += blockDim.x) S.scratch[g.abase[g.sortb[pos]] + pos] = g.sorted[pos];
 }
 
-template <int MC, bool ITEMS>
-__global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(const EnumArgs A, const PartArgs S) {
-  constexpr int NW = words_for(MC);
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t warp_tot[kScatterWarps];
-  __shared__ uint8_t ovf[kHistEntries];
-  __shared__ __align__(16) uint32_t ybuf_all[kScatterWarps][kTQ * stride_for(MC)];
-  const Stage g = stage_views(smem, ovf, warp_tot);
+// ---------------------------------------------------------------- tile descriptors
 
+__global__ void k_tiles(const TileGenArgs a) {
+  for (uint32_t r = a.rect_lo + blockIdx.x * blockDim.x + threadIdx.x; r < a.rect_hi; r += gridDim.x * blockDim.x) {
+    const RectDesc R = a.rects[r];
+    const uint32_t gs = R.gs();
+    const uint32_t unit = a.gs_unit ? a.gs_unit[gs] : 0u;
+    if (unit == 0xFFFFFFFFu) continue;
+    TileDesc *out = a.out + (a.gs_tile_base ? a.gs_tile_base[gs] : 0ull) + R.tile_off;
+    const uint32_t lx = R.lane_is_x() ? 1u : 0u;
+    for (uint32_t lc = 0; lc < R.nl; ++lc) {
+      const uint32_t ln = min(32u, R.L - lc * 32);
+      for (uint32_t qc = 0; qc < R.nq; ++qc) {
+        const uint32_t qn = min((uint32_t)kTQ, R.Q - qc * kTQ);
+        TileDesc t;
+        t.lane0 = R.lane_start + lc * 32;
+        t.loop0 = R.loop_start + qc * kTQ;
+        t.meta = unit | ((ln - 1) << 8) | ((qn - 1) << 13) | (lx << 18);
+        t.pad = 0;
+        *out++ = t;
+      }
+    }
+  }
+}
+
+void launch_tiles(const TileGenArgs &a, cudaStream_t st) {
+  const uint32_t n = a.rect_hi - a.rect_lo;
+  if (!n) return;
+  const uint32_t blocks = (n + 127) / 128;
+  k_tiles<<<blocks < 1184 ? blocks : 1184, 128, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------- scatter (enumerate + hash + partition)
+
+__device__ __forceinline__ uint4 ld_tile(const TileDesc *t, uint32_t i, uint32_t n) {
+  return i < n ? __ldg(reinterpret_cast<const uint4 *>(t + i)) : make_uint4(0, 0, 0, 0);
+}
+
+// FNV fold step (validate.py:40-42) on (lo, hi) for v < 2^32: (h ^ v) * (2^40 + 435) mod 2^64.
+__device__ __forceinline__ void fold(uint32_t &lo, uint32_t &hi, uint32_t v) {
+  const uint32_t x = lo ^ v;
+  hi = hi * 435u + __umulhi(x, 435u) + (x << 8);
+  lo = x * 435u;
+}
+
+// Companion-vector loads of one tile for this lane: its lane entry and its (lane-th) loop entry.
+template <int SW>
+__device__ __forceinline__ void tile_vecs(const ScatterArgs &A, const Stage &g, const uint4 d, uint32_t lane,
+                                          uint32_t (&lv)[SW], uint32_t (&yv)[SW]) {
+  const uint32_t meta = d.z;
+  const uint32_t side = (g.units[meta & 0xFFu].ent >> 16) & 1u;
+  const bool lx = (meta >> 18) & 1u;
+  const uint32_t ln = ((meta >> 8) & 31u) + 1u, qn = ((meta >> 13) & 31u) + 1u;
+  const uint32_t *lt = side ? (lx ? A.comp[2] : A.comp[3]) : (lx ? A.comp[0] : A.comp[1]);
+  const uint32_t *yt = side ? (lx ? A.comp[3] : A.comp[2]) : (lx ? A.comp[1] : A.comp[0]);
+  load_vec<SW>(lt, d.x + min(lane, ln - 1u), lv);
+  load_vec<SW>(yt, d.y + min(lane, qn - 1u), yv);
+}
+
+// kU keys of the current tile (loop entries q .. q+kU-1) into the stage.
+template <int MC, bool RIGHT>
+__device__ __forceinline__ void hash_step(Stage &g, const uint32_t *ybuf, const uint32_t (&lv)[stride_for(MC)],
+                                          const uint32_t (&dg)[words_for(MC) > 0 ? words_for(MC) : 1],
+                                          uint32_t warp, uint32_t lane_lt, uint32_t &cnt, uint32_t q, uint32_t qn,
+                                          bool lok, const UnitInfo &ui, uint32_t diag,
+                                          unsigned long long &filt, unsigned long long &dacc) {
+  constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
+  const uint32_t ebase = ui.ent & 0xFFFu, bits = (ui.ent >> 12) & 0xFu;
+  uint64_t key[kU];
+  uint32_t e[kU];
+  bool ok[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    uint32_t yv[SW];
+    lds_vec<SW>(ybuf + (q + u) * SW, yv);  // ybuf holds kTQ + kU entries: reads past qn are padding
+    uint32_t sv[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) sv[k] = lv[k] + yv[k];
+    bool in = lok && q + u < qn;
+    if (RIGHT) {
+      uint32_t acc = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < NW0; ++k) { sv[k] = dg[k] - sv[k]; acc &= sv[k]; }
+      const bool fit = (acc & 0x80008000u) == 0x80008000u;
+      filt += (in && !fit) ? 1u : 0u;
+      in = in && fit;
+    }
+    uint32_t lo = ui.h0lo, hi = ui.h0hi;
+#pragma unroll
+    for (int c = 0; c < MC; ++c) {
+      const uint32_t w = sv[c >> 1];
+      fold(lo, hi, (c & 1) ? (w >> 16) & (RIGHT ? 0x7FFFu : 0xFFFFu) : w & (RIGHT ? 0x7FFFu : 0xFFFFu));
+    }
+    key[u] = ((uint64_t)hi << 32) | lo;
+    ok[u] = in;
+    e[u] = ebase + (uint32_t)(((uint64_t)hi << bits) >> 32);  // top `bits` bits of the key
+  }
+  if (diag) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) dacc ^= ok[u] ? key[u] : 0ull;
+  } else {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) stage_key(g, warp, lane_lt, cnt, key[u], e[u], ok[u]);
+  }
+}
+
+// Enumerate + hash + partition the launch's tiles.  Each warp walks tiles warp, warp + W, ... with
+// the descriptor two tiles ahead and the companion vectors one tile ahead in flight, so a tile
+// change never waits on a load.  A full warp stage suspends the tile mid-way for a CTA round.
+template <int MC>
+__global__ void __launch_bounds__(kScatterWarps * 32, 1) k_scatter(const ScatterArgs A, const PartArgs S) {
+  constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Stage &g = *reinterpret_cast<Stage *>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  const uint32_t nbw = S.nb;
-  uint32_t dg[NW > 0 ? NW : 1];
+  const uint32_t lane_lt = (1u << lane) - 1u;
+  uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kU) * SW;
+  stage_init(g, S, A.units, A.nunits);
+  for (uint32_t i = lane; i < (uint32_t)((kTQ + kU) * SW); i += 32) ybuf[i] = 0;
+  uint32_t dg[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
-  for (uint32_t i = tid; i < kHistEntries; i += blockDim.x) g.hist[i] = 0;
   __syncthreads();
 
-  // ITEMS: one-tile work items statically strided over the grid (small waves, balanced);
-  // else: contiguous tile chunks per warp (huge batches: large chunks amortise the search).
-  using Walker = typename std::conditional<ITEMS, ItemWalker, TileWalker>::type;
-  Walker W;
-  uint64_t chunk = (uint64_t)blockIdx.x * kScatterWarps + warp;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kScatterWarps;
-  if constexpr (ITEMS) {
-    W.init(A, chunk, nwarps);
-  } else {
-    W.init(A, min(chunk * A.chunk_tiles, A.total_tiles), min(chunk * A.chunk_tiles + A.chunk_tiles, A.total_tiles));
-  }
-  TileCursor<stride_for(MC)> C;
-  C.ybuf = ybuf_all[warp];
-  bool have;
-  if constexpr (ITEMS) have = W.grab(A, lane); else have = W.valid();
-  if (have) begin_tile<MC>(A, W, lane, C);
-  unsigned long long filt = 0, diag_acc = 0;
-  while (true) {
-    uint32_t cnt = 0;
-    while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
-      const uint32_t bbase = ((W.d.flags >> 1) & 1u) * nbw + W.d.region_base;
-      const uint32_t bits = W.d.region_log2;
-      if (A.diag) {  // diagnostic timing: hash only, no staging / partition
-        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
-          if (ok) diag_acc ^= key;
-        });
-      } else {
-        step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
-          stage_key(g, warp, lt_mask, cnt, key, bbase + (bits ? (uint32_t)(key >> (64 - bits)) : 0u), ok);
-        });
+  const uint32_t nw = gridDim.x * kScatterWarps, n = A.ntiles;
+  uint32_t t = blockIdx.x * kScatterWarps + warp;
+  uint4 dcur = ld_tile(A.tiles, t, n), dnxt = ld_tile(A.tiles, t + nw, n), dnn = ld_tile(A.tiles, t + 2 * nw, n);
+  uint32_t lvc[SW], yvc[SW], lvn[SW], yvn[SW];
+  if (t < n) tile_vecs<SW>(A, g, dcur, lane, lvc, yvc);
+  if (t + nw < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
+  bool have = t < n;
+  uint32_t q = 0, qn = 0, fgid = 0xFFFFFFFFu;
+  bool lok = false, right = false;
+  UnitInfo ui{};
+  unsigned long long filt = 0, dacc = 0;
+  auto begin_tile = [&]() {
+    const uint32_t meta = dcur.z;
+    ui = g.units[meta & 0xFFu];
+    right = (ui.ent >> 16) & 1u;
+    qn = ((meta >> 13) & 31u) + 1u;
+    lok = lane <= ((meta >> 8) & 31u);
+    q = 0;
+    __syncwarp();
+    if (lane < qn) {
+#pragma unroll
+      for (int k = 0; k < SW; ++k) ybuf[lane * SW + k] = yvc[k];
+    }
+    __syncwarp();
+    if (ui.gid != fgid) {
+      if (fgid != 0xFFFFFFFFu) {
+        const unsigned long long f = warp_sum(filt);
+        if (lane == 0 && f) atomicAdd(A.batch_filtered + fgid, f);
       }
-      if (C.q >= C.q1) {
-        uint32_t old_gid;
-        bool changed;
-        if constexpr (ITEMS) {
-          changed = W.advance(A, lane, old_gid);
-        } else {
-          uint32_t old_u;
-          changed = W.advance(A, old_u);
-          old_gid = A.units[old_u].gid;
-          if (!W.valid()) {  // next contiguous chunk of this warp
-            chunk += nwarps;
-            changed = true;
-            W.init(A, min(chunk * A.chunk_tiles, A.total_tiles), min(chunk * A.chunk_tiles + A.chunk_tiles, A.total_tiles));
-          }
+      filt = 0;
+      fgid = ui.gid;
+    }
+  };
+  if (have) begin_tile();
+  uint32_t cnt = 0;
+  while (true) {
+    while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
+      if (right)
+        hash_step<MC, true>(g, ybuf, lvc, dg, warp, lane_lt, cnt, q, qn, lok, ui, A.diag, filt, dacc);
+      else
+        hash_step<MC, false>(g, ybuf, lvc, dg, warp, lane_lt, cnt, q, qn, lok, ui, A.diag, filt, dacc);
+      q += kU;
+      if (q >= qn) {  // next tile: everything it needs was loaded one (vectors) or two tiles ago
+        t += nw;
+        have = t < n;
+        if (have) {
+          dcur = dnxt;
+#pragma unroll
+          for (int k = 0; k < SW; ++k) { lvc[k] = lvn[k]; yvc[k] = yvn[k]; }
+          dnxt = dnn;
+          if (t + nw < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
+          dnn = ld_tile(A.tiles, t + 2 * nw, n);
+          begin_tile();
         }
-        if (changed) {
-          const unsigned long long f = warp_sum(filt);
-          if (lane == 0 && f) atomicAdd(A.batch_filtered + old_gid, f);
-          filt = 0;
-        }
-        have = W.valid();
-        if (have) begin_tile<MC>(A, W, lane, C);
       }
     }
     if (!__syncthreads_or(cnt > 0)) break;
     flush_round(g, S, cnt);
+    cnt = 0;
   }
-  if (diag_acc == 0x123456789ull) A.batch_filtered[0] = diag_acc;  // keep the diagnostic keys live
+  if (fgid != 0xFFFFFFFFu) {
+    const unsigned long long f = warp_sum(filt);
+    if (lane == 0 && f) atomicAdd(A.batch_filtered + fgid, f);
+  }
+  if (dacc == 0x123456789ull) A.batch_filtered[0] = dacc;  // keep the diagnostic keys live
 }
 
 // Level 2 of the huge-batch path: stream already-hashed keys back from coarse bucket regions
 // (HBM) and re-partition them into fine buckets (L2 scratch) for k_join.  Each CTA round takes
 // kStage consecutive input slots; slots past a region's fill are empty.
 __global__ void __launch_bounds__(kScatterWarps * 32) k_rescatter(const RescatterArgs R, const PartArgs S) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t warp_tot[kScatterWarps];
-  __shared__ uint8_t ovf[kHistEntries];
-  const Stage g = stage_views(smem, ovf, warp_tot);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Stage &g = *reinterpret_cast<Stage *>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
   const uint32_t nbw = S.nb;
-  for (uint32_t i = tid; i < kHistEntries; i += blockDim.x) g.hist[i] = 0;
+  stage_init(g, S, nullptr, 0);
   __syncthreads();
   for (uint64_t chunk = blockIdx.x; chunk * kStage < R.total; chunk += gridDim.x) {
     const uint64_t base = chunk * kStage + (uint64_t)warp * kWarpStage;
@@ -254,7 +359,7 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_rescatter(const Rescatte
       s = lo;
     }
     uint32_t cnt = 0;
-#pragma unroll 4
+#pragma unroll 2
     for (int k = 0; k < kWarpStage / 32; ++k) {
       const uint64_t idx = base + (uint64_t)k * 32 + lane;
       uint32_t sl = s;
@@ -262,12 +367,13 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_rescatter(const Rescatte
       const RescatterSrc &src = R.src[sl];
       const uint64_t local = idx - src.in_base;
       const bool ok = idx < R.total && local < min(*src.fill, src.cap);
-      const uint64_t key = ok ? src.keys[local] : 0ull;
+      const uint64_t key = ok ? __ldcs(src.keys + local) : 0ull;
       const uint32_t fb = src.fbits ? (uint32_t)((key << src.coarse_bits) >> (64 - src.fbits)) : 0u;
       stage_key(g, warp, lt_mask, cnt, key, src.role * nbw + src.fine_base + fb, ok);
     }
     __syncthreads();
     flush_round(g, S, cnt);
+    __syncthreads();
   }
 }
 
@@ -446,28 +552,23 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
   }
 }
 
-template <int MC, bool ITEMS>
-static cudaError_t launch_scatter_mi(const EnumArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
+template <int MC>
+static cudaError_t launch_scatter_mc(const ScatterArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
   static bool configured = false;
-  const size_t sm = scatter_smem_bytes();
+  const size_t sm = scatter_smem_bytes(stride_for(MC));
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_scatter<MC, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_scatter<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_scatter<MC, ITEMS><<<grid, kScatterWarps * 32, sm, st>>>(a, p);
+  k_scatter<MC><<<grid, kScatterWarps * 32, sm, st>>>(a, p);
   return cudaGetLastError();
 }
-template <int MC>
-static cudaError_t launch_scatter_mc(const EnumArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
-  return a.items ? launch_scatter_mi<MC, true>(a, p, grid, st) : launch_scatter_mi<MC, false>(a, p, grid, st);
-}
 
-cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int num_sms, cudaStream_t st) {
-  const uint64_t work = args.items ? args.item_hi - args.item_lo : args.nchunks;
-  if (args.items ? args.item_hi <= args.item_lo : args.nchunks == 0) return cudaSuccess;
-  const uint64_t blocks = (work + kScatterWarps - 1) / kScatterWarps;
-  const int grid = (int)(blocks < (uint64_t)num_sms ? blocks : (uint64_t)num_sms);
+cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, int num_sms, cudaStream_t st) {
+  if (args.ntiles == 0) return cudaSuccess;
+  const uint32_t blocks = (args.ntiles + kScatterWarps - 1) / kScatterWarps;
+  const int grid = (int)(blocks < (uint32_t)num_sms ? blocks : (uint32_t)num_sms);
   switch (mc) {
 #define MSP_CASE(N) case N: return launch_scatter_mc<N>(args, p, grid, st);
     MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
@@ -480,7 +581,7 @@ cudaError_t launch_scatter(int mc, const EnumArgs &args, const PartArgs &p, int 
 
 cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st) {
   static bool configured = false;
-  const size_t sm = scatter_smem_bytes();
+  const size_t sm = sizeof(Stage);
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_rescatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -86,6 +86,7 @@ struct Device {
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
   DBuf scratch2, fill2;
+  DBuf tdesc, gstb, gsu, uinfo;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
@@ -93,7 +94,7 @@ struct Device {
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
                    &bfilt, &bhits, &bovf, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
-                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2};
+                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &tdesc, &gstb, &gsu, &uinfo};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
                                   comp[i].release(); rs[i].release(); re[i].release(); }
@@ -377,6 +378,26 @@ UnitDesc make_unit(const Plan &P, uint32_t g, int side, uint64_t tile_base) {
   return u;
 }
 
+// The shared-memory unit record of k_scatter for a unit of a wave with `nb` buckets per role.
+UnitInfo make_info(const UnitDesc &u, uint32_t nb) {
+  UnitInfo i;
+  i.h0lo = (uint32_t)u.h0;
+  i.h0hi = (uint32_t)(u.h0 >> 32);
+  const uint32_t ebase = ((u.flags >> 1) & 1u) * nb + u.region_base;
+  i.ent = ebase | (u.region_log2 << 12) | (u.side << 16);
+  i.gid = u.gid;
+  return i;
+}
+
+ScatterArgs scatter_base(const Plan &P, const EnumArgs &A) {
+  ScatterArgs s{};
+  for (int t = 0; t < 4; ++t) s.comp[t] = P.base.tab[t].comp;
+  for (int k = 0; k < 8; ++k) s.dpack[k] = P.base.dpack[k];
+  s.batch_filtered = A.batch_filtered;
+  s.diag = A.diag;
+  return s;
+}
+
 void set_enum_range(EnumArgs &A, const UnitDesc *units_dev, size_t nunits, uint64_t total_tiles,
                     int num_sms) {
   A.units = units_dev;
@@ -610,8 +631,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     return MSP_OK;
   };
   auto ensure_wave_buffers = [&](uint64_t scratch_keys) -> int {
-    CK(D.scratch.ensure(8 * scratch_keys));
-    CK(D.scratch2.ensure(8 * scratch_keys));
+    CK(D.scratch.ensure(8 * (scratch_keys + kSinkSlots)));
+    CK(D.scratch2.ensure(8 * (scratch_keys + kSinkSlots)));
     void *f1 = D.fill.p, *f2 = D.fill2.p;
     CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
     CK(D.fill2.ensure(4 * 2 * kMaxWaveBuckets));
@@ -737,38 +758,36 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       part_b.push_back(g);
   }
 
-  // ---- dynamic item counters, one per scatter launch of this solve
-  const size_t n_ictr = P.G + 2 * huge_b.size() + 1;
-  CK(D.ictr.ensure(8 * n_ictr));
-  CK(cudaMemsetAsync(D.ictr.p, 0, 8 * n_ictr, st));
-  size_t ictr_next = 0;
-
   // ---- partitioned waves
   {
-    struct PWave { size_t u0, u1, b0, nb; uint64_t tiles, scratch, pairs; uint32_t g0, g1; };
+    struct PWave { size_t u0, u1, b0, nb; uint64_t t0, ntiles, scratch, pairs; uint32_t g0, g1; };
     std::vector<PWave> pw;
     std::vector<UnitDesc> units;
     std::vector<uint32_t> bstart[2], bcap[2], bgid;
-    PWave cur{0, 0, 0, 0, 0, 0, 0, 0, 0};
+    PWave cur{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     uint64_t cur_keys = 0;
+    // tile list of every partitioned batch side, in (batch, side) order
+    std::vector<uint64_t> gs_tb(2 * (size_t)P.G, 0);
+    std::vector<uint32_t> gs_unit(2 * (size_t)P.G, 0xFFFFFFFFu);
+    uint64_t all_tiles = 0;
     auto flush = [&]() {
       if (cur.nb == 0) return;
       cur.u1 = units.size();
       pw.push_back(cur);
-      cur = PWave{units.size(), units.size(), bgid.size(), 0, 0, 0, 0, 0, 0};
+      cur = PWave{units.size(), units.size(), bgid.size(), 0, all_tiles, 0, 0, 0, 0, 0};
       cur_keys = 0;
     };
     for (uint32_t g : part_b) {
-      if (cur.nb == 0) cur.g0 = g;
       const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
       const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
       const uint32_t bits = pow2ceil((nb + kBucketTarget - 1) / kBucketTarget);
       const uint32_t NB = 1u << bits;
       if (cur.nb + NB > (uint32_t)kMaxWaveBuckets || cur_keys + nb + np > key_budget ||
-          (cur.nb && g != cur.g1)) {  // waves hold consecutive batches (contiguous item ranges)
+          (cur.nb && g != cur.g1) ||  // waves hold consecutive batches (contiguous tile ranges)
+          units.size() - cur.u0 + 2 > (size_t)kMaxUnits) {
         flush();
-        cur.g0 = g;
       }
+      if (cur.nb == 0) { cur.g0 = g; cur.t0 = all_tiles; }
       const double mb = (double)nb / NB, mp = (double)np / NB;
       const uint32_t cb = (uint32_t)(mb + 7.0 * std::sqrt(mb) + 16), cp = (uint32_t)(mp + 7.0 * std::sqrt(mp) + 16);
       for (uint32_t k = 0; k < NB; ++k) {
@@ -777,12 +796,15 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         bgid.push_back(g);
       }
       for (int side = 0; side < 2; ++side) {
-        UnitDesc u = make_unit(P, g, side, cur.tiles);
+        UnitDesc u = make_unit(P, g, side, 0);
         u.region_base = cur.nb;
         u.region_log2 = bits;
         u.flags = (side == bside ? 0u : 1u) << 1;  // role: 0 build, 1 probe
-        u.count_filter = side == 1;
-        cur.tiles += P.tiles[2 * g + side];
+        const size_t gs = 2 * (size_t)g + side;
+        gs_unit[gs] = (uint32_t)(units.size() - cur.u0);
+        gs_tb[gs] = all_tiles;
+        all_tiles += P.tiles[gs];
+        cur.ntiles += P.tiles[gs];
         units.push_back(u);
       }
       cur.nb += NB;
@@ -798,13 +820,31 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       const size_t nbt = bgid.size();
       rc = ensure_wave_buffers(max_scratch);
       if (rc) return rc;
-      CK(D.units.ensure(sizeof(UnitDesc) * units.size()));
+      std::vector<UnitInfo> uinfo(units.size());
+      for (const PWave &w : pw)
+        for (size_t i = w.u0; i < w.u1; ++i) uinfo[i] = make_info(units[i], (uint32_t)w.nb);
+      CK(D.uinfo.ensure(sizeof(UnitInfo) * uinfo.size()));
+      CK(cudaMemcpyAsync(D.uinfo.p, uinfo.data(), sizeof(UnitInfo) * uinfo.size(), cudaMemcpyHostToDevice, st));
       CK(D.bk.ensure(4 * 5 * nbt));
       std::vector<uint32_t> bkimg;
       bkimg.reserve(5 * nbt);
       for (auto *v : {&bstart[0], &bstart[1], &bcap[0], &bcap[1], &bgid}) bkimg.insert(bkimg.end(), v->begin(), v->end());
       CK(cudaMemcpyAsync(D.bk.p, bkimg.data(), 4 * bkimg.size(), cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(D.units.p, units.data(), sizeof(UnitDesc) * units.size(), cudaMemcpyHostToDevice, st));
+      // K3b: every partitioned batch side's warp tiles, one launch
+      CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(all_tiles, 1)));
+      CK(D.gstb.ensure(8 * gs_tb.size()));
+      CK(D.gsu.ensure(4 * gs_unit.size()));
+      CK(cudaMemcpyAsync(D.gstb.p, gs_tb.data(), 8 * gs_tb.size(), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(D.gsu.p, gs_unit.data(), 4 * gs_unit.size(), cudaMemcpyHostToDevice, st));
+      TileGenArgs tg{};
+      tg.rects = P.base.rects;
+      tg.rect_lo = 0;
+      tg.rect_hi = P.rect_base.empty() ? 0 : P.rect_base.back() + P.nrect.back();
+      tg.gs_tile_base = D.gstb.as<uint64_t>();
+      tg.gs_unit = D.gsu.as<uint32_t>();
+      tg.out = D.tdesc.as<TileDesc>();
+      launch_tiles(tg, st);
+      ++S.kernel_launches;
       const uint32_t *bkd = D.bk.as<uint32_t>();
       PartArgs pa{};
       pa.scratch = D.scratch.as<unsigned long long>();
@@ -815,6 +855,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
+      pa.sink = (uint32_t)max_scratch;
+      ScatterArgs sa = scatter_base(P, A);
       for (size_t wi = 0; wi < pw.size(); ++wi) {
         const PWave &w = pw[wi];
         pa.start[0] = bkd + w.b0;
@@ -823,14 +865,12 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         pa.cap[1] = bkd + 3 * nbt + w.b0;
         pa.gid = bkd + 4 * nbt + w.b0;
         pa.nb = (uint32_t)w.nb;
-        set_enum_range(A, D.units.as<UnitDesc>() + w.u0, w.u1 - w.u0, w.tiles, D.num_sms);
-        A.items = D.items.as<uint64_t>();
-        A.item_lo = P.item_base[2 * (size_t)w.g0];
-        A.item_hi = P.item_base[2 * (size_t)w.g1];
-        A.gs_base = 2 * w.g0;
-        A.item_ctr = D.ictr.as<unsigned long long>() + (ictr_next++);
+        sa.tiles = D.tdesc.as<TileDesc>() + w.t0;
+        sa.ntiles = (uint32_t)w.ntiles;
+        sa.units = D.uinfo.as<UnitInfo>() + w.u0;
+        sa.nunits = (uint32_t)(w.u1 - w.u0);
         if (profile) CK(cudaEventRecord(D.pev[0], st));
-        rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_scatter(P.mc, A, p2, D.num_sms, s2); }, pa);
+        rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_scatter(P.mc, sa, p2, D.num_sms, s2); }, pa);
         if (rc) return rc;
         S.kernel_launches += 2;
         if (profile) {
@@ -884,8 +924,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         cbk[3 * NC + c] = (uint32_t)cp;
         cbk[4 * NC + c] = g;
       }
-      CK(D.cscratch[0].ensure(8 * cb * NC));
-      CK(D.cscratch[1].ensure(8 * cp * NC));
+      CK(D.cscratch[0].ensure(8 * (cb * NC + kSinkSlots)));
+      CK(D.cscratch[1].ensure(8 * (cp * NC + kSinkSlots)));
       CK(D.cbk.ensure(4 * cbk.size()));
       CK(cudaMemcpyAsync(D.cbk.p, cbk.data(), 4 * cbk.size(), cudaMemcpyHostToDevice, st));
       CK(cudaMemsetAsync(D.cfill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
@@ -900,8 +940,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         lu[role].count_filter = side == 1;
         ltiles[role] = P.tiles[2 * g + side];
       }
-      CK(D.hunits.ensure(sizeof(UnitDesc) * 2));
-      CK(cudaMemcpyAsync(D.hunits.p, lu, sizeof(UnitDesc) * 2, cudaMemcpyHostToDevice, st));
+      UnitInfo li[2] = {make_info(lu[0], NC), make_info(lu[1], NC)};
+      CK(D.hunits.ensure(sizeof(UnitInfo) * 2));
+      CK(cudaMemcpyAsync(D.hunits.p, li, sizeof(UnitInfo) * 2, cudaMemcpyHostToDevice, st));
       const uint32_t *cbkd = D.cbk.as<uint32_t>();
       PartArgs c1{};
       c1.start[0] = cbkd; c1.start[1] = cbkd + NC;
@@ -912,14 +953,25 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       c1.nb = NC;
       c1.batch_ovf = D.bovf.as<unsigned int>();
       if (profile) CK(cudaEventRecord(D.pev[0], st));
+      CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, std::max(ltiles[0], ltiles[1]))));
       for (int role = 0; role < 2; ++role) {
+        const int side = role == 0 ? bside : 1 - bside;
+        const size_t gs = 2 * (size_t)g + side;
+        TileGenArgs tg{};
+        tg.rects = P.base.rects;
+        tg.rect_lo = P.rect_base[gs];
+        tg.rect_hi = P.rect_base[gs] + P.nrect[gs];
+        tg.out = D.tdesc.as<TileDesc>();
+        launch_tiles(tg, st);
         c1.scratch = D.cscratch[role].as<unsigned long long>();
-        set_enum_range(A, D.hunits.as<UnitDesc>() + role, 1, ltiles[role], D.num_sms);
-        A.items = nullptr;  // huge batch: contiguous tile chunks
-        A.chunk_tiles = std::max<uint64_t>(1, std::min<uint64_t>(1024, ltiles[role] / ((uint64_t)D.num_sms * kScatterWarpsHost * 8)));
-        A.nchunks = (ltiles[role] + A.chunk_tiles - 1) / A.chunk_tiles;
-        CK(launch_scatter(P.mc, A, c1, D.num_sms, st));
-        ++S.kernel_launches;
+        c1.sink = (uint32_t)((role ? cp : cb) * NC);
+        ScatterArgs sa = scatter_base(P, A);
+        sa.tiles = D.tdesc.as<TileDesc>();
+        sa.ntiles = (uint32_t)ltiles[role];
+        sa.units = D.hunits.as<UnitInfo>() + role;
+        sa.nunits = 1;
+        CK(launch_scatter(P.mc, sa, c1, D.num_sms, st));
+        S.kernel_launches += 2;
       }
       // level 2 waves over the coarse buckets
       const uint32_t fbits = pow2ceil((uint64_t)std::ceil(mb / kBucketTarget));
@@ -980,6 +1032,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
+      pa.sink = (uint32_t)max_scr;
       for (size_t wi = 0; wi < lw.size(); ++wi) {
         const L2Wave &w = lw[wi];
         pa.start[0] = fb + w.b0;
