@@ -41,7 +41,7 @@ __device__ __forceinline__ void reserve_async(uint32_t &r, uint32_t *p, uint32_t
 
 // Shared memory of a scatter CTA (k_scatter / k_rescatter); the producers' loop-vector buffers
 // follow it (k_scatter only).
-struct Stage {
+struct __align__(16) Stage {
   unsigned long long skey[kStage];   // staged keys (warp-private slot ranges)
   unsigned long long sorted[kStage]; // the round's keys sorted by (role, bucket)
   uint16_t sbkt[kStage], rank[kStage], sortb[kStage];
@@ -52,6 +52,7 @@ struct Stage {
   uint32_t ecap[kHistEntries];       // its capacity
   UnitInfo units[kMaxUnits];
   uint32_t warp_tot[kScatterWarps];
+  uint32_t round_end;                // set by the first warp whose stage is full
 };
 
 size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kU) * sw * 4; }
@@ -65,6 +66,7 @@ __device__ __forceinline__ void stage_init(Stage &g, const PartArgs &S, const Un
     g.ecap[j] = __ldg((role ? S.cap[1] : S.cap[0]) + b);
   }
   for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) g.units[u] = units[u];
+  if (threadIdx.x == 0) g.round_end = 0;
 }
 
 // Append one warp-step of keys densely to the warp's stage (ballot + popc) and rank each key
@@ -304,8 +306,12 @@ __global__ void __launch_bounds__(kScatterWarps * 32, 1) k_scatter(const Scatter
   };
   if (have) begin_tile();
   uint32_t cnt = 0;
+  volatile uint32_t *round_end = &g.round_end;
   while (true) {
-    while (have && cnt + 32 * kU <= (uint32_t)kWarpStage) {
+    // a round ends as soon as one warp's stage is full: the others stop within one step, so no
+    // warp idles at the barrier while a slow one fills up
+    while (have && !*round_end) {
+      if (cnt + 32 * kU > (uint32_t)kWarpStage) { *round_end = 1u; break; }
       if (right)
         hash_step<MC, true>(g, ybuf, lvc, dg, warp, lane_lt, cnt, q, qn, lok, ui, A.diag, filt, dacc);
       else
@@ -325,7 +331,8 @@ __global__ void __launch_bounds__(kScatterWarps * 32, 1) k_scatter(const Scatter
         }
       }
     }
-    if (!__syncthreads_or(cnt > 0)) break;
+    if (!__syncthreads_or(cnt > 0 || have)) break;
+    if (tid == 0) *round_end = 0u;  // ordered before the next fill by the flush's barriers
     flush_round(g, S, cnt);
     cnt = 0;
   }
