@@ -435,7 +435,7 @@ __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   if (s >= 4) { b = o; s = atomicAdd(&T.cnt[b], 1u); }
   if (s < 4) {
     T.key[b][s] = k;
-    atomicOr(reinterpret_cast<unsigned long long *>(&T.fp[b]), (unsigned long long)h.fp << (16 * s));
+    reinterpret_cast<uint16_t *>(&T.fp[b])[s] = (uint16_t)h.fp;  // slot s is this thread's alone
   } else {
     const uint32_t i = atomicAdd(&T.nstash, 1u);
     if (i < (uint32_t)kStash) T.stash[i] = k; else T.ovf = 1u;
