@@ -416,6 +416,7 @@ __device__ __forceinline__ JoinHash join_hash(unsigned long long k) {
   h.b2 = (uint32_t)(m >> 40) & (kJBuckets - 1);
   if (h.b2 == h.b1) h.b2 ^= 1u;
   h.fp = (uint32_t)(m >> 24) & 0xFFFFu;
+  if (h.fp == 0) h.fp = 1;  // 0 marks an empty slot: a probe needs no slot counts
   return h;
 }
 
@@ -443,24 +444,22 @@ __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
 }
 
 // Multiplicity of k in the table; *first = slot id of its first copy (bucket-major, then stash).
+// Fast path: two fingerprint words, one zero-lane test each (no slot counts, no loop).
 __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long long k, uint32_t nstash,
                                                uint32_t &first) {
+  constexpr unsigned long long kL = 0x0001000100010001ull, kH = 0x8000800080008000ull;
   const JoinHash h = join_hash(k);
-  const uint32_t n1 = min(T.cnt[h.b1], 4u), n2 = min(T.cnt[h.b2], 4u);
-  uint32_t m1 = fp_match(T.fp[h.b1], h.fp, n1), m2 = fp_match(T.fp[h.b2], h.fp, n2);
+  const unsigned long long w1 = T.fp[h.b1], w2 = T.fp[h.b2], pat = h.fp * kL;
+  const unsigned long long x1 = w1 ^ pat, x2 = w2 ^ pat;
   uint32_t c = 0;
   first = 0xFFFFFFFFu;
-  if (m1 | m2) {  // rare: fingerprint hit, compare full keys
-    while (m1) {
-      const uint32_t s = __ffs(m1) - 1;
-      m1 &= m1 - 1;
-      if (T.key[h.b1][s] == k) { if (!c) first = h.b1 * 4 + s; ++c; }
-    }
-    while (m2) {
-      const uint32_t s = __ffs(m2) - 1;
-      m2 &= m2 - 1;
-      if (T.key[h.b2][s] == k) { if (!c) first = h.b2 * 4 + s; ++c; }
-    }
+  if ((((x1 - kL) & ~x1) | ((x2 - kL) & ~x2)) & kH) {  // some lane may hold fp: compare full keys
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      if (((w1 >> (16 * s)) & 0xFFFFu) == h.fp && T.key[h.b1][s] == k) { if (!c) first = h.b1 * 4 + s; ++c; }
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      if (((w2 >> (16 * s)) & 0xFFFFu) == h.fp && T.key[h.b2][s] == k) { if (!c) first = h.b2 * 4 + s; ++c; }
   }
   for (uint32_t i = 0; i < nstash; ++i)
     if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
