@@ -305,7 +305,7 @@ def main() -> int:
         "traffic": None,
     }
     try:  # DRAM bytes per wave from the committed ncu --set full capture (profiles/README.md)
-        with open(os.path.join(HERE, "profiles", "r1_kernels.json")) as fh:
+        with open(os.path.join(HERE, "profiles", "r1b_kernels.json")) as fh:
             tr = json.load(fh)["traffic"]
         roofline["traffic"] = {"dram_bytes_per_wave": tr["wave_dram_bytes"],
                                "algorithmic_bytes_per_wave": tr["algorithmic_bytes_per_wave"],

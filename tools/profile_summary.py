@@ -52,8 +52,10 @@ def full(rep, kernels=()):
                   if "smsp__pcsamp_warps_issue_stalled" in h and not h.endswith("not_issued") and _num(v) is not None]
         tot = sum(v for v, _ in stalls) or 1.0
         top = ", ".join(f"{n} {100 * v / tot:.0f}%" for v, n in sorted(stalls, reverse=True)[:5])
-        dram = (_num(d.get("dram__bytes_read.sum", 0)) or 0) + (_num(d.get("dram__bytes_write.sum", 0)) or 0)
-        dram_unit = units.get("dram__bytes_read.sum", "")
+        scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+        dram = sum((_num(d.get(k, 0)) or 0) * scale.get(units.get(k, "Mbyte"), 1.0)
+                   for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        dram_unit = "Mbyte"
         rows.append({
             "kernel": name.split("(")[0],
             "duration_us": _num(d.get("gpu__time_duration.sum")),
