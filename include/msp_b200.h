@@ -66,6 +66,9 @@ typedef struct {
   int32_t brute_force_max_n; /* < 0 -> 12 (solver.py:48) */
   uint64_t wave_keys;        /* 0 -> default join wave budget (keys per wave) */
   void *stream;              /* cudaStream_t to run on, NULL -> library stream */
+  const volatile int32_t *cancel; /* optional cross-rank early exit (first mode): when *cancel != 0
+                                     at a wave checkpoint, the solve stops and returns what it has
+                                     confirmed so far with stats.cancelled = 1 */
 } msp_options;
 
 typedef struct {
@@ -84,6 +87,8 @@ typedef struct {
   int64_t hot_launches;    /* launches of the dominant kernel */
   int64_t hot_pairs;       /* candidate pairs the dominant kernel processed */
   int64_t hot_bytes;       /* algorithmic HBM/L2 bytes of those launches */
+  int32_t cancelled;       /* 1: stopped early by msp_options.cancel (counters are partial) */
+  int32_t reserved;
 } msp_stats;
 
 typedef struct {

@@ -84,6 +84,7 @@ class Options(C.Structure):
         ("brute_force_max_n", C.c_int32),
         ("wave_keys", C.c_uint64),
         ("stream", C.c_void_p),
+        ("cancel", C.c_void_p),
     ]
 
 
@@ -99,6 +100,7 @@ class Stats(C.Structure):
         ("dev_ms_total", C.c_double), ("dev_ms_tables", C.c_double), ("dev_ms_join", C.c_double),
         ("dev_ms_hot", C.c_double), ("hot_launches", C.c_int64), ("hot_pairs", C.c_int64),
         ("hot_bytes", C.c_int64),
+        ("cancelled", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
@@ -163,10 +165,11 @@ class _ProblemArrays:
 
 def make_options(mode: str = "all", device: int = 0, time_limit: float | None = None,
                  alpha_lo: int = 0, alpha_hi: int = 0, flags: int = 0, brute_force_max_n: int = -1,
-                 wave_keys: int = 0, stream: int | None = None) -> Options:
+                 wave_keys: int = 0, stream: int | None = None, cancel: int | None = None) -> Options:
+    """``cancel``: address of a shared int32 (CancelFlag.address) polled at wave checkpoints."""
     return Options(MSP_MODE_ALL if mode == "all" else MSP_MODE_FIRST, device,
                    float(time_limit) if time_limit else 0.0, alpha_lo, alpha_hi, flags,
-                   brute_force_max_n, wave_keys, stream or None)
+                   brute_force_max_n, wave_keys, stream or None, cancel or None)
 
 
 def solve_raw(a, d, opts: Options, alpha: int | None = None):

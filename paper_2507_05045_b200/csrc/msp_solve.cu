@@ -573,6 +573,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   S.row1_pairs_lo = (uint64_t)row1;
   S.row1_pairs_hi = (uint64_t)(row1 >> 64);
   if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
+  if (opt->cancel && *opt->cancel) {
+    S.cancelled = 1;
+    return emit();
+  }
 
   // ---- per-batch counters, hit list
   const size_t G1 = std::max<size_t>(1, P.G);
@@ -732,6 +736,11 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(cudaGetLastError());
     if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
     if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
+    if (opt->cancel && *opt->cancel) {  // another rank confirmed a solution (first mode)
+      S.cancelled = 1;
+      stop_now = true;
+      return MSP_OK;
+    }
     if (opt->mode == MSP_MODE_FIRST && nh > hits_done) {
       std::vector<HitRec> hv;
       int r2 = fetch_hits(hits_done, nh, hv);
@@ -743,7 +752,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
     return MSP_OK;
   };
-  const bool periodic = deadline || opt->mode == MSP_MODE_FIRST;
+  const bool periodic = deadline || opt->mode == MSP_MODE_FIRST || opt->cancel;
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
   std::vector<uint32_t> part_b, huge_b, global_b;

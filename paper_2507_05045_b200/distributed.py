@@ -11,6 +11,7 @@ pipeline_run's result merge (solver.py:284-289,415-418).
 
 from __future__ import annotations
 
+import os
 import time
 from typing import Callable, Sequence
 
@@ -20,7 +21,8 @@ from .instances import MspInstance, solution_encoding, verify_solution
 from .solver import SolveResult, SolverConfig, SolveStats, native_solve, stats_from_native
 
 COUNTERS = ("batches", "candidates_left", "candidates_right", "filtered_residuals", "hash_hits",
-            "exact_hits", "peak_table_entries", "peak_heap1", "peak_heap2", "kernel_launches", "waves")
+            "exact_hits", "peak_table_entries", "peak_heap1", "peak_heap2", "kernel_launches", "waves",
+            "cancelled")
 
 
 def alpha_bands(plan: Sequence[tuple[int, int, int, int]], world: int) -> list[tuple[int, int]]:
@@ -96,14 +98,71 @@ def _gather_counters(st: dict, dist, device) -> list[dict]:
 BandSolver = Callable[[MspInstance, str, tuple[int, int]], tuple[list[tuple[int, ...]], dict]]
 
 
+class CancelFlag:
+    """One int32 shared by the rank processes of a node (a /dev/shm mapping).
+
+    First mode's cross-GPU early exit (the reference stops its one
+    process at the first verified solution, solver.py:278-279,391-392): the rank that confirms a
+    solution sets the word; every rank's ``msp_solve`` polls it at its wave checkpoints through
+    ``msp_options.cancel`` and stops.  The word is host memory: a checkpoint already synchronises
+    the host with the device, so polling costs nothing on the device.
+    """
+
+    def __init__(self, name: str, create: bool):
+        import ctypes
+        import mmap
+        import tempfile
+
+        base = "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir()
+        self.path = os.path.join(base, name)
+        if create:
+            with open(self.path, "wb") as fh:
+                fh.write(b"\0" * 8)
+        self._fh = open(self.path, "r+b")
+        self._mm = mmap.mmap(self._fh.fileno(), 8)
+        self._word = ctypes.c_int32.from_buffer(self._mm)
+        self.address = ctypes.addressof(self._word)
+
+    def set(self) -> None:
+        self._word.value = 1
+
+    def is_set(self) -> bool:
+        return self._word.value != 0
+
+    def close(self, unlink: bool = False) -> None:
+        del self._word
+        self._mm.close()
+        self._fh.close()
+        if unlink:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+
+
+def shared_cancel_flag(dist) -> CancelFlag:
+    """Rank 0 creates the word, every rank maps it (collective over ``dist``)."""
+    import uuid
+
+    name = [f"msp_cancel_{uuid.uuid4().hex}" if dist.get_rank() == 0 else None]
+    if dist.get_rank() == 0:
+        flag = CancelFlag(name[0], create=True)
+    dist.broadcast_object_list(name, src=0)
+    if dist.get_rank() != 0:
+        flag = CancelFlag(name[0], create=False)
+    dist.barrier()
+    return flag
+
+
 def cuda_band_solver(device: int, time_limit: float | None = None, wave_keys: int = 0,
-                     stream: int | None = None) -> BandSolver:
+                     stream: int | None = None, cancel: CancelFlag | None = None) -> BandSolver:
     def run(work: MspInstance, mode: str, band: tuple[int, int]):
         lo, hi = band
         if hi != 0 and lo >= hi:  # empty band: nothing to enumerate on this rank
             return [], {}
         return native_solve(work, mode, time_limit, device=device, alpha_lo=lo, alpha_hi=hi,
-                            wave_keys=wave_keys, stream=stream)
+                            wave_keys=wave_keys, stream=stream,
+                            cancel=cancel.address if cancel is not None else None)
     return run
 
 
@@ -126,9 +185,15 @@ def solve_sharded(inst: MspInstance, cfg: SolverConfig | None = None, dist=None,
     if plan is None:
         plan = _native.alpha_plan(inst.a, inst.d, device=cfg.device)
     bands = alpha_bands(plan, world)
+    cancel = shared_cancel_flag(dist) if cfg.mode == "first" else None
     if band_solver is None:
-        band_solver = cuda_band_solver(cfg.device, wave_keys=cfg.wave_keys)
-    sols, st = band_solver(inst, cfg.mode, bands[rank])
+        band_solver = cuda_band_solver(cfg.device, wave_keys=cfg.wave_keys, cancel=cancel)
+    if cancel is not None and cancel.is_set():
+        sols, st = [], {}
+    else:
+        sols, st = band_solver(inst, cfg.mode, bands[rank])
+    if cancel is not None and sols:
+        cancel.set()  # the other ranks stop at their next wave checkpoint
     if device is None:
         import torch
         device = torch.device("cuda", cfg.device) if dist.get_backend() == "nccl" else torch.device("cpu")
@@ -146,6 +211,10 @@ def solve_sharded(inst: MspInstance, cfg: SolverConfig | None = None, dist=None,
     all_sols.sort(key=solution_encoding)
     if len(set(all_sols)) != len(all_sols):
         raise RuntimeError("internal error: duplicate solutions emitted")
+    if cancel is not None:
+        dist.barrier()
+        stats.cancelled_ranks = int(sum(r.get("cancelled", 0) for r in per_rank))
+        cancel.close(unlink=rank == 0)
     if cfg.mode == "first":
         all_sols = all_sols[:1]
     stats.t_total = time.perf_counter() - t0

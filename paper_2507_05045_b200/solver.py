@@ -107,6 +107,7 @@ class SolveStats:
     row1_candidate_pairs: int = 0
     waves: int = 0
     kernel_launches: int = 0
+    cancelled_ranks: int = 0  # sharded first mode: ranks stopped early by another rank's solution
     dev_ms_total: float = 0.0
 
     def as_dict(self) -> dict:
@@ -165,11 +166,15 @@ def _check_verified(original: MspInstance, sols) -> None:  # solver.py:248-253
 
 def native_solve(work: MspInstance, mode: str, time_limit: float | None, device: int = 0,
                  alpha_lo: int = 0, alpha_hi: int = 0, flags: int = 0, wave_keys: int = 0,
-                 brute_force_max_n: int = BRUTE_FORCE_MAX_N, stream: int | None = None):
-    """One msp_solve call; returns (solution tuples, raw stats dict)."""
+                 brute_force_max_n: int = BRUTE_FORCE_MAX_N, stream: int | None = None,
+                 cancel: int | None = None):
+    """One msp_solve call; returns (solution tuples, raw stats dict).
+
+    ``cancel``: address of a shared int32 polled at wave checkpoints (cross-rank early exit).
+    """
     opts = _native.make_options(mode=mode, device=device, time_limit=time_limit, alpha_lo=alpha_lo,
                                 alpha_hi=alpha_hi, flags=flags, brute_force_max_n=brute_force_max_n,
-                                wave_keys=wave_keys, stream=stream)
+                                wave_keys=wave_keys, stream=stream, cancel=cancel)
     rc, xb, st = _native.solve_raw(work.a, work.d, opts)
     raise_for_status(rc, time_limit)
     sols = [tuple(int(v) for v in row) for row in xb]

@@ -102,3 +102,53 @@ def test_two_rank_gloo_solve_equals_single_rank(m, seed):
         assert sols == ref_sols, rank
         for k in STATS:
             assert st[k] == ref.stats[k], (rank, k)
+
+
+def _first_worker(rank, world, port, m, seed, q):
+    import torch.distributed as dist
+
+    from paper_2507_05045_b200.distributed import shared_cancel_flag
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # the shared cancel word: set by rank 1, observed by rank 0 through its own mapping
+        flag = shared_cancel_flag(dist)
+        seen_before = flag.is_set()
+        dist.barrier()
+        if rank == 1:
+            flag.set()
+        dist.barrier()
+        seen_after = flag.is_set()
+        flag.close(unlink=rank == 0)
+        inst = msb.generate_instance(m, 100, seed)
+        res = solve_sharded(inst, msb.SolverConfig(mode="first"), dist=dist, plan=_plan(inst),
+                            band_solver=oracle_band_solver)
+        q.put((rank, seen_before, seen_after, [msb.solution_to_string(x) for x in res.solutions],
+               res.verdict))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_first_mode_shares_the_cancel_word():
+    """First mode over 2 ranks (gloo): the cancel word is one shared int32; one verified solution."""
+    import torch.multiprocessing as tmp
+
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    m, seed = 6, 4  # feasible (SURVEY.md §8(c) frozen seeds)
+    procs = [ctx.Process(target=_first_worker, args=(r, 2, port, m, seed, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    inst = msb.generate_instance(m, 100, seed)
+    sols = [s for _, _, _, s, _ in outs]
+    assert sols[0] == sols[1] and len(sols[0]) == 1
+    x = tuple(int(c) for c in sols[0][0])
+    assert msb.verify_solution(inst, x)
+    for rank, before, after, _, verdict in outs:
+        assert not before and after and verdict == "feasible", rank

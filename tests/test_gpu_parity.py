@@ -190,3 +190,40 @@ def test_m7_s1_full_against_reference():
         assert getattr(res.stats, k) == rec["stats"][k], k
     ref_rows = rec["batches"]
     assert res.stats.row1_candidate_pairs == sum(b[1] * b[2] for b in ref_rows)
+
+
+def test_cancel_word_stops_the_solve(tmp_path):
+    """msp_options.cancel: a set word stops the solve (stats.cancelled, no solutions); unset is inert."""
+    from paper_2507_05045_b200.distributed import CancelFlag
+    from paper_2507_05045_b200.solver import native_solve
+
+    inst = msb.generate_instance(6, 100, 4)
+    flag = CancelFlag(f"msp_cancel_test_{tmp_path.name}", create=True)
+    try:
+        sols, st = native_solve(inst, "first", None, cancel=flag.address)
+        assert len(sols) == 1 and st["cancelled"] == 0
+        assert msb.verify_solution(inst, sols[0])
+        flag.set()
+        sols, st = native_solve(inst, "first", None, cancel=flag.address)
+        assert sols == [] and st["cancelled"] == 1
+    finally:
+        flag.close(unlink=True)
+
+
+def test_gpu_brute_force_agrees_with_table_path():
+    """the GPU brute force (k_brute, n <= 28) as an independent conformance
+    check of the table path on many small instances (and both against the oracle on a few)."""
+    from paper_2507_05045_b200.solver import native_solve
+
+    for seed in range(24):
+        m, n = 2 + seed % 3, 12 + seed % 13
+        inst = seeded_instance(7000 + seed, m=m, n=n, k=5 + seed % 30, d_mode="half" if seed % 2 else "random")
+        brute, bst = native_solve(inst, "all", None, brute_force_max_n=28)
+        table, tst = native_solve(inst, "all", None, brute_force_max_n=0,
+                                  flags=_native.MSP_FLAG_FORCE_TABLE_PATH)
+        assert bst["fallback"] == 1 and tst["fallback"] == 0
+        key = msb.solution_encoding
+        assert sorted(brute, key=key) == sorted(table, key=key), seed
+        if seed < 6:
+            ref = O.solve(inst.a, inst.d, mode="all")
+            assert sorted(table, key=key) == ref.solutions, seed
