@@ -81,7 +81,8 @@ void launch_brute(const BruteArgs &a, cudaStream_t st);
 
 // Partitioned join (msp_part.cu).  Buckets of one wave, per role (0 = build, 1 = probe).
 constexpr int kMaxWaveBuckets = 1024;  // buckets per role per wave
-constexpr int kScatterWarpsHost = 16;  // warps per k_scatter CTA (must match msp_part.cu)
+constexpr int kScatterStageKeys = 10240;   // stage slots of a scatter CTA (all entries)
+constexpr int kScatterCtasHost = 2;        // resident k_scatter CTAs per SM (grid = SMs x this)
 constexpr int kJoinSlotsLog2 = 14;     // shared-memory join table: 16K (key, count) slots
 constexpr uint32_t kBucketTarget = 1u << (kJoinSlotsLog2 - 1);  // mean build keys per bucket
 struct PartArgs {
@@ -91,17 +92,21 @@ struct PartArgs {
   uint32_t *fill[2];          // keys written (reset by k_join)
   const uint32_t *gid;        // batch of each bucket
   uint32_t nb;                // buckets per role
+  uint32_t roles;             // roles present in the launch's entries (0 means 2)
+  unsigned long long *zero_keys;  // per (batch, side): real keys equal to 0 (never staged: 0 pads runs)
+  unsigned long long *dbg;    // diagnostics (MSP_DEBUG_STATS): rounds, staged, overflow, pads
+  uint32_t ovf_trigger;       // overflow keys that end a scatter round (0: default)
   unsigned int *batch_ovf;    // per batch: a bucket overflowed -> re-join with the global table
   HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;
   unsigned long long *batch_hits;
-  uint32_t sink;              // scratch index of kSinkSlots slots nobody reads: dropped runs land there
 };
-constexpr uint32_t kSinkSlots = 8192;  // >= keys of one scatter round
+constexpr uint32_t kSinkSlots = 64;    // scratch slack past the last region
 // One (batch, side) unit of a scatter launch, kept in shared memory by k_scatter.
 constexpr int kMaxUnits = 128;         // units per scatter launch (64 batches per wave)
 struct UnitInfo {
   uint32_t h0lo, h0hi;                 // FNV state after coordinate 0 (alpha)
-  uint32_t ent;                        // first (role, bucket) entry | bucket bits << 12 | side << 16
+  uint32_t ent;                        // first (role, bucket) entry | buckets NB << 12 | side << 23
+                                       // (bucket of a key = floor(hi32 * NB / 2^32))
   uint32_t gid;                        // batch index within the solve
 };
 // One warp tile: up to 32 lane entries x up to 32 loop entries of one rectangle (16 B, one load).
@@ -121,7 +126,11 @@ void launch_tiles(const TileGenArgs &a, cudaStream_t st);
 struct ScatterArgs {
   const uint32_t *comp[4];             // companion tables A, B, C, D
   uint32_t dpack[8];                   // d rows 1..m-1 packed, +0x8000 guard per half
-  const TileDesc *tiles; uint32_t ntiles;
+  const TileDesc *tiles;
+  const unsigned long long *chunks;    // work chunks: first tile | tile count << 32 | unit << 48
+  uint32_t nchunks;
+  unsigned int *chunk_ctr;             // next chunk (zeroed before the launch)
+  const uint32_t *cta_first;           // static mode: CTA b runs chunks [cta_first[b], cta_first[b+1])
   const UnitInfo *units; uint32_t nunits;
   unsigned long long *batch_filtered;  // per batch (gid)
   uint32_t diag;                       // MSP_FLAG_DIAG_HASH_ONLY: hash without staging
@@ -132,11 +141,16 @@ struct RescatterSrc {
   const unsigned long long *keys;  // coarse bucket region
   const uint32_t *fill;            // keys written into it (device counter)
   uint32_t cap, role;              // region capacity; 0 build, 1 probe
-  uint32_t fine_base, fbits;       // first fine bucket (per role) and fine bits of this source
-  uint32_t coarse_bits, pad;       // key bits already consumed by the coarse level
+  uint32_t fine_base, nf;          // first fine bucket (per role) and fine buckets of this source
+  uint32_t nc, pad;                // coarse buckets of the level-1 partition
   uint64_t in_base;                // first input slot of this source
 };
-struct RescatterArgs { const RescatterSrc *src; uint32_t nsrc; uint64_t total; };
+struct RescatterArgs {
+  const RescatterSrc *src;
+  const unsigned long long *chunks;  // first slot | 32-slot groups << 32 | source << 48
+  uint32_t nchunks;
+  unsigned int *chunk_ctr;           // next chunk (zeroed before the launch)
+};
 cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st);
 cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 

@@ -22,13 +22,21 @@
 #include "msp_kernels.h"
 #include "msp_tile.cuh"
 
+#define MSP_SCATTER_CTAS 2
+
 namespace msp {
 
-constexpr int kScatterWarps = 16;
-constexpr int kWarpStage = 448;                         // keys a warp stages per round
-constexpr int kStage = kScatterWarps * kWarpStage;      // keys staged per CTA round
-constexpr int kHistEntries = 2 * kMaxWaveBuckets;       // (role, bucket)
-constexpr int kPer = kHistEntries / (kScatterWarps * 32);
+// Scatter CTA shape: kScatterCtas resident CTAs per SM, so one CTA's flush (reservation atomics +
+// write-out) overlaps the other's enumeration.
+constexpr int kScatterCtas = MSP_SCATTER_CTAS;
+static_assert(kScatterCtas == kScatterCtasHost, "scatter CTAs per SM: msp_kernels.h and msp_part.cu disagree");
+constexpr int kScatterWarps = 8;
+constexpr int kScatterThreads = kScatterWarps * 32;
+constexpr int kStageKeys = kScatterStageKeys;                   // stage slots of a CTA
+constexpr int kOvf = 1024;                                      // keys ranked past their entry's C slots
+constexpr int kOvfTrigger = 384;                                // a round ends at this many (default)
+constexpr int kMaxNB = kMaxWaveBuckets;                         // entries of one unit
+constexpr uint32_t kDrop = 0xFFFFFFFFu;
 
 // Reservation of n slots at *p, result left in flight in r (predicated: no-op when n == 0, so no
 // select has to wait for the atomic's return value).
@@ -39,112 +47,167 @@ __device__ __forceinline__ void reserve_async(uint32_t &r, uint32_t *p, uint32_t
                : "memory");
 }
 
-// Shared memory of a scatter CTA (k_scatter / k_rescatter); the producers' loop-vector buffers
-// follow it (k_scatter only).
+// Shared memory of a scatter CTA (k_scatter / k_rescatter).  A CTA works on one CHUNK at a time:
+// consecutive tiles of ONE unit (one batch side), whose keys spread uniformly over the unit's NB
+// bucket entries.  The round's keys are bucketed in place: entry j owns slots [j*C, j*C + C),
+// C = kStageKeys / NB, and a key's slot is its rank within the entry (one shared atomic), so the
+// round needs no sort.  Keys ranked past C go to the overflow list with their (entry, rank); the
+// round ends when that list passes kOvfTrigger, or at the end of the chunk.  The producers'
+// loop-vector buffers follow the struct (k_scatter only).
 struct __align__(16) Stage {
-  unsigned long long skey[kStage];   // staged keys (warp-private slot ranges)
-  unsigned long long sorted[kStage]; // the round's keys sorted by (role, bucket)
-  uint16_t sbkt[kStage], rank[kStage], sortb[kStage];
-  uint32_t hist[kHistEntries];       // keys per entry in the round being filled
-  uint32_t off[kHistEntries];        // sorted position of each entry's run
-  uint32_t abase[kHistEntries];      // scratch index of sorted position 0 of the run, or kDrop
-  uint32_t est[kHistEntries];        // scratch start of each entry's bucket region
-  uint32_t ecap[kHistEntries];       // its capacity
+  unsigned long long key[kStageKeys];
+  unsigned long long ovk[kOvf];
+  uint32_t ove[kOvf];                // entry | rank << 11
+  uint32_t cnt[kMaxNB];              // keys ranked into each entry this round
+  uint2 run[kMaxNB];                 // flush: (scratch index of rank 0, staged keys to write)
   UnitInfo units[kMaxUnits];
-  uint32_t warp_tot[kScatterWarps];
-  uint32_t round_end;                // set by the first warp whose stage is full
+  uint32_t ufilt[kMaxUnits];         // filtered right pairs per unit (k_scatter)
+  uint32_t novf, round_end, chunk, ove_spill;  // ove_spill: some rank past C has no key this round
 };
 
 size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kU) * sw * 4; }
 
-__device__ __forceinline__ void stage_init(Stage &g, const PartArgs &S, const UnitInfo *units, uint32_t nunits) {
-  const uint32_t nbw = S.nb;
-  for (uint32_t i = threadIdx.x; i < kHistEntries; i += blockDim.x) g.hist[i] = 0;
-  for (uint32_t j = threadIdx.x; j < 2 * nbw; j += blockDim.x) {
-    const uint32_t role = j >= nbw, b = j - role * nbw;
-    g.est[j] = __ldg((role ? S.start[1] : S.start[0]) + b);
-    g.ecap[j] = __ldg((role ? S.cap[1] : S.cap[0]) + b);
-  }
-  for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) g.units[u] = units[u];
-  if (threadIdx.x == 0) g.round_end = 0;
+__device__ __forceinline__ void stage_init(Stage &g, const UnitInfo *units, uint32_t nunits) {
+  for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
+  for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) { g.units[u] = units[u]; g.ufilt[u] = 0; }
+  if (threadIdx.x == 0) { g.novf = 0; g.round_end = 0; g.ove_spill = 0; }
 }
 
-// Append one warp-step of keys densely to the warp's stage (ballot + popc) and rank each key
-// within its (role, bucket) entry with one shared-memory atomic.
-__device__ __forceinline__ void stage_key(Stage &g, uint32_t warp, uint32_t lane_lt, uint32_t &cnt,
-                                          uint64_t key, uint32_t e, bool ok) {
-  const uint32_t m = __ballot_sync(0xffffffffu, ok);
-  if (ok) {
-    const uint32_t pos = warp * kWarpStage + cnt + __popc(m & lane_lt);
-    g.skey[pos] = key;
-    g.sbkt[pos] = (uint16_t)e;
-    g.rank[pos] = (uint16_t)atomicAdd(g.hist + e, 1u);
-  }
-  cnt += __popc(m);
+// The CTA's next work chunk (dynamic: one global atomic per chunk), broadcast through shared memory.
+__device__ __forceinline__ uint32_t next_chunk(Stage &g, unsigned int *ctr) {
+  if (threadIdx.x == 0) g.chunk = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const uint32_t c = g.chunk;
+  __syncthreads();
+  return c;
 }
 
-// After a __syncthreads: scan the round's entry counts and reserve one scratch range per nonempty
-// entry (global atomics, left in flight), sort each warp's staged keys into bucket-contiguous runs
-// (hiding the atomics' latency), then turn the reservations into run bases and write the runs out
-// coalesced.  The histogram is zeroed for the next fill.
-__device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_t cnt) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nbw = S.nb, nent = 2 * nbw;
-  const uint32_t j0 = tid * kPer;
-  uint32_t hv[kPer], gres[kPer], local = 0;
+// Spill of an overflow key that found the overflow list full: straight to its bucket region (one
+// global atomic + store); its rank slot of the round stays empty (the flush pads it).
+__device__ __noinline__ void stage_spill(Stage &g, const PartArgs &S, uint32_t e, unsigned long long key) {
+  const uint32_t role = e >= S.nb, b = e - role * S.nb;
+  const uint32_t pos = atomicAdd(S.fill[role] + b, 1u);
+  if (pos < __ldg(S.cap[role] + b)) __stcg(S.scratch + __ldg(S.start[role] + b) + pos, key);
+  else atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+  g.ove_spill = 1u;
+}
+
+// Stage N keys per lane into their entries j (local to the chunk's unit): rank (shared atomics,
+// all issued before any dependent store), store into the entry's slots.  Keys ranked past C go to
+// the overflow list with (entry, rank): one warp-aggregated reservation per warp step; the round
+// ends once the list passes `trig`.
+template <int N>
+__device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t lane, uint32_t C,
+                                           uint32_t trig,
+                                           const unsigned long long (&key)[N], const uint32_t (&j)[N],
+                                           const bool (&ok)[N]) {
+  uint32_t r[N];
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    hv[k] = j0 + k < nent ? g.hist[j0 + k] : 0u;
-    g.hist[j0 + k] = 0u;  // ready for the next fill
-    local += hv[k];
+  for (int u = 0; u < N; ++u) r[u] = ok[u] ? atomicAdd(&g.cnt[j[u]], 1u) : 0u;
+  uint32_t nov = 0;
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    if (ok[u] && r[u] < C) g.key[j[u] * C + r[u]] = key[u];
+    nov += (ok[u] && r[u] >= C) ? 1u : 0u;
   }
+  if (__any_sync(0xffffffffu, nov != 0u)) {
+    uint32_t inc = nov;  // warp inclusive scan of the lanes' overflow counts
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const uint32_t j = j0 + k, role = j >= nbw;
-    gres[k] = 0u;
-    reserve_async(gres[k], (role ? S.fill[1] : S.fill[0]) + (j - role * nbw), hv[k]);
-  }
-  uint32_t incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= (uint32_t)o) inc += y;
+    }
+    uint32_t ob = 0;
+    if (lane == 31) ob = atomicAdd(&g.novf, inc);
+    ob = __shfl_sync(0xffffffffu, ob, 31);
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    uint32_t o = ob + inc - nov;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= (uint32_t)o) incl += y;
-  }
-  if (lane == 31) g.warp_tot[warp] = incl;
-  __syncthreads();
-  uint32_t run = incl - local, total = 0;
-#pragma unroll
-  for (int w = 0; w < kScatterWarps; ++w) {
-    const uint32_t t = g.warp_tot[w];
-    if ((uint32_t)w < warp) run += t;
-    total += t;
-  }
-  uint32_t offs[kPer];
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) { offs[k] = run; g.off[j0 + k] = run; run += hv[k]; }
-  __syncthreads();
-  for (uint32_t j = lane; j < cnt; j += 32) {  // each warp sorts its own staged keys
-    const uint32_t i = warp * kWarpStage + j;
-    const uint16_t b = g.sbkt[i];
-    const uint32_t pos = g.off[b] + g.rank[i];
-    g.sorted[pos] = g.skey[i];
-    g.sortb[pos] = b;
-  }
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const uint32_t j = j0 + k;
-    if (hv[k]) {
-      if (gres[k] + hv[k] > g.ecap[j]) {  // overflow: the run goes to the sink, the batch is re-joined
-        g.abase[j] = S.sink - offs[k];
-        const uint32_t role = j >= nbw;
-        atomicOr(S.batch_ovf + __ldg(S.gid + (j - role * nbw)), 1u);
+    for (int u = 0; u < N; ++u) {
+      if (!(ok[u] && r[u] >= C)) continue;
+      if (o < (uint32_t)kOvf) {
+        g.ovk[o] = key[u];
+        g.ove[o] = j[u] | (r[u] << 11);
       } else {
-        g.abase[j] = g.est[j] + gres[k] - offs[k];
+        stage_spill(g, S, ebase + j[u], key[u]);
       }
+      ++o;
+    }
+    if (lane == 31 && ob + tot >= trig) *(volatile uint32_t *)&g.round_end = 1u;
+  }
+}
+
+// After a barrier: reserve one scratch range per nonempty entry of the chunk's unit (entries
+// ebase .. ebase + NB - 1 of the launch; global atomics, one thread per entry), write the round's
+// runs out (slot-major, so consecutive threads store consecutive keys of a run) and the overflow
+// keys, reset the round.  Ends with a barrier.
+__device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t NB, uint32_t C,
+                                            uint32_t cmagic) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nb = S.nb;
+  constexpr int kPerT = (kMaxNB + kScatterThreads - 1) / kScatterThreads;
+  uint32_t res[kPerT], cn[kPerT];
+#pragma unroll
+  for (int k = 0; k < kPerT; ++k) {
+    const uint32_t j = tid + k * kScatterThreads;
+    cn[k] = j < NB ? g.cnt[j] : 0u;
+    res[k] = 0u;
+    if (j < NB) {
+      const uint32_t e = ebase + j, role = e >= nb;
+      reserve_async(res[k], S.fill[role] + (e - role * nb), cn[k]);
     }
   }
+  unsigned long long nstaged = 0;
+#pragma unroll
+  for (int k = 0; k < kPerT; ++k) {
+    const uint32_t j = tid + k * kScatterThreads;
+    if (j >= NB) continue;
+    if (!cn[k]) { g.run[j] = make_uint2(kDrop, 0u); continue; }
+    nstaged += cn[k];
+    const uint32_t e = ebase + j, role = e >= nb, b = e - role * nb;
+    uint2 run = make_uint2(kDrop, 0u);
+    if (res[k] + cn[k] <= __ldg(S.cap[role] + b)) run = make_uint2(__ldg(S.start[role] + b) + res[k], min(cn[k], C));
+    else atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+    g.run[j] = run;
+  }
+  if (S.dbg) {  // diagnostics: rounds, staged keys, overflow keys
+    nstaged = warp_sum(nstaged);
+    if ((tid & 31) == 0 && nstaged) atomicAdd(S.dbg + 1, nstaged);
+    if (tid == 0) { atomicAdd(S.dbg + 0, 1ull); atomicAdd(S.dbg + 2, (unsigned long long)g.novf); }
+  }
   __syncthreads();
-  for (uint32_t pos = tid; pos < total; pos += blockDim.x) S.scratch[g.abase[g.sortb[pos]] + pos] = g.sorted[pos];
+  const uint32_t tot = NB * C;  // (NB * C <= kStageKeys; a dropped entry has run.y == 0)
+  for (uint32_t s = tid; s < tot; s += kScatterThreads) {
+    const uint32_t j = __umulhi(s, cmagic), i = s - j * C;
+    const uint2 run = g.run[j];
+    if (i < run.y) __stcg(S.scratch + run.x + i, g.key[s]);
+  }
+  if (g.ove_spill) {  // ranks past C whose keys were spilled stay empty: pad every rank past C
+    __syncthreads();   // with key 0 (readers skip it), then write the listed overflow keys
+    for (uint32_t j = warp; j < NB; j += kScatterWarps) {
+      const uint32_t n = g.cnt[j], b = g.run[j].x;
+      if (b == kDrop) continue;
+      for (uint32_t i = C + lane; i < n; i += 32) __stcg(S.scratch + b + i, 0ull);
+    }
+    __syncthreads();
+  }
+  const uint32_t no = min(g.novf, (uint32_t)kOvf);
+  for (uint32_t o = tid; o < no; o += kScatterThreads) {
+    const uint32_t w = g.ove[o], j = w & 0x7FFu;
+    const uint32_t b = g.run[j].x;
+    if (b != kDrop) __stcg(S.scratch + b + (w >> 11), g.ovk[o]);
+  }
+  __syncthreads();
+  for (uint32_t j = tid; j < NB; j += kScatterThreads) g.cnt[j] = 0u;
+  if (tid == 0) { g.novf = 0u; g.round_end = 0u; g.ove_spill = 0u; }
+  __syncthreads();
+}
+
+// Per-chunk stage geometry: C slots per entry and ceil(2^32 / C) (s / C == umulhi(s, cmagic) for
+// every slot index s < kStageKeys).
+__device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_t &cmagic) {
+  C = kStageKeys / NB;
+  cmagic = (uint32_t)((0xFFFFFFFFull + C) / C);
 }
 
 // ---------------------------------------------------------------- tile descriptors
@@ -197,7 +260,7 @@ template <int SW>
 __device__ __forceinline__ void tile_vecs(const ScatterArgs &A, const Stage &g, const uint4 d, uint32_t lane,
                                           uint32_t (&lv)[SW], uint32_t (&yv)[SW]) {
   const uint32_t meta = d.z;
-  const uint32_t side = (g.units[meta & 0xFFu].ent >> 16) & 1u;
+  const uint32_t side = (g.units[meta & 0xFFu].ent >> 23) & 1u;
   const bool lx = (meta >> 18) & 1u;
   const uint32_t ln = ((meta >> 8) & 31u) + 1u, qn = ((meta >> 13) & 31u) + 1u;
   const uint32_t *lt = side ? (lx ? A.comp[2] : A.comp[3]) : (lx ? A.comp[0] : A.comp[1]);
@@ -208,15 +271,15 @@ __device__ __forceinline__ void tile_vecs(const ScatterArgs &A, const Stage &g, 
 
 // kU keys of the current tile (loop entries q .. q+kU-1) into the stage.
 template <int MC, bool RIGHT>
-__device__ __forceinline__ void hash_step(Stage &g, const uint32_t *ybuf, const uint32_t (&lv)[stride_for(MC)],
+__device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uint32_t *ybuf,
+                                          const uint32_t (&lv)[stride_for(MC)],
                                           const uint32_t (&dg)[words_for(MC) > 0 ? words_for(MC) : 1],
-                                          uint32_t warp, uint32_t lane_lt, uint32_t &cnt, uint32_t q, uint32_t qn,
-                                          bool lok, const UnitInfo &ui, uint32_t diag,
+                                          uint32_t lane, uint32_t C, uint32_t q, uint32_t qn, bool lok,
+                                          const UnitInfo &ui, uint32_t nbk, uint32_t diag,
                                           unsigned long long &filt, unsigned long long &dacc) {
   constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
-  const uint32_t ebase = ui.ent & 0xFFFu, bits = (ui.ent >> 12) & 0xFu;
-  uint64_t key[kU];
-  uint32_t e[kU];
+  unsigned long long key[kU];
+  uint32_t j[kU];
   bool ok[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
@@ -240,147 +303,155 @@ __device__ __forceinline__ void hash_step(Stage &g, const uint32_t *ybuf, const 
       const uint32_t w = sv[c >> 1];
       fold(lo, hi, (c & 1) ? (w >> 16) & (RIGHT ? 0x7FFFu : 0xFFFFu) : w & (RIGHT ? 0x7FFFu : 0xFFFFu));
     }
-    key[u] = ((uint64_t)hi << 32) | lo;
+    key[u] = ((unsigned long long)hi << 32) | lo;
+    if (in && (hi | lo) == 0u) {  // a real key 0: counted per (batch, side), never staged
+      atomicAdd(S.zero_keys + 2 * ui.gid + (RIGHT ? 1u : 0u), 1ull);
+      in = false;
+    }
     ok[u] = in;
-    e[u] = ebase + (uint32_t)(((uint64_t)hi << bits) >> 32);  // top `bits` bits of the key
+    j[u] = __umulhi(hi, nbk);  // bucket within the unit = floor(hi * NB / 2^32)
   }
   if (diag) {
 #pragma unroll
     for (int u = 0; u < kU; ++u) dacc ^= ok[u] ? key[u] : 0ull;
   } else {
-#pragma unroll
-    for (int u = 0; u < kU; ++u) stage_key(g, warp, lane_lt, cnt, key[u], e[u], ok[u]);
+    stage_keys<kU>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, key, j, ok);
   }
 }
 
-// Enumerate + hash + partition the launch's tiles.  Each warp walks tiles warp, warp + W, ... with
-// the descriptor two tiles ahead and the companion vectors one tile ahead in flight, so a tile
-// change never waits on a load.  A full warp stage suspends the tile mid-way for a CTA round.
+// Enumerate + hash + partition.  CTAs take work chunks (consecutive tiles of one unit) from a
+// global counter; the chunk's warps walk tiles warp, warp + W, ... with the descriptor two tiles
+// ahead and the companion vectors one tile ahead in flight.  A round ends for every warp of the
+// CTA as soon as the overflow list passes its trigger (the CTA flushes, then resumes mid-tile) and
+// at the end of the chunk.
 template <int MC>
-__global__ void __launch_bounds__(kScatterWarps * 32, 1) k_scatter(const ScatterArgs A, const PartArgs S) {
+__global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const ScatterArgs A, const PartArgs S) {
   constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage &g = *reinterpret_cast<Stage *>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lane_lt = (1u << lane) - 1u;
   uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kU) * SW;
-  stage_init(g, S, A.units, A.nunits);
+  stage_init(g, A.units, A.nunits);
   for (uint32_t i = lane; i < (uint32_t)((kTQ + kU) * SW); i += 32) ybuf[i] = 0;
   uint32_t dg[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
-  __syncthreads();
-
-  const uint32_t nw = gridDim.x * kScatterWarps, n = A.ntiles;
-  uint32_t t = blockIdx.x * kScatterWarps + warp;
-  uint4 dcur = ld_tile(A.tiles, t, n), dnxt = ld_tile(A.tiles, t + nw, n), dnn = ld_tile(A.tiles, t + 2 * nw, n);
-  uint32_t lvc[SW], yvc[SW], lvn[SW], yvn[SW];
-  if (t < n) tile_vecs<SW>(A, g, dcur, lane, lvc, yvc);
-  if (t + nw < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
-  bool have = t < n;
-  uint32_t q = 0, qn = 0, fgid = 0xFFFFFFFFu;
-  bool lok = false, right = false;
-  UnitInfo ui{};
   unsigned long long filt = 0, dacc = 0;
-  auto begin_tile = [&]() {
-    const uint32_t meta = dcur.z;
-    ui = g.units[meta & 0xFFu];
-    right = (ui.ent >> 16) & 1u;
-    qn = ((meta >> 13) & 31u) + 1u;
-    lok = lane <= ((meta >> 8) & 31u);
-    q = 0;
-    __syncwarp();
-    if (lane < qn) {
-#pragma unroll
-      for (int k = 0; k < SW; ++k) ybuf[lane * SW + k] = yvc[k];
-    }
-    __syncwarp();
-    if (ui.gid != fgid) {
-      if (fgid != 0xFFFFFFFFu) {
-        const unsigned long long f = warp_sum(filt);
-        if (lane == 0 && f) atomicAdd(A.batch_filtered + fgid, f);
-      }
-      filt = 0;
-      fgid = ui.gid;
-    }
-  };
-  if (have) begin_tile();
-  uint32_t cnt = 0;
   volatile uint32_t *round_end = &g.round_end;
-  while (true) {
-    // a round ends as soon as one warp's stage is full: the others stop within one step, so no
-    // warp idles at the barrier while a slow one fills up
-    while (have && !*round_end) {
-      if (cnt + 32 * kU > (uint32_t)kWarpStage) { *round_end = 1u; break; }
-      if (right)
-        hash_step<MC, true>(g, ybuf, lvc, dg, warp, lane_lt, cnt, q, qn, lok, ui, A.diag, filt, dacc);
-      else
-        hash_step<MC, false>(g, ybuf, lvc, dg, warp, lane_lt, cnt, q, qn, lok, ui, A.diag, filt, dacc);
-      q += kU;
-      if (q >= qn) {  // next tile: everything it needs was loaded one (vectors) or two tiles ago
-        t += nw;
-        have = t < n;
-        if (have) {
-          dcur = dnxt;
+  __syncthreads();  // units and counters of stage_init
+
+  // static mode (cta_first): CTA b owns chunks [cta_first[b], cta_first[b+1]); else dynamic
+  const bool stat = A.cta_first != nullptr;
+  const uint32_t cend = stat ? __ldg(A.cta_first + blockIdx.x + 1) : A.nchunks;
+  for (uint32_t c = stat ? __ldg(A.cta_first + blockIdx.x) : next_chunk(g, A.chunk_ctr); c < cend;
+       c = stat ? c + 1 : next_chunk(g, A.chunk_ctr)) {
+    const unsigned long long cw = __ldg(A.chunks + c);
+    const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
+    const UnitInfo ui = g.units[unit];
+    const uint32_t ebase = ui.ent & 0xFFFu, nbk = (ui.ent >> 12) & 0x7FFu;
+    const bool right = (ui.ent >> 23) & 1u;
+    uint32_t C, cmagic;
+    stage_geometry(nbk, C, cmagic);
+
+    uint32_t t = t0 + warp;
+    uint4 dcur = ld_tile(A.tiles, t, n), dnxt = ld_tile(A.tiles, t + kScatterWarps, n),
+          dnn = ld_tile(A.tiles, t + 2 * kScatterWarps, n);
+    uint32_t lvc[SW], yvc[SW], lvn[SW], yvn[SW];
+    if (t < n) tile_vecs<SW>(A, g, dcur, lane, lvc, yvc);
+    if (t + kScatterWarps < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
+    bool have = t < n;
+    uint32_t q = 0, qn = 0;
+    bool lok = false;
+    auto begin_tile = [&]() {
+      const uint32_t meta = dcur.z;
+      qn = ((meta >> 13) & 31u) + 1u;
+      lok = lane <= ((meta >> 8) & 31u);
+      q = 0;
+      __syncwarp();
+      if (lane < qn) {
 #pragma unroll
-          for (int k = 0; k < SW; ++k) { lvc[k] = lvn[k]; yvc[k] = yvn[k]; }
-          dnxt = dnn;
-          if (t + nw < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
-          dnn = ld_tile(A.tiles, t + 2 * nw, n);
-          begin_tile();
+        for (int k = 0; k < SW; ++k) ybuf[lane * SW + k] = yvc[k];
+      }
+      __syncwarp();
+    };
+    if (have) begin_tile();
+    while (true) {
+      while (have && !*round_end) {
+        if (right)
+          hash_step<MC, true>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
+        else
+          hash_step<MC, false>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
+        q += kU;
+        if (q >= qn) {  // next tile: everything it needs was loaded one (vectors) or two tiles ago
+          t += kScatterWarps;
+          have = t < n;
+          if (have) {
+            dcur = dnxt;
+#pragma unroll
+            for (int k = 0; k < SW; ++k) { lvc[k] = lvn[k]; yvc[k] = yvn[k]; }
+            dnxt = dnn;
+            if (t + kScatterWarps < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
+            dnn = ld_tile(A.tiles, t + 2 * kScatterWarps, n);
+            begin_tile();
+          }
         }
       }
+      const bool more = __syncthreads_or(have);
+      flush_round(g, S, ebase, nbk, C, cmagic);
+      if (!more) break;
     }
-    if (!__syncthreads_or(cnt > 0 || have)) break;
-    if (tid == 0) *round_end = 0u;  // ordered before the next fill by the flush's barriers
-    flush_round(g, S, cnt);
-    cnt = 0;
+    if (right) {  // filtered right pairs of the chunk into the unit's shared counter
+      const unsigned long long f = warp_sum(filt);
+      if (lane == 0 && f) atomicAdd(&g.ufilt[unit], (uint32_t)f);
+      filt = 0;
+    }
   }
-  if (fgid != 0xFFFFFFFFu) {
-    const unsigned long long f = warp_sum(filt);
-    if (lane == 0 && f) atomicAdd(A.batch_filtered + fgid, f);
-  }
+  __syncthreads();
+  for (uint32_t u = tid; u < A.nunits; u += blockDim.x)
+    if (g.ufilt[u]) atomicAdd(A.batch_filtered + g.units[u].gid, (unsigned long long)g.ufilt[u]);
   if (dacc == 0x123456789ull) A.batch_filtered[0] = dacc;  // keep the diagnostic keys live
 }
 
 // Level 2 of the huge-batch path: stream already-hashed keys back from coarse bucket regions
-// (HBM) and re-partition them into fine buckets (L2 scratch) for k_join.  Each CTA round takes
-// kStage consecutive input slots; slots past a region's fill are empty.
-__global__ void __launch_bounds__(kScatterWarps * 32) k_rescatter(const RescatterArgs R, const PartArgs S) {
+// (HBM) and re-partition them into fine buckets (L2 scratch) for k_join.  Work chunks are slot
+// ranges of ONE source (a coarse region of one role, whose keys spread uniformly over its NF fine
+// buckets); slots past the region's fill are empty.  Fine bucket = floor(frac * NF / 2^32), frac
+// = the key's position inside its coarse bucket (the low word of hi * NC).
+__global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_rescatter(const RescatterArgs R, const PartArgs S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage &g = *reinterpret_cast<Stage *>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  const uint32_t nbw = S.nb;
-  stage_init(g, S, nullptr, 0);
-  __syncthreads();
-  for (uint64_t chunk = blockIdx.x; chunk * kStage < R.total; chunk += gridDim.x) {
-    const uint64_t base = chunk * kStage + (uint64_t)warp * kWarpStage;
-    uint32_t s = 0;
-    {
-      uint32_t lo = 0, hi = R.nsrc;  // last source with in_base <= base
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (R.src[mid].in_base <= base) lo = mid; else hi = mid;
+  stage_init(g, nullptr, 0);
+  volatile uint32_t *round_end = &g.round_end;
+  constexpr int N = 2;
+  for (uint32_t c = next_chunk(g, R.chunk_ctr); c < R.nchunks; c = next_chunk(g, R.chunk_ctr)) {
+    const unsigned long long cw = __ldg(R.chunks + c);
+    const RescatterSrc &src = R.src[(uint32_t)(cw >> 48)];
+    const uint32_t s0 = (uint32_t)cw, s1 = min(s0 + (uint32_t)((cw >> 32) & 0xFFFFu) * 32u, min(*src.fill, src.cap));
+    const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
+    uint32_t C, cmagic;
+    stage_geometry(NB, C, cmagic);
+    uint32_t idx = s0 + warp * 32 + lane;
+    const uint32_t stride = kScatterThreads;
+    while (true) {
+      while (idx - lane < s1 && !*round_end) {
+        unsigned long long key[N];
+        uint32_t j[N];
+        bool ok[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+          const uint32_t x = idx + u * stride;
+          ok[u] = x < s1;
+          key[u] = ok[u] ? __ldcs(src.keys + x) : 0ull;
+          j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
+        }
+        stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, key, j, ok);
+        idx += N * stride;
       }
-      s = lo;
+      const bool more = __syncthreads_or(idx - lane < s1);
+      flush_round(g, S, ebase, NB, C, cmagic);
+      if (!more) break;
     }
-    uint32_t cnt = 0;
-#pragma unroll 2
-    for (int k = 0; k < kWarpStage / 32; ++k) {
-      const uint64_t idx = base + (uint64_t)k * 32 + lane;
-      uint32_t sl = s;
-      while (sl + 1 < R.nsrc && idx >= R.src[sl + 1].in_base) ++sl;
-      const RescatterSrc &src = R.src[sl];
-      const uint64_t local = idx - src.in_base;
-      const bool ok = idx < R.total && local < min(*src.fill, src.cap);
-      const uint64_t key = ok ? __ldcs(src.keys + local) : 0ull;
-      const uint32_t fb = src.fbits ? (uint32_t)((key << src.coarse_bits) >> (64 - src.fbits)) : 0u;
-      stage_key(g, warp, lt_mask, cnt, key, src.role * nbw + src.fine_base + fb, ok);
-    }
-    __syncthreads();
-    flush_round(g, S, cnt);
-    __syncthreads();
   }
 }
 
@@ -403,7 +474,7 @@ struct JoinSmem {
   unsigned long long stash[kStash];
   uint32_t hitbits[kHitWords];
   unsigned long long bhits[kJoinThreads / 32];
-  uint32_t nstash, zb, zhit, ovf;
+  uint32_t nstash, ovf;
 };
 
 size_t join_smem_bytes() { return sizeof(JoinSmem); }
@@ -475,7 +546,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
   for (uint32_t b = blockIdx.x; b < S.nb; b += gridDim.x) {
     for (uint32_t i = tid; i < (uint32_t)kJBuckets; i += kJoinThreads) { T.cnt[i] = 0u; T.fp[i] = 0ull; }
     for (uint32_t i = tid; i < (uint32_t)kHitWords; i += kJoinThreads) T.hitbits[i] = 0u;
-    if (tid == 0) { T.nstash = 0; T.zb = 0; T.zhit = 0; T.ovf = 0; }
+    if (tid == 0) { T.nstash = 0; T.ovf = 0; }
     const uint32_t gid = __ldg(S.gid + b);
     const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
     const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
@@ -492,7 +563,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (base + u * kJoinThreads + tid >= nbuild) continue;
-        if (kv[u] == 0) { atomicAdd(&T.zb, 1u); continue; }
+        if (kv[u] == 0) continue;  // run pad (real zero keys are counted by the scatter)
         join_insert(T, kv[u]);
       }
       const uint32_t nb2 = base + kJoinThreads * U;
@@ -509,7 +580,6 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
     }
     __syncthreads();
     const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
-    const uint32_t zb = T.zb;
     if (T.ovf && tid == 0) atomicOr(S.batch_ovf + gid, 1u);
     unsigned long long hits = 0;
     for (uint32_t base = 0; base < nprobe; base += kJoinThreads * U) {
@@ -517,16 +587,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
       for (int u = 0; u < U; ++u) {
         const unsigned long long k = kv[u];
         if (base + u * kJoinThreads + tid >= nprobe) continue;
-        if (k == 0) {
-          if (zb) {
-            hits += zb;
-            if (atomicExch(&T.zhit, 1u) == 0u) {
-              const unsigned long long h = atomicAdd(S.nhits, 1ull);
-              if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, 0ull};
-            }
-          }
-          continue;
-        }
+        if (k == 0) continue;  // run pad
         uint32_t first;
         const uint32_t c = join_count(T, k, nstash, first);
         if (c) {
@@ -567,14 +628,14 @@ static cudaError_t launch_scatter_mc(const ScatterArgs &a, const PartArgs &p, in
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_scatter<MC><<<grid, kScatterWarps * 32, sm, st>>>(a, p);
+  k_scatter<MC><<<grid, kScatterThreads, sm, st>>>(a, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, int num_sms, cudaStream_t st) {
-  if (args.ntiles == 0) return cudaSuccess;
-  const uint32_t blocks = (args.ntiles + kScatterWarps - 1) / kScatterWarps;
-  const int grid = (int)(blocks < (uint32_t)num_sms ? blocks : (uint32_t)num_sms);
+  if (args.nchunks == 0) return cudaSuccess;
+  const uint32_t slots = (uint32_t)num_sms * kScatterCtas;
+  const int grid = args.cta_first ? (int)slots : (int)(args.nchunks < slots ? args.nchunks : slots);
   switch (mc) {
 #define MSP_CASE(N) case N: return launch_scatter_mc<N>(args, p, grid, st);
     MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
@@ -593,10 +654,10 @@ cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const uint64_t chunks = (r.total + kStage - 1) / kStage;
-  if (!chunks) return cudaSuccess;
-  const int grid = (int)(chunks < (uint64_t)num_sms ? chunks : (uint64_t)num_sms);
-  k_rescatter<<<grid, kScatterWarps * 32, sm, st>>>(r, p);
+  if (!r.nchunks) return cudaSuccess;
+  const uint32_t slots = (uint32_t)num_sms * kScatterCtas;
+  const int grid = (int)(r.nchunks < slots ? r.nchunks : slots);
+  k_rescatter<<<grid, kScatterThreads, sm, st>>>(r, p);
   return cudaGetLastError();
 }
 

@@ -80,21 +80,23 @@ struct Device {
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
   DBuf rkeys, runits, rfilt, rhits;
-  DBuf bfilt, bhits, bovf, scratch, bk, fill;
+  DBuf bfilt, bhits, bovf, scratch, bk, fill, zkeys, dbg;
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
   DBuf scratch2, fill2;
-  DBuf tdesc, gstb, gsu, uinfo;
+  DBuf tdesc, gstb, gsu, uinfo, chunks, cchunks, l2chunks, cctr, cfirst, ccfirst;
+  uint32_t cctr_next = 0;  // next unused chunk counter in cctr (zeroed per solve)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
     DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err, &nitem, &ibase, &items, &ictr,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
-                   &bfilt, &bhits, &bovf, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
-                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &tdesc, &gstb, &gsu, &uinfo};
+                   &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
+                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &tdesc, &gstb, &gsu, &uinfo,
+                   &chunks, &cchunks, &l2chunks, &cctr, &cfirst, &ccfirst};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
                                   comp[i].release(); rs[i].release(); re[i].release(); }
@@ -378,13 +380,15 @@ UnitDesc make_unit(const Plan &P, uint32_t g, int side, uint64_t tile_base) {
   return u;
 }
 
-// The shared-memory unit record of k_scatter for a unit of a wave with `nb` buckets per role.
+// The shared-memory unit record of k_scatter for a unit of a wave with `nb` buckets per role; the
+// unit's batch owns buckets [region_base, region_base + region_log2) of its role (for partitioned
+// units region_log2 holds the bucket COUNT NB, not a log).
 UnitInfo make_info(const UnitDesc &u, uint32_t nb) {
   UnitInfo i;
   i.h0lo = (uint32_t)u.h0;
   i.h0hi = (uint32_t)(u.h0 >> 32);
   const uint32_t ebase = ((u.flags >> 1) & 1u) * nb + u.region_base;
-  i.ent = ebase | (u.region_log2 << 12) | (u.side << 16);
+  i.ent = ebase | (u.region_log2 << 12) | (u.side << 23);
   i.gid = u.gid;
   return i;
 }
@@ -511,6 +515,30 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+uint32_t even_up(double x) { const uint32_t v = (uint32_t)x; return v + (v & 1u); }
+
+constexpr uint32_t kChunkCounters = 1u << 16;
+
+// Static split of a launch's tiles (units given as consecutive tile ranges [ub[i], ub[i+1])) over
+// `nct` CTAs: CTA b gets tiles [b*T/nct, (b+1)*T/nct), cut at unit boundaries into chunks.
+void static_chunks(const std::vector<uint64_t> &ub, uint32_t nct, std::vector<unsigned long long> &chunks,
+                   std::vector<uint32_t> &first) {
+  const uint64_t T = ub.back();
+  size_t u = 0;
+  for (uint32_t b = 0; b < nct; ++b) {
+    first.push_back((uint32_t)chunks.size());
+    uint64_t t = T * b / nct;
+    const uint64_t te = T * (b + 1) / nct;
+    while (t < te) {
+      while (ub[u + 1] <= t) ++u;
+      const uint64_t e = std::min<uint64_t>({te, ub[u + 1], t + 65535});
+      chunks.push_back(t | ((e - t) << 32) | ((unsigned long long)u << 48));
+      t = e;
+    }
+  }
+  first.push_back((uint32_t)chunks.size());
+}
+
 int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   const double t0 = now_s();
   memset(res, 0, sizeof(*res));
@@ -586,6 +614,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   CK(cudaMemsetAsync(D.bfilt.p, 0, 8 * G1, st));
   CK(cudaMemsetAsync(D.bhits.p, 0, 8 * G1, st));
   CK(cudaMemsetAsync(D.bovf.p, 0, 4 * G1, st));
+  CK(D.zkeys.ensure(16 * G1));
+  CK(cudaMemsetAsync(D.zkeys.p, 0, 16 * G1, st));
   const uint64_t hit_cap = 1 << 20;
   CK(D.hits.ensure(sizeof(HitRec) * hit_cap));
   CK(D.nhits.ensure(8));
@@ -753,15 +783,39 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     return MSP_OK;
   };
   const bool periodic = deadline || opt->mode == MSP_MODE_FIRST || opt->cancel;
+  // buckets per role of one partitioned wave (scatter entries = 2x): fewer entries give longer
+  // runs per round; MSP_WAVE_BUCKETS overrides for tuning
+  uint32_t wave_buckets = kMaxWaveBuckets;
+  uint32_t ovf_trigger = 0;
+  if (const char *ev = getenv("MSP_OVF_TRIGGER")) ovf_trigger = (uint32_t)std::max(1, std::min(1024, atoi(ev)));
+  unsigned long long *dbg_stats = nullptr;
+  CK(D.cctr.ensure(4 * kChunkCounters));
+  CK(cudaMemsetAsync(D.cctr.p, 0, 4 * kChunkCounters, st));
+  D.cctr_next = 0;
+  // a zeroed chunk counter for the next scatter launch (stream-ordered reuse after a wrap)
+  auto take_counter = [&](unsigned int **out) -> int {
+    if (D.cctr_next == kChunkCounters) {
+      CK(cudaMemsetAsync(D.cctr.p, 0, 4 * kChunkCounters, st));
+      D.cctr_next = 0;
+    }
+    *out = D.cctr.as<unsigned int>() + D.cctr_next++;
+    return MSP_OK;
+  };
+  if (getenv("MSP_DEBUG_STATS")) {
+    CK(D.dbg.ensure(64));
+    CK(cudaMemsetAsync(D.dbg.p, 0, 64, st));
+    dbg_stats = D.dbg.as<unsigned long long>();
+  }
+  if (const char *ev = getenv("MSP_WAVE_BUCKETS")) wave_buckets = (uint32_t)std::max(1, std::min(kMaxWaveBuckets, atoi(ev)));
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
   std::vector<uint32_t> part_b, huge_b, global_b;
   for (uint32_t g = 0; g < P.G; ++g) {
     const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
-    const uint64_t nbk = 1ull << pow2ceil((nb + kBucketTarget - 1) / kBucketTarget);
+    const uint64_t nbk = std::max<uint64_t>(1, (nb + kBucketTarget - 1) / kBucketTarget);
     if (opt->flags & MSP_FLAG_JOIN_GLOBAL)
       global_b.push_back(g);
-    else if (nbk > (uint64_t)kMaxWaveBuckets || nb + np > key_budget)
+    else if (nbk > (uint64_t)wave_buckets || nb + np > key_budget)
       huge_b.push_back(g);
     else
       part_b.push_back(g);
@@ -789,16 +843,16 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     for (uint32_t g : part_b) {
       const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
       const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
-      const uint32_t bits = pow2ceil((nb + kBucketTarget - 1) / kBucketTarget);
-      const uint32_t NB = 1u << bits;
-      if (cur.nb + NB > (uint32_t)kMaxWaveBuckets || cur_keys + nb + np > key_budget ||
+      const uint32_t NB = (uint32_t)std::max<uint64_t>(1, (nb + kBucketTarget - 1) / kBucketTarget);
+      if (cur.nb + NB > wave_buckets || cur_keys + nb + np > key_budget ||
           (cur.nb && g != cur.g1) ||  // waves hold consecutive batches (contiguous tile ranges)
           units.size() - cur.u0 + 2 > (size_t)kMaxUnits) {
         flush();
       }
       if (cur.nb == 0) { cur.g0 = g; cur.t0 = all_tiles; }
       const double mb = (double)nb / NB, mp = (double)np / NB;
-      const uint32_t cb = (uint32_t)(mb + 7.0 * std::sqrt(mb) + 16), cp = (uint32_t)(mp + 7.0 * std::sqrt(mp) + 16);
+      // capacities even: bucket regions start 16-byte aligned for the scatter's bulk copies
+      const uint32_t cb = even_up(mb + 7.0 * std::sqrt(mb) + 16), cp = even_up(mp + 7.0 * std::sqrt(mp) + 16);
       for (uint32_t k = 0; k < NB; ++k) {
         bstart[0].push_back((uint32_t)cur.scratch); bcap[0].push_back(cb); cur.scratch += cb;
         bstart[1].push_back((uint32_t)cur.scratch); bcap[1].push_back(cp); cur.scratch += cp;
@@ -807,7 +861,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       for (int side = 0; side < 2; ++side) {
         UnitDesc u = make_unit(P, g, side, 0);
         u.region_base = cur.nb;
-        u.region_log2 = bits;
+        u.region_log2 = NB;
         u.flags = (side == bside ? 0u : 1u) << 1;  // role: 0 build, 1 probe
         const size_t gs = 2 * (size_t)g + side;
         gs_unit[gs] = (uint32_t)(units.size() - cur.u0);
@@ -839,6 +893,28 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       bkimg.reserve(5 * nbt);
       for (auto *v : {&bstart[0], &bstart[1], &bcap[0], &bcap[1], &bgid}) bkimg.insert(bkimg.end(), v->begin(), v->end());
       CK(cudaMemcpyAsync(D.bk.p, bkimg.data(), 4 * bkimg.size(), cudaMemcpyHostToDevice, st));
+      // per wave: each CTA's equal share of the wave's tiles, cut at unit boundaries
+      const uint32_t nct = (uint32_t)D.num_sms * kScatterCtasHost;
+      std::vector<unsigned long long> chimg;
+      std::vector<uint32_t> cfirst;
+      std::vector<size_t> choff, cfoff;
+      for (const PWave &w : pw) {
+        choff.push_back(chimg.size());
+        cfoff.push_back(cfirst.size());
+        std::vector<uint64_t> ub{0};
+        for (size_t i = w.u0; i < w.u1; ++i) {
+          const UnitDesc &u = units[i];
+          ub.push_back(ub.back() + P.tiles[2 * (size_t)u.gid + u.side]);
+        }
+        std::vector<uint32_t> f;
+        static_chunks(ub, nct, chimg, f);
+        for (uint32_t &x : f) x -= (uint32_t)choff.back();
+        cfirst.insert(cfirst.end(), f.begin(), f.end());
+      }
+      CK(D.chunks.ensure(8 * std::max<size_t>(1, chimg.size())));
+      CK(cudaMemcpyAsync(D.chunks.p, chimg.data(), 8 * chimg.size(), cudaMemcpyHostToDevice, st));
+      CK(D.cfirst.ensure(4 * std::max<size_t>(1, cfirst.size())));
+      CK(cudaMemcpyAsync(D.cfirst.p, cfirst.data(), 4 * cfirst.size(), cudaMemcpyHostToDevice, st));
       // K3b: every partitioned batch side's warp tiles, one launch
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(all_tiles, 1)));
       CK(D.gstb.ensure(8 * gs_tb.size()));
@@ -860,11 +936,13 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.fill[0] = D.fill.as<uint32_t>();
       pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
       pa.batch_ovf = D.bovf.as<unsigned int>();
+      pa.zero_keys = D.zkeys.as<unsigned long long>();
+      pa.dbg = dbg_stats;
+      pa.ovf_trigger = ovf_trigger;
       pa.hits = D.hits.as<HitRec>();
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
-      pa.sink = (uint32_t)max_scratch;
       ScatterArgs sa = scatter_base(P, A);
       for (size_t wi = 0; wi < pw.size(); ++wi) {
         const PWave &w = pw[wi];
@@ -875,7 +953,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         pa.gid = bkd + 4 * nbt + w.b0;
         pa.nb = (uint32_t)w.nb;
         sa.tiles = D.tdesc.as<TileDesc>() + w.t0;
-        sa.ntiles = (uint32_t)w.ntiles;
+        sa.chunks = D.chunks.as<unsigned long long>() + choff[wi];
+        sa.cta_first = D.cfirst.as<uint32_t>() + cfoff[wi];
+        sa.nchunks = 1;  // (static mode: the launch runs a full grid)
         sa.units = D.uinfo.as<UnitInfo>() + w.u0;
         sa.nunits = (uint32_t)(w.u1 - w.u0);
         if (profile) CK(cudaEventRecord(D.pev[0], st));
@@ -919,7 +999,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, 10));
       const uint32_t NC = 1u << cbits;
       const double mb = (double)nb / NC, mp = (double)np / NC;
-      const uint64_t cb = (uint64_t)(mb + 7.0 * std::sqrt(mb) + 16), cp = (uint64_t)(mp + 7.0 * std::sqrt(mp) + 16);
+      const uint64_t cb = even_up(mb + 7.0 * std::sqrt(mb) + 16), cp = even_up(mp + 7.0 * std::sqrt(mp) + 16);
       if (cb * NC > 0xFFFFFFF0ull || cp * NC > 0xFFFFFFF0ull) {
         set_err("batch side too large for 32-bit coarse regions");
         return MSP_UNSUPPORTED;
@@ -944,8 +1024,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         const uint32_t role = side == bside ? 0u : 1u;
         lu[role] = make_unit(P, g, side, 0);
         lu[role].region_base = 0;
-        lu[role].region_log2 = cbits;
-        lu[role].flags = role << 1;
+        lu[role].region_log2 = NC;
+        lu[role].flags = 0;  // each side is scattered by its own launch as role 0 (roles = 1)
         lu[role].count_filter = side == 1;
         ltiles[role] = P.tiles[2 * g + side];
       }
@@ -954,13 +1034,28 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(cudaMemcpyAsync(D.hunits.p, li, sizeof(UnitInfo) * 2, cudaMemcpyHostToDevice, st));
       const uint32_t *cbkd = D.cbk.as<uint32_t>();
       PartArgs c1{};
-      c1.start[0] = cbkd; c1.start[1] = cbkd + NC;
-      c1.cap[0] = cbkd + 2 * NC; c1.cap[1] = cbkd + 3 * NC;
       c1.gid = cbkd + 4 * NC;
-      c1.fill[0] = D.cfill.as<uint32_t>();
-      c1.fill[1] = D.cfill.as<uint32_t>() + kMaxWaveBuckets;
       c1.nb = NC;
+      c1.roles = 1;
+      std::vector<unsigned long long> cch;  // level-1 chunks (static split): role 0's, then role 1's
+      std::vector<uint32_t> ccf;
+      const uint32_t nct = (uint32_t)D.num_sms * kScatterCtasHost;
+      static_chunks({0, ltiles[0]}, nct, cch, ccf);
+      const size_t cch1 = cch.size(), ccf1 = ccf.size();
+      {
+        std::vector<uint32_t> f;
+        static_chunks({0, ltiles[1]}, nct, cch, f);
+        for (uint32_t &x : f) x -= (uint32_t)cch1;
+        ccf.insert(ccf.end(), f.begin(), f.end());
+      }
+      CK(D.cchunks.ensure(8 * std::max<size_t>(1, cch.size())));
+      CK(cudaMemcpyAsync(D.cchunks.p, cch.data(), 8 * cch.size(), cudaMemcpyHostToDevice, st));
+      CK(D.ccfirst.ensure(4 * ccf.size()));
+      CK(cudaMemcpyAsync(D.ccfirst.p, ccf.data(), 4 * ccf.size(), cudaMemcpyHostToDevice, st));
       c1.batch_ovf = D.bovf.as<unsigned int>();
+      c1.dbg = dbg_stats;
+      c1.ovf_trigger = ovf_trigger;
+      c1.zero_keys = D.zkeys.as<unsigned long long>();
       if (profile) CK(cudaEventRecord(D.pev[0], st));
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, std::max(ltiles[0], ltiles[1]))));
       for (int role = 0; role < 2; ++role) {
@@ -973,20 +1068,24 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         tg.out = D.tdesc.as<TileDesc>();
         launch_tiles(tg, st);
         c1.scratch = D.cscratch[role].as<unsigned long long>();
-        c1.sink = (uint32_t)((role ? cp : cb) * NC);
+        c1.start[0] = cbkd + role * NC;
+        c1.cap[0] = cbkd + (2 + role) * NC;
+        c1.fill[0] = D.cfill.as<uint32_t>() + role * kMaxWaveBuckets;
         ScatterArgs sa = scatter_base(P, A);
         sa.tiles = D.tdesc.as<TileDesc>();
-        sa.ntiles = (uint32_t)ltiles[role];
+        sa.chunks = D.cchunks.as<unsigned long long>() + (role ? cch1 : 0);
+        sa.cta_first = D.ccfirst.as<uint32_t>() + (role ? ccf1 : 0);
+        sa.nchunks = 1;
         sa.units = D.hunits.as<UnitInfo>() + role;
         sa.nunits = 1;
         CK(launch_scatter(P.mc, sa, c1, D.num_sms, st));
         S.kernel_launches += 2;
       }
       // level 2 waves over the coarse buckets
-      const uint32_t fbits = pow2ceil((uint64_t)std::ceil(mb / kBucketTarget));
-      const uint32_t NF = 1u << fbits;
+      const uint32_t NF = (uint32_t)std::max<uint64_t>(1, (uint64_t)std::ceil(mb / kBucketTarget));
+      if (NF > (uint32_t)kMaxWaveBuckets) { set_err("coarse bucket too large for one level-2 wave"); return MSP_UNSUPPORTED; }
       const double fmb = mb / NF, fmp = mp / NF;
-      const uint32_t fcb = (uint32_t)(fmb + 7.0 * std::sqrt(fmb) + 16), fcp = (uint32_t)(fmp + 7.0 * std::sqrt(fmp) + 16);
+      const uint32_t fcb = even_up(fmb + 7.0 * std::sqrt(fmb) + 16), fcp = even_up(fmp + 7.0 * std::sqrt(fmp) + 16);
       struct L2Wave { size_t s0, ns, b0, nb; uint64_t total, scratch; };
       std::vector<L2Wave> lw;
       std::vector<RescatterSrc> srcs;
@@ -1004,8 +1103,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
           r.cap = (uint32_t)(role ? cp : cb);
           r.role = role;
           r.fine_base = (uint32_t)cw.nb;
-          r.fbits = fbits;
-          r.coarse_bits = cbits;
+          r.nf = NF;
+          r.nc = NC;
           r.in_base = cw.total;
           cw.total += r.cap;
           srcs.push_back(r);
@@ -1037,20 +1136,42 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.fill[0] = D.fill.as<uint32_t>();
       pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
       pa.batch_ovf = D.bovf.as<unsigned int>();
+      pa.zero_keys = D.zkeys.as<unsigned long long>();
+      pa.dbg = dbg_stats;
+      pa.ovf_trigger = ovf_trigger;
       pa.hits = D.hits.as<HitRec>();
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
-      pa.sink = (uint32_t)max_scr;
+      std::vector<unsigned long long> l2ch;  // per wave: 16K-slot chunks of each source region
+      std::vector<size_t> l2off;
+      for (const L2Wave &w : lw) {
+        l2off.push_back(l2ch.size());
+        for (size_t si = 0; si < w.ns; ++si) {
+          const uint64_t cap = srcs[w.s0 + si].cap;
+          for (uint64_t o = 0; o < cap; o += 16384) {
+            const uint64_t grp = std::min<uint64_t>(512, (cap - o + 31) / 32);
+            l2ch.push_back(o | (grp << 32) | ((unsigned long long)si << 48));
+          }
+        }
+      }
+      l2off.push_back(l2ch.size());
+      CK(D.l2chunks.ensure(8 * std::max<size_t>(1, l2ch.size())));
+      CK(cudaMemcpyAsync(D.l2chunks.p, l2ch.data(), 8 * l2ch.size(), cudaMemcpyHostToDevice, st));
       for (size_t wi = 0; wi < lw.size(); ++wi) {
         const L2Wave &w = lw[wi];
+
         pa.start[0] = fb + w.b0;
         pa.start[1] = fb + nft + w.b0;
         pa.cap[0] = fb + 2 * nft + w.b0;
         pa.cap[1] = fb + 3 * nft + w.b0;
         pa.gid = fb + 4 * nft + w.b0;
         pa.nb = (uint32_t)w.nb;
-        RescatterArgs ra{D.l2src.as<RescatterSrc>() + w.s0, (uint32_t)w.ns, w.total};
+        RescatterArgs ra{};
+        ra.src = D.l2src.as<RescatterSrc>() + w.s0;
+        ra.chunks = D.l2chunks.as<unsigned long long>() + l2off[wi];
+        ra.nchunks = (uint32_t)(l2off[wi + 1] - l2off[wi]);
+        if (int r0 = take_counter(&ra.chunk_ctr)) return r0;
         rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_rescatter(ra, p2, D.num_sms, s2); }, pa);
         if (rc) return rc;
         S.kernel_launches += 2;
@@ -1210,12 +1331,13 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
 
   // ---- totals
   CK(cudaEventRecord(D.ev[2], st));
-  std::vector<unsigned long long> bf(P.G), bh(P.G);
+  std::vector<unsigned long long> bf(P.G), bh(P.G), zk(2 * (size_t)P.G);
   unsigned long long nh = 0;
   int err = 0;
   if (P.G) {
     CK(cudaMemcpyAsync(bf.data(), D.bfilt.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(bh.data(), D.bhits.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(zk.data(), D.zkeys.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
@@ -1225,6 +1347,14 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   S.dev_ms_join = elapsed_ms(D.ev[1], D.ev[2]);
   S.dev_ms_hot = hot_ms;
   if (err) { set_err("join table region overflow (err=%d)", err); return MSP_INTERNAL; }
+  // real zero keys never reach the partitioned join (0 pads the scatter's runs): their hash hits
+  // are the per-batch product, and key 0 joins the recovery set (global-table batches count their
+  // own zeros and never touch zkeys)
+  std::vector<HitRec> zero_hits;
+  for (uint32_t g = 0; g < P.G; ++g) {
+    const unsigned long long zz = dropped[g] ? 0ull : zk[2 * (size_t)g] * zk[2 * (size_t)g + 1];
+    if (zz) { bh[g] += zz; zero_hits.push_back(HitRec{g, 0u, 0ull}); }
+  }
   for (uint32_t g = 0; g < P.G; ++g) { S.filtered_residuals += (int64_t)bf[g]; S.hash_hits += (int64_t)bh[g]; }
   if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
   if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
@@ -1240,6 +1370,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(cudaMemcpy(t2.data(), D.hits.as<HitRec>() + from, sizeof(HitRec) * t2.size(), cudaMemcpyDeviceToHost));
       hv.insert(hv.end(), t2.begin(), t2.end());
     }
+    hv.insert(hv.end(), zero_hits.begin(), zero_hits.end());
     rc = recover(hv);
     if (rc) return rc;
     if (opt->mode == MSP_MODE_ALL && recovered_hh != S.hash_hits) {
@@ -1250,6 +1381,14 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   }
   CK(cudaEventRecord(D.ev[3], st));
   CK(cudaEventSynchronize(D.ev[3]));
+  if (dbg_stats) {
+    unsigned long long dv[8];
+    CK(cudaMemcpy(dv, dbg_stats, 64, cudaMemcpyDeviceToHost));
+    int nov = 0;
+    for (uint32_t g = 0; g < P.G; ++g) nov += dropped[g];
+    fprintf(stderr, "[msp dbg] scatter rounds %llu staged %llu overflow %llu pads %llu; keys/round %.0f; overflowed batches %d of %u\n",
+            dv[0], dv[1], dv[2], dv[3], dv[0] ? (double)dv[1] / dv[0] : 0.0, nov, P.G);
+  }
   S.dev_ms_total = elapsed_ms(D.ev[0], D.ev[3]);
   S.exact_hits = (int64_t)sols.size();
   S.t_enumerate = S.t_build;  // the plan replaces the heap stream
