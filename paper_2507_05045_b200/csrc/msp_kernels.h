@@ -81,8 +81,11 @@ void launch_brute(const BruteArgs &a, cudaStream_t st);
 
 // Partitioned join (msp_part.cu).  Buckets of one wave, per role (0 = build, 1 = probe).
 constexpr int kMaxWaveBuckets = 1024;  // buckets per role per wave
-constexpr int kScatterStageKeys = 10240;   // stage slots of a scatter CTA (all entries)
-constexpr int kScatterCtasHost = 2;        // resident k_scatter CTAs per SM (grid = SMs x this)
+#ifndef MSP_SCATTER_CTAS
+#define MSP_SCATTER_CTAS 1
+#endif
+constexpr int kScatterCtasHost = MSP_SCATTER_CTAS;  // resident k_scatter CTAs per SM (grid = SMs x this)
+constexpr int kScatterStageKeys = 20480 / MSP_SCATTER_CTAS;  // stage slots of a scatter CTA
 constexpr int kJoinSlotsLog2 = 14;     // shared-memory join table: 16K (key, count) slots
 constexpr uint32_t kBucketTarget = 1u << (kJoinSlotsLog2 - 1);  // mean build keys per bucket
 struct PartArgs {
@@ -153,6 +156,32 @@ struct RescatterArgs {
 };
 cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st);
 cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
+
+// Persistent pipeline of partitioned waves (msp_part.cu k_waves): scatter chunks of wave w + 1 and
+// join bucket groups of wave w from one task queue, one CTA per SM.
+constexpr uint32_t kJoinGroup = 6;     // buckets per join task
+constexpr uint32_t kWaveBuffers = 3;   // scratch buffers of the pipeline
+struct WaveDesc {
+  uint32_t tile0;                      // first tile of the wave in the tile array
+  uint32_t chunk0, nchunks;            // its scatter chunks (wave-relative tiles) in the chunk array
+  uint32_t unit0;                      // its units in the UnitInfo array
+  uint32_t b0, nb;                     // its buckets (per role) in the bucket arrays
+  uint32_t njoin;                      // its join tasks (ceil(nb / kJoinGroup))
+  uint32_t pad;
+};
+struct WavesArgs {
+  ScatterArgs sc;                      // comp, dpack, tiles (all waves), units (all waves), filters
+  PartArgs pa;                         // hit list, per-batch counters, zero keys, diagnostics
+  const uint32_t *bstart0, *bstart1, *bcap0, *bcap1, *bgid;  // bucket arrays of all waves
+  unsigned long long *scratch[kWaveBuffers];  // wave w uses buffer w % kWaveBuffers
+  uint32_t *fill[kWaveBuffers];
+  const WaveDesc *waves;
+  const unsigned long long *chunks;    // scatter chunks of all waves
+  const unsigned long long *tasks;     // join << 63 | wave << 32 | chunk or first bucket
+  uint32_t ntasks;
+  unsigned int *task_ctr, *scat_done, *join_done;  // zeroed before the launch
+};
+cudaError_t launch_waves(int mc, const WavesArgs &w, int num_sms, cudaStream_t st);
 
 void launch_clear(void *p, size_t bytes, int num_sms, cudaStream_t st);
 

@@ -17,12 +17,12 @@
 // overflows (duplicate-heavy instances) marks its batch, which the host re-joins with the global
 // table path (msp_enum.cu), so results never depend on the partitioning.
 #include <cstdint>
+#include <algorithm>
 #include <type_traits>
 #include "msp_common.cuh"
 #include "msp_kernels.h"
 #include "msp_tile.cuh"
 
-#define MSP_SCATTER_CTAS 2
 
 namespace msp {
 
@@ -30,11 +30,11 @@ namespace msp {
 // write-out) overlaps the other's enumeration.
 constexpr int kScatterCtas = MSP_SCATTER_CTAS;
 static_assert(kScatterCtas == kScatterCtasHost, "scatter CTAs per SM: msp_kernels.h and msp_part.cu disagree");
-constexpr int kScatterWarps = 8;
+constexpr int kScatterWarps = 16 / kScatterCtas;
 constexpr int kScatterThreads = kScatterWarps * 32;
 constexpr int kStageKeys = kScatterStageKeys;                   // stage slots of a CTA
-constexpr int kOvf = 1024;                                      // keys ranked past their entry's C slots
-constexpr int kOvfTrigger = 384;                                // a round ends at this many (default)
+constexpr int kOvf = 2048 / kScatterCtas;                       // keys ranked past their entry's C slots
+constexpr int kOvfTrigger = kOvf * 3 / 8;                       // a round ends at this many (default)
 constexpr int kMaxNB = kMaxWaveBuckets;                         // entries of one unit
 constexpr uint32_t kDrop = 0xFFFFFFFFu;
 
@@ -60,16 +60,14 @@ struct __align__(16) Stage {
   uint32_t ove[kOvf];                // entry | rank << 11
   uint32_t cnt[kMaxNB];              // keys ranked into each entry this round
   uint2 run[kMaxNB];                 // flush: (scratch index of rank 0, staged keys to write)
-  UnitInfo units[kMaxUnits];
-  uint32_t ufilt[kMaxUnits];         // filtered right pairs per unit (k_scatter)
   uint32_t novf, round_end, chunk, ove_spill;  // ove_spill: some rank past C has no key this round
+  uint32_t tctr, pad[3];             // tiles of the chunk handed out past the first 2 per warp
 };
 
 size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kU) * sw * 4; }
 
-__device__ __forceinline__ void stage_init(Stage &g, const UnitInfo *units, uint32_t nunits) {
+__device__ __forceinline__ void stage_init(Stage &g) {
   for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
-  for (uint32_t u = threadIdx.x; u < nunits; u += blockDim.x) { g.units[u] = units[u]; g.ufilt[u] = 0; }
   if (threadIdx.x == 0) { g.novf = 0; g.round_end = 0; g.ove_spill = 0; }
 }
 
@@ -257,10 +255,9 @@ __device__ __forceinline__ void fold(uint32_t &lo, uint32_t &hi, uint32_t v) {
 
 // Companion-vector loads of one tile for this lane: its lane entry and its (lane-th) loop entry.
 template <int SW>
-__device__ __forceinline__ void tile_vecs(const ScatterArgs &A, const Stage &g, const uint4 d, uint32_t lane,
+__device__ __forceinline__ void tile_vecs(const ScatterArgs &A, uint32_t side, const uint4 d, uint32_t lane,
                                           uint32_t (&lv)[SW], uint32_t (&yv)[SW]) {
   const uint32_t meta = d.z;
-  const uint32_t side = (g.units[meta & 0xFFu].ent >> 23) & 1u;
   const bool lx = (meta >> 18) & 1u;
   const uint32_t ln = ((meta >> 8) & 31u) + 1u, qn = ((meta >> 13) & 31u) + 1u;
   const uint32_t *lt = side ? (lx ? A.comp[2] : A.comp[3]) : (lx ? A.comp[0] : A.comp[1]);
@@ -319,96 +316,107 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
   }
 }
 
-// Enumerate + hash + partition.  CTAs take work chunks (consecutive tiles of one unit) from a
-// global counter; the chunk's warps walk tiles warp, warp + W, ... with the descriptor two tiles
-// ahead and the companion vectors one tile ahead in flight.  A round ends for every warp of the
-// CTA as soon as the overflow list passes its trigger (the CTA flushes, then resumes mid-tile) and
-// at the end of the chunk.
+// One work chunk: tiles [t0, n) of ONE unit (one batch side), enumerated + hashed + partitioned by
+// the CTA.  Warps take their first two tiles statically and later ones from a shared counter (so
+// they finish within one tile of each other), with the descriptor two tiles ahead and the
+// companion vectors one tile ahead in flight.  A round ends for every warp as soon as the overflow
+// list passes its trigger (the CTA flushes, then resumes mid-tile) and at the end of the chunk.
+// Filtered right pairs go to batch_filtered.  Ends with a barrier (the last flush).
+template <int MC>
+__device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const ScatterArgs &A, const PartArgs &S,
+                                              const uint32_t (&dg)[words_for(MC) > 0 ? words_for(MC) : 1],
+                                              const UnitInfo ui, uint32_t t0, uint32_t n, unsigned long long &dacc) {
+  constexpr int SW = stride_for(MC);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  volatile uint32_t *round_end = &g.round_end;
+  const uint32_t ebase = ui.ent & 0xFFFu, nbk = (ui.ent >> 12) & 0x7FFu, side = (ui.ent >> 23) & 1u;
+  const bool right = side != 0;
+  uint32_t C, cmagic;
+  stage_geometry(nbk, C, cmagic);
+  if (tid == 0) g.tctr = 0;
+  __syncthreads();
+  auto grab = [&]() {
+    uint32_t x = 0;
+    if (lane == 0) x = atomicAdd(&g.tctr, 1u);
+    return t0 + 2 * kScatterWarps + __shfl_sync(0xffffffffu, x, 0);
+  };
+  uint32_t t = t0 + warp, tn = t + kScatterWarps, tnn = grab();
+  uint4 dcur = ld_tile(A.tiles, t, n), dnxt = ld_tile(A.tiles, tn, n), dnn = ld_tile(A.tiles, tnn, n);
+  uint32_t lvc[SW], yvc[SW], lvn[SW], yvn[SW];
+  if (t < n) tile_vecs<SW>(A, side, dcur, lane, lvc, yvc);
+  if (tn < n) tile_vecs<SW>(A, side, dnxt, lane, lvn, yvn);
+  bool have = t < n;
+  uint32_t q = 0, qn = 0;
+  bool lok = false;
+  unsigned long long filt = 0;
+  auto begin_tile = [&]() {
+    const uint32_t meta = dcur.z;
+    qn = ((meta >> 13) & 31u) + 1u;
+    lok = lane <= ((meta >> 8) & 31u);
+    q = 0;
+    __syncwarp();
+    if (lane < qn) {
+#pragma unroll
+      for (int k = 0; k < SW; ++k) ybuf[lane * SW + k] = yvc[k];
+    }
+    __syncwarp();
+  };
+  if (have) begin_tile();
+  while (true) {
+    while (have && !*round_end) {
+      if (right)
+        hash_step<MC, true>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
+      else
+        hash_step<MC, false>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
+      q += kU;
+      if (q >= qn) {  // next tile: everything it needs was loaded one (vectors) or two tiles ago
+        t = tn;
+        tn = tnn;
+        have = t < n;
+        if (have) {
+          dcur = dnxt;
+#pragma unroll
+          for (int k = 0; k < SW; ++k) { lvc[k] = lvn[k]; yvc[k] = yvn[k]; }
+          dnxt = dnn;
+          if (tn < n) tile_vecs<SW>(A, side, dnxt, lane, lvn, yvn);
+          tnn = tn < n ? grab() : n;
+          dnn = ld_tile(A.tiles, tnn, n);
+          begin_tile();
+        }
+      }
+    }
+    const bool more = __syncthreads_or(have);
+    flush_round(g, S, ebase, nbk, C, cmagic);
+    if (!more) break;
+  }
+  if (right) {
+    const unsigned long long f = warp_sum(filt);
+    if (lane == 0 && f) atomicAdd(A.batch_filtered + ui.gid, f);
+  }
+}
+
+// Enumerate + hash + partition one launch (the huge-batch level-1 pass, and the per-wave launch
+// path used under MSP_FLAG_PROFILE): CTA b runs chunks [cta_first[b], cta_first[b+1]).
 template <int MC>
 __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const ScatterArgs A, const PartArgs S) {
   constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage &g = *reinterpret_cast<Stage *>(smem_raw);
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kU) * SW;
-  stage_init(g, A.units, A.nunits);
+  stage_init(g);
   for (uint32_t i = lane; i < (uint32_t)((kTQ + kU) * SW); i += 32) ybuf[i] = 0;
   uint32_t dg[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
-  unsigned long long filt = 0, dacc = 0;
-  volatile uint32_t *round_end = &g.round_end;
-  __syncthreads();  // units and counters of stage_init
-
-  // static mode (cta_first): CTA b owns chunks [cta_first[b], cta_first[b+1]); else dynamic
-  const bool stat = A.cta_first != nullptr;
-  const uint32_t cend = stat ? __ldg(A.cta_first + blockIdx.x + 1) : A.nchunks;
-  for (uint32_t c = stat ? __ldg(A.cta_first + blockIdx.x) : next_chunk(g, A.chunk_ctr); c < cend;
-       c = stat ? c + 1 : next_chunk(g, A.chunk_ctr)) {
+  unsigned long long dacc = 0;
+  __syncthreads();
+  const uint32_t cend = __ldg(A.cta_first + blockIdx.x + 1);
+  for (uint32_t c = __ldg(A.cta_first + blockIdx.x); c < cend; ++c) {
     const unsigned long long cw = __ldg(A.chunks + c);
     const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
-    const UnitInfo ui = g.units[unit];
-    const uint32_t ebase = ui.ent & 0xFFFu, nbk = (ui.ent >> 12) & 0x7FFu;
-    const bool right = (ui.ent >> 23) & 1u;
-    uint32_t C, cmagic;
-    stage_geometry(nbk, C, cmagic);
-
-    uint32_t t = t0 + warp;
-    uint4 dcur = ld_tile(A.tiles, t, n), dnxt = ld_tile(A.tiles, t + kScatterWarps, n),
-          dnn = ld_tile(A.tiles, t + 2 * kScatterWarps, n);
-    uint32_t lvc[SW], yvc[SW], lvn[SW], yvn[SW];
-    if (t < n) tile_vecs<SW>(A, g, dcur, lane, lvc, yvc);
-    if (t + kScatterWarps < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
-    bool have = t < n;
-    uint32_t q = 0, qn = 0;
-    bool lok = false;
-    auto begin_tile = [&]() {
-      const uint32_t meta = dcur.z;
-      qn = ((meta >> 13) & 31u) + 1u;
-      lok = lane <= ((meta >> 8) & 31u);
-      q = 0;
-      __syncwarp();
-      if (lane < qn) {
-#pragma unroll
-        for (int k = 0; k < SW; ++k) ybuf[lane * SW + k] = yvc[k];
-      }
-      __syncwarp();
-    };
-    if (have) begin_tile();
-    while (true) {
-      while (have && !*round_end) {
-        if (right)
-          hash_step<MC, true>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
-        else
-          hash_step<MC, false>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
-        q += kU;
-        if (q >= qn) {  // next tile: everything it needs was loaded one (vectors) or two tiles ago
-          t += kScatterWarps;
-          have = t < n;
-          if (have) {
-            dcur = dnxt;
-#pragma unroll
-            for (int k = 0; k < SW; ++k) { lvc[k] = lvn[k]; yvc[k] = yvn[k]; }
-            dnxt = dnn;
-            if (t + kScatterWarps < n) tile_vecs<SW>(A, g, dnxt, lane, lvn, yvn);
-            dnn = ld_tile(A.tiles, t + 2 * kScatterWarps, n);
-            begin_tile();
-          }
-        }
-      }
-      const bool more = __syncthreads_or(have);
-      flush_round(g, S, ebase, nbk, C, cmagic);
-      if (!more) break;
-    }
-    if (right) {  // filtered right pairs of the chunk into the unit's shared counter
-      const unsigned long long f = warp_sum(filt);
-      if (lane == 0 && f) atomicAdd(&g.ufilt[unit], (uint32_t)f);
-      filt = 0;
-    }
+    scatter_chunk<MC>(g, ybuf, A, S, dg, A.units[unit], t0, n, dacc);
   }
-  __syncthreads();
-  for (uint32_t u = tid; u < A.nunits; u += blockDim.x)
-    if (g.ufilt[u]) atomicAdd(A.batch_filtered + g.units[u].gid, (unsigned long long)g.ufilt[u]);
   if (dacc == 0x123456789ull) A.batch_filtered[0] = dacc;  // keep the diagnostic keys live
 }
 
@@ -421,7 +429,8 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_rescatter(con
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage &g = *reinterpret_cast<Stage *>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  stage_init(g, nullptr, 0);
+  stage_init(g);
+  __syncthreads();
   volatile uint32_t *round_end = &g.round_end;
   constexpr int N = 2;
   for (uint32_t c = next_chunk(g, R.chunk_ctr); c < R.nchunks; c = next_chunk(g, R.chunk_ctr)) {
@@ -457,20 +466,24 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_rescatter(con
 
 constexpr int kJoinThreads = 1024;
 constexpr int kJoinSlots = 1 << kJoinSlotsLog2;        // 16K key slots
-constexpr int kJBuckets = kJoinSlots / 4;               // 4K buckets of 4 slots
+constexpr int kJWays = 8;                               // slots per table bucket
+constexpr int kJBuckets = kJoinSlots / kJWays;          // 2K buckets of 8 slots
 constexpr int kStash = 256;                             // keys whose two buckets were both full
 constexpr int kHitWords = (kJoinSlots + kStash) / 32;
 
-// Shared-memory join table of one bucket: two-choice hashing into 4-slot buckets.  Each slot keeps
-// the full 64-bit key and, in a packed word per bucket, a 16-bit fingerprint, so a probe reads two
-// fingerprint words and two counts and compares four fingerprints per word with one SIMD compare;
-// the full keys are read only on a fingerprint match (~1e-4 of probes plus the true hits).  No
-// probe ever loops, so warps do not diverge on chain lengths.  Only the counts are cleared per
-// bucket (slots past a bucket's count are never read).
+// Shared-memory join table of one bucket: 8-slot buckets, first fit in bucket b1, then b2, then a
+// small stash.  Each slot keeps the full 64-bit key and an 8-bit fingerprint (0 = empty); the eight
+// fingerprints of a bucket are one 64-bit word.  An insert is one shared atomic + two stores; a
+// probe reads ONE fingerprint word and tests all eight lanes at once (zero-byte test), reading
+// full keys only on a fingerprint match (~3% of probes plus the true hits).  A key can sit in b2
+// only if b1 is full (no zero lane), so b2 is read only by probes whose b1 is full.  Keys arriving
+// here are FNV outputs whose top bits chose the bucket; b1/b2 come from a multiplicative mix of the
+// low word, the fingerprint from the middle of the high word.  Only counts and fingerprints are
+// cleared per bucket.
 struct JoinSmem {
-  unsigned long long key[kJBuckets][4];
-  unsigned long long fp[kJBuckets];     // four 16-bit fingerprints
-  uint32_t cnt[kJBuckets];              // claims (may exceed 4: failed claims spill over)
+  unsigned long long key[kJBuckets][kJWays];
+  unsigned long long fp[kJBuckets];     // eight 8-bit fingerprints
+  uint32_t cnt[kJBuckets];              // claims (may exceed 8: failed claims move on)
   unsigned long long stash[kStash];
   uint32_t hitbits[kHitWords];
   unsigned long long bhits[kJoinThreads / 32];
@@ -481,142 +494,257 @@ size_t join_smem_bytes() { return sizeof(JoinSmem); }
 
 struct JoinHash { uint32_t b1, b2, fp; };
 __device__ __forceinline__ JoinHash join_hash(unsigned long long k) {
-  const unsigned long long m = k * kGolden;  // odd multiplier: a bijection on 64-bit keys
+  const uint32_t t = (uint32_t)k * 0x9E3779B1u, hi = (uint32_t)(k >> 32);
   JoinHash h;
-  h.b1 = (uint32_t)(m >> 52);
-  h.b2 = (uint32_t)(m >> 40) & (kJBuckets - 1);
+  h.b1 = t >> 21;
+  h.b2 = (t >> 10) & (kJBuckets - 1);
   if (h.b2 == h.b1) h.b2 ^= 1u;
-  h.fp = (uint32_t)(m >> 24) & 0xFFFFu;
-  if (h.fp == 0) h.fp = 1;  // 0 marks an empty slot: a probe needs no slot counts
+  h.fp = (hi >> 8) & 0xFFu;
+  if (h.fp == 0) h.fp = 1;  // 0 marks an empty slot
   return h;
 }
 
-// Lanes of `w` (four 16-bit fingerprints) equal to fp, as a 4-bit mask, restricted to n slots.
-__device__ __forceinline__ uint32_t fp_match(unsigned long long w, uint32_t fp, uint32_t n) {
-  const uint32_t f2 = fp * 0x10001u;
-  const uint32_t lo = __vcmpeq2((uint32_t)w, f2), hi = __vcmpeq2((uint32_t)(w >> 32), f2);
-  const uint32_t m = (lo & 1u) | ((lo >> 15) & 2u) | ((hi & 1u) << 2) | ((hi >> 13) & 8u);
-  return m & ((1u << n) - 1u);
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {  // nonzero iff some byte of x is 0
+  return (x - 0x01010101u) & ~x & 0x80808080u;
+}
+__device__ __forceinline__ bool any_lane_eq(unsigned long long w, uint32_t pat) {
+  return (zero_bytes((uint32_t)w ^ pat) | zero_bytes((uint32_t)(w >> 32) ^ pat)) != 0u;
+}
+__device__ __forceinline__ bool bucket_full(unsigned long long w) {
+  return (zero_bytes((uint32_t)w) | zero_bytes((uint32_t)(w >> 32))) == 0u;
 }
 
 __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   const JoinHash h = join_hash(k);
-  const uint32_t c1 = T.cnt[h.b1], c2 = T.cnt[h.b2];
-  uint32_t b = c1 <= c2 ? h.b1 : h.b2, o = c1 <= c2 ? h.b2 : h.b1;
-  uint32_t s = atomicAdd(&T.cnt[b], 1u);
-  if (s >= 4) { b = o; s = atomicAdd(&T.cnt[b], 1u); }
-  if (s < 4) {
+  uint32_t b = h.b1, s = atomicAdd(&T.cnt[b], 1u);
+  if (s >= (uint32_t)kJWays) { b = h.b2; s = atomicAdd(&T.cnt[b], 1u); }
+  if (s < (uint32_t)kJWays) {
     T.key[b][s] = k;
-    reinterpret_cast<uint16_t *>(&T.fp[b])[s] = (uint16_t)h.fp;  // slot s is this thread's alone
+    reinterpret_cast<uint8_t *>(&T.fp[b])[s] = (uint8_t)h.fp;  // slot s is this thread's alone
   } else {
     const uint32_t i = atomicAdd(&T.nstash, 1u);
     if (i < (uint32_t)kStash) T.stash[i] = k; else T.ovf = 1u;
   }
 }
 
-// Multiplicity of k in the table; *first = slot id of its first copy (bucket-major, then stash).
-// Fast path: two fingerprint words, one zero-lane test each (no slot counts, no loop).
+__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, unsigned long long w, uint32_t fp,
+                                                unsigned long long k, uint32_t &c, uint32_t &first) {
+#pragma unroll
+  for (int s = 0; s < kJWays; ++s)
+    if (((w >> (8 * s)) & 0xFFu) == fp && T.key[b][s] == k) {
+      if (!c) first = b * kJWays + s;
+      ++c;
+    }
+}
+
+// Multiplicity of k in the table; `first` = slot id of its first copy (b1, then b2, then stash).
 __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long long k, uint32_t nstash,
                                                uint32_t &first) {
-  constexpr unsigned long long kL = 0x0001000100010001ull, kH = 0x8000800080008000ull;
   const JoinHash h = join_hash(k);
-  const unsigned long long w1 = T.fp[h.b1], w2 = T.fp[h.b2], pat = h.fp * kL;
-  const unsigned long long x1 = w1 ^ pat, x2 = w2 ^ pat;
+  const uint32_t pat = h.fp * 0x01010101u;
+  const unsigned long long w1 = T.fp[h.b1];
   uint32_t c = 0;
   first = 0xFFFFFFFFu;
-  if ((((x1 - kL) & ~x1) | ((x2 - kL) & ~x2)) & kH) {  // some lane may hold fp: compare full keys
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if (((w1 >> (16 * s)) & 0xFFFFu) == h.fp && T.key[h.b1][s] == k) { if (!c) first = h.b1 * 4 + s; ++c; }
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if (((w2 >> (16 * s)) & 0xFFFFu) == h.fp && T.key[h.b2][s] == k) { if (!c) first = h.b2 * 4 + s; ++c; }
+  if (any_lane_eq(w1, pat)) count_in_bucket(T, h.b1, w1, h.fp, k, c, first);
+  if (bucket_full(w1)) {  // k may have moved on to b2 (and, if b2 is full too, to the stash)
+    const unsigned long long w2 = T.fp[h.b2];
+    if (any_lane_eq(w2, pat)) count_in_bucket(T, h.b2, w2, h.fp, k, c, first);
+    if (bucket_full(w2))
+      for (uint32_t i = 0; i < nstash; ++i)
+        if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
   }
-  for (uint32_t i = 0; i < nstash; ++i)
-    if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
   return c;
+}
+
+// Join of bucket b of a wave by one CTA of NT threads: clear the table, insert the build keys,
+// probe with the probe keys (fastval.py:75-107 semantics: every full-64-bit-hash-equal pair is a
+// hit), record each hit key once, reset the bucket's fill counters for the next use of the buffer.
+// Key 0 only pads runs (real zero keys are counted by the scatter) and is skipped, as are the
+// zero-filled loads past the bucket's end.  Ends with a barrier.
+template <int NT>
+__device__ __forceinline__ void join_bucket(JoinSmem &T, const PartArgs &S, uint32_t b) {
+  const uint32_t tid = threadIdx.x;
+  constexpr int U = 8;  // keys loaded per thread before the table operations
+  long long tp0 = 0, tp1 = 0, tp2 = 0;
+  if (S.dbg && tid == 0) tp0 = clock64();
+  for (uint32_t i = tid; i < (uint32_t)kJBuckets; i += NT) { T.cnt[i] = 0u; T.fp[i] = 0ull; }
+  for (uint32_t i = tid; i < (uint32_t)kHitWords; i += NT) T.hitbits[i] = 0u;
+  if (tid == 0) { T.nstash = 0; T.ovf = 0; }
+  const uint32_t gid = __ldg(S.gid + b);
+  const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
+  const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
+  const unsigned long long *bk = S.scratch + __ldg(S.start[0] + b);
+  const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
+  unsigned long long kv[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {  // first build keys in flight across the clear
+    const uint32_t i = u * NT + tid;
+    kv[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
+  }
+  __syncthreads();
+  for (uint32_t base = 0; base < nbuild; base += NT * U) {
+    unsigned long long nx[U];  // next keys in flight while this batch is inserted
+    const uint32_t nb2 = base + NT * U;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = nb2 + u * NT + tid;
+      nx[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (kv[u]) join_insert(T, kv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) kv[u] = nx[u];
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {  // first probe keys in flight across the barrier
+    const uint32_t i = u * NT + tid;
+    kv[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
+  }
+  __syncthreads();
+  if (S.dbg && tid == 0) tp1 = clock64();
+  const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
+  if (T.ovf && tid == 0) atomicOr(S.batch_ovf + gid, 1u);
+  unsigned long long hits = 0;
+  for (uint32_t base = 0; base < nprobe; base += NT * U) {
+    unsigned long long nx[U];  // next keys in flight while this batch is probed
+    const uint32_t nb2 = base + NT * U;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = nb2 + u * NT + tid;
+      nx[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned long long k = kv[u];
+      if (!k) continue;
+      uint32_t first;
+      const uint32_t c = join_count(T, k, nstash, first);
+      if (c) {
+        hits += c;
+        if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
+          const unsigned long long h = atomicAdd(S.nhits, 1ull);
+          if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) kv[u] = nx[u];
+  }
+  hits = warp_sum(hits);
+  if ((tid & 31) == 0) T.bhits[tid >> 5] = hits;
+  __syncthreads();
+  if (S.dbg && tid == 0) {
+    tp2 = clock64();
+    atomicAdd(S.dbg + 8, (unsigned long long)(tp1 - tp0));
+    atomicAdd(S.dbg + 9, (unsigned long long)(tp2 - tp1));
+    atomicAdd(S.dbg + 10, (unsigned long long)nstash);
+    atomicAdd(S.dbg + 11, 1ull);
+  }
+  if (tid == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < NT / 32; ++w) t += T.bhits[w];
+    if (t) atomicAdd(S.batch_hits + gid, t);
+    S.fill[0][b] = 0;
+    S.fill[1][b] = 0;
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   JoinSmem &T = *reinterpret_cast<JoinSmem *>(smem_raw);
-  const uint32_t tid = threadIdx.x;
-  constexpr int U = 8;  // keys loaded per thread before the table operations
+  for (uint32_t b = blockIdx.x; b < S.nb; b += gridDim.x) join_bucket<kJoinThreads>(T, S, b);
+}
 
-  for (uint32_t b = blockIdx.x; b < S.nb; b += gridDim.x) {
-    for (uint32_t i = tid; i < (uint32_t)kJBuckets; i += kJoinThreads) { T.cnt[i] = 0u; T.fp[i] = 0ull; }
-    for (uint32_t i = tid; i < (uint32_t)kHitWords; i += kJoinThreads) T.hitbits[i] = 0u;
-    if (tid == 0) { T.nstash = 0; T.ovf = 0; }
-    const uint32_t gid = __ldg(S.gid + b);
-    const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
-    const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
-    const unsigned long long *bk = S.scratch + __ldg(S.start[0] + b);
-    const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
-    unsigned long long kv[U];
+// ---------------------------------------------------------------- persistent wave pipeline
+
+// All partitioned waves of a solve in ONE launch, one CTA per SM: CTAs pull tasks in queue order
+// S(0) S(1) J(0) S(2) J(1) ... where S(w) are wave w's scatter chunks and J(w) its join bucket
+// groups.  J(w) waits for every chunk of S(w) (scat_done[w]); S(w) waits for J(w-3) (join_done),
+// the last reader of its scratch buffer w % 3 (three buffers, so S(w) never waits on the joins
+// handed out just before it).  Every wait points at tasks earlier in the queue,
+// already held by resident CTAs, so the pipeline cannot deadlock; joins of wave w run on some SMs
+// while others scatter wave w + 1, and no wave ends in a launch tail.
+template <int MC>
+__global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W) {
+  constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Stage &g = *reinterpret_cast<Stage *>(smem_raw);
+  JoinSmem &T = *reinterpret_cast<JoinSmem *>(smem_raw);  // (union with the stage)
+  __shared__ unsigned long long s_task;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kU) * SW;
+  for (uint32_t i = lane; i < (uint32_t)((kTQ + kU) * SW); i += 32) ybuf[i] = 0;
+  uint32_t dg[NW];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {  // first build keys in flight across the clear
-      const uint32_t i = u * kJoinThreads + tid;
-      kv[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
-    }
-    __syncthreads();
-    for (uint32_t base = 0; base < nbuild; base += kJoinThreads * U) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (base + u * kJoinThreads + tid >= nbuild) continue;
-        if (kv[u] == 0) continue;  // run pad (real zero keys are counted by the scatter)
-        join_insert(T, kv[u]);
-      }
-      const uint32_t nb2 = base + kJoinThreads * U;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t i = nb2 + u * kJoinThreads + tid;
-        kv[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {  // first probe keys in flight across the barrier
-      const uint32_t i = u * kJoinThreads + tid;
-      kv[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
-    }
-    __syncthreads();
-    const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
-    if (T.ovf && tid == 0) atomicOr(S.batch_ovf + gid, 1u);
-    unsigned long long hits = 0;
-    for (uint32_t base = 0; base < nprobe; base += kJoinThreads * U) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const unsigned long long k = kv[u];
-        if (base + u * kJoinThreads + tid >= nprobe) continue;
-        if (k == 0) continue;  // run pad
-        uint32_t first;
-        const uint32_t c = join_count(T, k, nstash, first);
-        if (c) {
-          hits += c;
-          if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
-            const unsigned long long h = atomicAdd(S.nhits, 1ull);
-            if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
-          }
-        }
-      }
-      const uint32_t nb2 = base + kJoinThreads * U;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t i = nb2 + u * kJoinThreads + tid;
-        kv[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
-      }
-    }
-    hits = warp_sum(hits);
-    if ((tid & 31) == 0) T.bhits[tid >> 5] = hits;
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long t = 0;
-      for (int w = 0; w < kJoinThreads / 32; ++w) t += T.bhits[w];
-      if (t) atomicAdd(S.batch_hits + gid, t);
-      S.fill[0][b] = 0;
-      S.fill[1][b] = 0;
-    }
-    __syncthreads();
+  for (int k = 0; k < NW; ++k) dg[k] = W.sc.dpack[k];
+  unsigned long long dacc = 0;
+  long long t_prev = clock64();
+  // thread 0 keeps the NEXT task (index claimed and word loaded) in flight while the CTA works
+  unsigned long long tk_next = ~0ull;
+  if (tid == 0) {
+    const uint32_t i = atomicAdd(W.task_ctr, 1u);
+    tk_next = i < W.ntasks ? W.tasks[i] : ~0ull;
   }
+  while (true) {
+    if (tid == 0) {
+      unsigned long long tk = tk_next;
+      if (tk != ~0ull) {
+        const uint32_t i = atomicAdd(W.task_ctr, 1u);
+        tk_next = i < W.ntasks ? W.tasks[i] : ~0ull;
+      }
+      if (tk != ~0ull) {  // wait for the task's dependency
+        const uint32_t w = (uint32_t)(tk >> 32) & 0x7FFFFFFFu;
+        const bool join = tk >> 63;
+        const uint32_t prev = w >= kWaveBuffers ? w - kWaveBuffers : 0u;  // last wave on this buffer
+        volatile unsigned int *ctr = join ? W.scat_done + w : (w >= kWaveBuffers ? W.join_done + prev : nullptr);
+        const uint32_t need = join ? W.waves[w].nchunks : (w >= kWaveBuffers ? W.waves[prev].njoin : 0u);
+        const long long tw = clock64();
+        if (ctr) while (*ctr < need) __nanosleep(256);
+        __threadfence();
+        if (W.pa.dbg) atomicAdd(W.pa.dbg + 6, (unsigned long long)(clock64() - tw));
+      }
+      s_task = tk;
+    }
+    __syncthreads();
+    const unsigned long long tk = s_task;
+    if (tk == ~0ull) break;
+    const uint32_t w = (uint32_t)(tk >> 32) & 0x7FFFFFFFu, idx = (uint32_t)tk;
+    const WaveDesc wd = W.waves[w];
+    PartArgs S = W.pa;
+    S.scratch = W.scratch[w % kWaveBuffers];
+    S.fill[0] = W.fill[w % kWaveBuffers];
+    S.fill[1] = W.fill[w % kWaveBuffers] + kMaxWaveBuckets;
+    S.start[0] = W.bstart0 + wd.b0;
+    S.start[1] = W.bstart1 + wd.b0;
+    S.cap[0] = W.bcap0 + wd.b0;
+    S.cap[1] = W.bcap1 + wd.b0;
+    S.gid = W.bgid + wd.b0;
+    S.nb = wd.nb;
+    S.roles = 2;
+    if (tk >> 63) {  // join: buckets [idx, idx + kJoinGroup) of the wave
+      const uint32_t b1 = min(idx + (uint32_t)kJoinGroup, wd.nb);
+      for (uint32_t b = idx; b < b1; ++b) join_bucket<kScatterThreads>(T, S, b);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(W.join_done + w, 1u);
+      if (tid == 0 && W.pa.dbg) { const long long now = clock64(); atomicAdd(W.pa.dbg + 5, (unsigned long long)(now - t_prev)); t_prev = now; }
+    } else {  // scatter chunk idx of the wave
+      ScatterArgs A = W.sc;
+      A.tiles = W.sc.tiles + wd.tile0;
+      stage_init(g);
+      __syncthreads();
+      const unsigned long long cw = __ldg(W.chunks + wd.chunk0 + idx);
+      const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
+      scatter_chunk<MC>(g, ybuf, A, S, dg, W.sc.units[wd.unit0 + unit], t0, n, dacc);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(W.scat_done + w, 1u);
+      if (tid == 0 && W.pa.dbg) { const long long now = clock64(); atomicAdd(W.pa.dbg + 4, (unsigned long long)(now - t_prev)); t_prev = now; }
+    }
+  }
+  if (dacc == 0x123456789ull) W.sc.batch_filtered[0] = dacc;
 }
 
 template <int MC>
@@ -638,6 +766,31 @@ cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, i
   const int grid = args.cta_first ? (int)slots : (int)(args.nchunks < slots ? args.nchunks : slots);
   switch (mc) {
 #define MSP_CASE(N) case N: return launch_scatter_mc<N>(args, p, grid, st);
+    MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
+    MSP_CASE(8) MSP_CASE(9) MSP_CASE(10) MSP_CASE(11) MSP_CASE(12) MSP_CASE(13) MSP_CASE(14)
+    MSP_CASE(15)
+#undef MSP_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int MC>
+static cudaError_t launch_waves_mc(const WavesArgs &w, int grid, cudaStream_t st) {
+  static bool configured = false;
+  const size_t sm = std::max(scatter_smem_bytes(stride_for(MC)), sizeof(JoinSmem));
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_waves<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_waves<MC><<<grid, kScatterThreads, sm, st>>>(w);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_waves(int mc, const WavesArgs &w, int num_sms, cudaStream_t st) {
+  if (w.ntasks == 0) return cudaSuccess;
+  switch (mc) {
+#define MSP_CASE(N) case N: return launch_waves_mc<N>(w, num_sms, st);
     MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
     MSP_CASE(8) MSP_CASE(9) MSP_CASE(10) MSP_CASE(11) MSP_CASE(12) MSP_CASE(13) MSP_CASE(14)
     MSP_CASE(15)

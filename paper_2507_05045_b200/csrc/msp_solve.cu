@@ -85,8 +85,8 @@ struct Device {
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
-  DBuf scratch2, fill2;
-  DBuf tdesc, gstb, gsu, uinfo, chunks, cchunks, l2chunks, cctr, cfirst, ccfirst;
+  DBuf scratch2, fill2, scratch3, fill3;
+  DBuf tdesc, gstb, gsu, uinfo, chunks, cchunks, l2chunks, cctr, cfirst, ccfirst, tchunks, wdesc, wctr, tasks;
   uint32_t cctr_next = 0;  // next unused chunk counter in cctr (zeroed per solve)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
@@ -95,8 +95,8 @@ struct Device {
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
                    &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
-                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &tdesc, &gstb, &gsu, &uinfo,
-                   &chunks, &cchunks, &l2chunks, &cctr, &cfirst, &ccfirst};
+                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &scratch3, &fill3, &tdesc, &gstb, &gsu, &uinfo,
+                   &chunks, &cchunks, &l2chunks, &cctr, &cfirst, &ccfirst, &tchunks, &wdesc, &wctr, &tasks};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
                                   comp[i].release(); rs[i].release(); re[i].release(); }
@@ -518,6 +518,7 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 uint32_t even_up(double x) { const uint32_t v = (uint32_t)x; return v + (v & 1u); }
 
 constexpr uint32_t kChunkCounters = 1u << 16;
+constexpr uint64_t kTaskTiles = 96;  // tiles per scatter task of the persistent wave pipeline
 
 // Static split of a launch's tiles (units given as consecutive tile ranges [ub[i], ub[i+1])) over
 // `nct` CTAs: CTA b gets tiles [b*T/nct, (b+1)*T/nct), cut at unit boundaries into chunks.
@@ -802,8 +803,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     return MSP_OK;
   };
   if (getenv("MSP_DEBUG_STATS")) {
-    CK(D.dbg.ensure(64));
-    CK(cudaMemsetAsync(D.dbg.p, 0, 64, st));
+    CK(D.dbg.ensure(128));
+    CK(cudaMemsetAsync(D.dbg.p, 0, 128, st));
     dbg_stats = D.dbg.as<unsigned long long>();
   }
   if (const char *ev = getenv("MSP_WAVE_BUCKETS")) wave_buckets = (uint32_t)std::max(1, std::min(kMaxWaveBuckets, atoi(ev)));
@@ -944,7 +945,87 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
       ScatterArgs sa = scatter_base(P, A);
-      for (size_t wi = 0; wi < pw.size(); ++wi) {
+      if (!profile) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
+        std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
+        std::vector<WaveDesc> wds(pw.size());
+        for (size_t wi = 0; wi < pw.size(); ++wi) {
+          const PWave &w = pw[wi];
+          WaveDesc &wd = wds[wi];
+          wd.tile0 = (uint32_t)w.t0;
+          wd.chunk0 = (uint32_t)tch.size();
+          uint64_t t = 0;
+          for (size_t i = w.u0; i < w.u1; ++i) {
+            const uint64_t nt = P.tiles[2 * (size_t)units[i].gid + units[i].side];
+            for (uint64_t k = 0; k < nt; k += kTaskTiles) {
+              const uint64_t c = std::min<uint64_t>(kTaskTiles, nt - k);
+              tch.push_back((t + k) | (c << 32) | ((unsigned long long)(i - w.u0) << 48));
+            }
+            t += nt;
+          }
+          wd.nchunks = (uint32_t)(tch.size() - wd.chunk0);
+          wd.unit0 = (uint32_t)w.u0;
+          wd.b0 = (uint32_t)w.b0;
+          wd.nb = (uint32_t)w.nb;
+          wd.njoin = (uint32_t)((w.nb + kJoinGroup - 1) / kJoinGroup);
+        }
+        CK(D.tchunks.ensure(8 * std::max<size_t>(1, tch.size())));
+        CK(cudaMemcpyAsync(D.tchunks.p, tch.data(), 8 * tch.size(), cudaMemcpyHostToDevice, st));
+        CK(D.wdesc.ensure(sizeof(WaveDesc) * wds.size()));
+        CK(cudaMemcpyAsync(D.wdesc.p, wds.data(), sizeof(WaveDesc) * wds.size(), cudaMemcpyHostToDevice, st));
+        CK(D.wctr.ensure(4 * (1 + 2 * pw.size())));
+        CK(cudaMemsetAsync(D.wctr.p, 0, 4 * (1 + 2 * pw.size()), st));
+        WavesArgs W{};
+        W.sc = sa;
+        W.sc.tiles = D.tdesc.as<TileDesc>();
+        W.sc.units = D.uinfo.as<UnitInfo>();
+        W.pa = pa;
+        W.bstart0 = bkd; W.bstart1 = bkd + nbt; W.bcap0 = bkd + 2 * nbt; W.bcap1 = bkd + 3 * nbt; W.bgid = bkd + 4 * nbt;
+        {  // a third scratch buffer (the per-wave launch path uses two)
+          uint64_t mx = 0;
+          for (const PWave &w : pw) mx = std::max(mx, w.scratch);
+          CK(D.scratch3.ensure(8 * (mx + kSinkSlots)));
+          CK(D.fill3.ensure(4 * 2 * kMaxWaveBuckets));
+          CK(cudaMemsetAsync(D.fill3.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+        }
+        W.scratch[0] = D.scratch.as<unsigned long long>();
+        W.scratch[1] = D.scratch2.as<unsigned long long>();
+        W.scratch[2] = D.scratch3.as<unsigned long long>();
+        W.fill[0] = D.fill.as<uint32_t>();
+        W.fill[1] = D.fill2.as<uint32_t>();
+        W.fill[2] = D.fill3.as<uint32_t>();
+        W.waves = D.wdesc.as<WaveDesc>();
+        W.chunks = D.tchunks.as<unsigned long long>();
+        W.task_ctr = D.wctr.as<unsigned int>();
+        W.scat_done = W.task_ctr + 1;
+        W.join_done = W.scat_done + pw.size();
+        const size_t seg = periodic ? 16 : pw.size();
+        for (size_t s0 = 0; s0 < pw.size() && !stopped; s0 += seg) {
+          const size_t s1 = std::min(pw.size(), s0 + seg);
+          std::vector<unsigned long long> tasks;  // S(s0) S(s0+1) J(s0) S(s0+2) J(s0+1) ... J(s1-1)
+          auto push_join = [&](size_t w) {
+            for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks.push_back((1ull << 63) | ((unsigned long long)w << 32) | b);
+          };
+          for (size_t w = s0; w < s1; ++w) {
+            for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks.push_back(((unsigned long long)w << 32) | c);
+            if (w > s0) push_join(w - 1);
+          }
+          push_join(s1 - 1);
+          CK(D.tasks.ensure(8 * tasks.size()));
+          CK(cudaMemcpyAsync(D.tasks.p, tasks.data(), 8 * tasks.size(), cudaMemcpyHostToDevice, st));
+          CK(cudaMemsetAsync(W.task_ctr, 0, 4, st));
+          W.tasks = D.tasks.as<unsigned long long>();
+          W.ntasks = (uint32_t)tasks.size();
+          CK(launch_waves(P.mc, W, D.num_sms, st));
+          S.kernel_launches += 1;
+          if (periodic) {
+            bool stop_now = false;
+            rc = checkpoint(stop_now);
+            if (rc) return rc;
+            if (stop_now) stopped = true;
+          }
+        }
+      }
+      for (size_t wi = 0; profile && wi < pw.size(); ++wi) {
         const PWave &w = pw[wi];
         pa.start[0] = bkd + w.b0;
         pa.start[1] = bkd + nbt + w.b0;
@@ -1382,12 +1463,16 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   CK(cudaEventRecord(D.ev[3], st));
   CK(cudaEventSynchronize(D.ev[3]));
   if (dbg_stats) {
-    unsigned long long dv[8];
-    CK(cudaMemcpy(dv, dbg_stats, 64, cudaMemcpyDeviceToHost));
+    unsigned long long dv[16];
+    CK(cudaMemcpy(dv, dbg_stats, 128, cudaMemcpyDeviceToHost));
     int nov = 0;
     for (uint32_t g = 0; g < P.G; ++g) nov += dropped[g];
-    fprintf(stderr, "[msp dbg] scatter rounds %llu staged %llu overflow %llu pads %llu; keys/round %.0f; overflowed batches %d of %u\n",
-            dv[0], dv[1], dv[2], dv[3], dv[0] ? (double)dv[1] / dv[0] : 0.0, nov, P.G);
+    fprintf(stderr, "[msp dbg] scatter rounds %llu staged %llu overflow %llu; keys/round %.0f; overflowed batches %d of %u; "
+            "SM-ms scatter %.1f join %.1f (incl. wait %.1f)\n",
+            dv[0], dv[1], dv[2], dv[0] ? (double)dv[1] / dv[0] : 0.0, nov, P.G, dv[4] / 1.965e6, dv[5] / 1.965e6,
+            dv[6] / 1.965e6);
+    fprintf(stderr, "[msp dbg] join buckets %llu: build phase %.1f SM-ms, probe phase %.1f SM-ms, mean stash %.2f\n",
+            dv[11], dv[8] / 1.965e6, dv[9] / 1.965e6, dv[11] ? (double)dv[10] / dv[11] : 0.0);
   }
   S.dev_ms_total = elapsed_ms(D.ev[0], D.ev[3]);
   S.exact_hits = (int64_t)sols.size();
