@@ -46,8 +46,10 @@ enum msp_flags {
   MSP_FLAG_PROFILE = 1u << 0,      /* time the dominant kernel per launch with CUDA events */
   MSP_FLAG_FORCE_TABLE_PATH = 1u << 1, /* never take the n <= brute_force_max_n branch */
   MSP_FLAG_JOIN_GLOBAL = 1u << 2,  /* force the global-hash-table join (fallback path) */
-  MSP_FLAG_DIAG_HASH_ONLY = 1u << 3 /* diagnostic timing: global path kernels hash but do not join
+  MSP_FLAG_DIAG_HASH_ONLY = 1u << 3, /* diagnostic timing: global path kernels hash but do not join
                                        (results invalid; never set in a real solve) */
+  MSP_FLAG_WAVE_LAUNCHES = 1u << 4  /* partitioned waves as per-wave scatter + join launches instead
+                                       of the persistent pipeline (parity testing) */
 };
 
 typedef struct {

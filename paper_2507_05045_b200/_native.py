@@ -26,6 +26,7 @@ MSP_FLAG_PROFILE = 1 << 0
 MSP_FLAG_FORCE_TABLE_PATH = 1 << 1
 MSP_FLAG_JOIN_GLOBAL = 1 << 2
 MSP_FLAG_DIAG_HASH_ONLY = 1 << 3
+MSP_FLAG_WAVE_LAUNCHES = 1 << 4
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

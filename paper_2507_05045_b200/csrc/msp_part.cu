@@ -61,14 +61,15 @@ struct __align__(16) Stage {
   uint32_t cnt[kMaxNB];              // keys ranked into each entry this round
   uint2 run[kMaxNB];                 // flush: (scratch index of rank 0, staged keys to write)
   uint32_t novf, round_end, chunk, ove_spill;  // ove_spill: some rank past C has no key this round
-  uint32_t tctr, pad[3];             // tiles of the chunk handed out past the first 2 per warp
+  uint32_t tctr;                     // tiles of the chunk handed out past the first 2 per warp
+  uint32_t nstaged, pad[2];          // keys staged this round (fill trigger)
 };
 
 size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kU) * sw * 4; }
 
 __device__ __forceinline__ void stage_init(Stage &g) {
   for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
-  if (threadIdx.x == 0) { g.novf = 0; g.round_end = 0; g.ove_spill = 0; }
+  if (threadIdx.x == 0) { g.novf = 0; g.round_end = 0; g.ove_spill = 0; g.nstaged = 0; }
 }
 
 // The CTA's next work chunk (dynamic: one global atomic per chunk), broadcast through shared memory.
@@ -88,20 +89,27 @@ __device__ __noinline__ void stage_spill(Stage &g, const PartArgs &S, uint32_t e
   if (pos < __ldg(S.cap[role] + b)) __stcg(S.scratch + __ldg(S.start[role] + b) + pos, key);
   else atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
   g.ove_spill = 1u;
+  if (S.dbg) atomicAdd(S.dbg + 13, 1ull);
 }
 
 // Stage N keys per lane into their entries j (local to the chunk's unit): rank (shared atomics,
 // all issued before any dependent store), store into the entry's slots.  Keys ranked past C go to
-// the overflow list with (entry, rank): one warp-aggregated reservation per warp step; the round
-// ends once the list passes `trig`.
+// the overflow list with (entry, rank): one warp-aggregated reservation per warp step.  The round
+// ends once the list passes `trig` (few big entries... many small ones overflow early) or the stage
+// holds `ftrig` keys (few big entries all fill at once: stop before the warps in flight overflow).
 template <int N>
 __device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t lane, uint32_t C,
-                                           uint32_t trig,
+                                           uint32_t trig, uint32_t ftrig,
                                            const unsigned long long (&key)[N], const uint32_t (&j)[N],
                                            const bool (&ok)[N]) {
-  uint32_t r[N];
+  uint32_t r[N], nok = 0;
 #pragma unroll
-  for (int u = 0; u < N; ++u) r[u] = ok[u] ? atomicAdd(&g.cnt[j[u]], 1u) : 0u;
+  for (int u = 0; u < N; ++u) {
+    r[u] = ok[u] ? atomicAdd(&g.cnt[j[u]], 1u) : 0u;
+    nok += ok[u] ? 1u : 0u;
+  }
+  const uint32_t wok = __reduce_add_sync(0xffffffffu, nok);
+  if (lane == 0 && wok && atomicAdd(&g.nstaged, wok) + wok >= ftrig) *(volatile uint32_t *)&g.round_end = 1u;
   uint32_t nov = 0;
 #pragma unroll
   for (int u = 0; u < N; ++u) {
@@ -165,7 +173,7 @@ __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_
     const uint32_t e = ebase + j, role = e >= nb, b = e - role * nb;
     uint2 run = make_uint2(kDrop, 0u);
     if (res[k] + cn[k] <= __ldg(S.cap[role] + b)) run = make_uint2(__ldg(S.start[role] + b) + res[k], min(cn[k], C));
-    else atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+    else { atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u); if (S.dbg) atomicAdd(S.dbg + 12, 1ull); }
     g.run[j] = run;
   }
   if (S.dbg) {  // diagnostics: rounds, staged keys, overflow keys
@@ -197,7 +205,7 @@ __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_
   }
   __syncthreads();
   for (uint32_t j = tid; j < NB; j += kScatterThreads) g.cnt[j] = 0u;
-  if (tid == 0) { g.novf = 0u; g.round_end = 0u; g.ove_spill = 0u; }
+  if (tid == 0) { g.novf = 0u; g.round_end = 0u; g.ove_spill = 0u; g.nstaged = 0u; }
   __syncthreads();
 }
 
@@ -312,7 +320,8 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
 #pragma unroll
     for (int u = 0; u < kU; ++u) dacc ^= ok[u] ? key[u] : 0ull;
   } else {
-    stage_keys<kU>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, key, j, ok);
+    stage_keys<kU>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, nbk * C * 7 / 8,
+                   key, j, ok);
   }
 }
 
@@ -454,7 +463,7 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_rescatter(con
           key[u] = ok[u] ? __ldcs(src.keys + x) : 0ull;
           j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
         }
-        stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, key, j, ok);
+        stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, NB * C * 7 / 8, key, j, ok);
         idx += N * stride;
       }
       const bool more = __syncthreads_or(idx - lane < s1);
@@ -604,7 +613,7 @@ __device__ __forceinline__ void join_bucket(JoinSmem &T, const PartArgs &S, uint
   __syncthreads();
   if (S.dbg && tid == 0) tp1 = clock64();
   const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
-  if (T.ovf && tid == 0) atomicOr(S.batch_ovf + gid, 1u);
+  if (T.ovf && tid == 0) { atomicOr(S.batch_ovf + gid, 1u); if (S.dbg) atomicAdd(S.dbg + 14, 1ull); }
   unsigned long long hits = 0;
   for (uint32_t base = 0; base < nprobe; base += NT * U) {
     unsigned long long nx[U];  // next keys in flight while this batch is probed

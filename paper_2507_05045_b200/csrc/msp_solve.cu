@@ -641,7 +641,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   bool fill_zeroed = false;  // wave fill counters (reset by k_join after each bucket)
   // Double-buffered waves: wave k scatters into buffer k&1 on `st` while wave k-1 joins on
   // stream2; ordering is carried by events (scatter k waits for join k-2, join k for scatter k).
-  const bool overlap = !profile;
+  const bool overlap = !profile;  // (per-wave launch path and huge batches)
   auto join_streams = [&]() -> int {
     CK(cudaEventRecord(D.ev_x, D.stream2));
     CK(cudaStreamWaitEvent(st, D.ev_x, 0));
@@ -803,8 +803,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     return MSP_OK;
   };
   if (getenv("MSP_DEBUG_STATS")) {
-    CK(D.dbg.ensure(128));
-    CK(cudaMemsetAsync(D.dbg.p, 0, 128, st));
+    CK(D.dbg.ensure(3 * 128));
+    CK(cudaMemsetAsync(D.dbg.p, 0, 3 * 128, st));
     dbg_stats = D.dbg.as<unsigned long long>();
   }
   if (const char *ev = getenv("MSP_WAVE_BUCKETS")) wave_buckets = (uint32_t)std::max(1, std::min(kMaxWaveBuckets, atoi(ev)));
@@ -945,7 +945,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
       ScatterArgs sa = scatter_base(P, A);
-      if (!profile) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
+      const bool per_wave = opt->flags & MSP_FLAG_WAVE_LAUNCHES;
+      if (!per_wave) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
         std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
         std::vector<WaveDesc> wds(pw.size());
         for (size_t wi = 0; wi < pw.size(); ++wi) {
@@ -1015,8 +1016,16 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
           CK(cudaMemsetAsync(W.task_ctr, 0, 4, st));
           W.tasks = D.tasks.as<unsigned long long>();
           W.ntasks = (uint32_t)tasks.size();
+          if (profile) CK(cudaEventRecord(D.pev[0], st));
           CK(launch_waves(P.mc, W, D.num_sms, st));
           S.kernel_launches += 1;
+          if (profile) {
+            CK(cudaEventRecord(D.pev[1], st));
+            CK(cudaEventSynchronize(D.pev[1]));
+            hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
+            S.hot_launches += 1;
+            for (size_t w = s0; w < s1; ++w) S.hot_pairs += (int64_t)pw[w].pairs;
+          }
           if (periodic) {
             bool stop_now = false;
             rc = checkpoint(stop_now);
@@ -1025,7 +1034,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
           }
         }
       }
-      for (size_t wi = 0; profile && wi < pw.size(); ++wi) {
+      for (size_t wi = 0; per_wave && wi < pw.size(); ++wi) {
         const PWave &w = pw[wi];
         pa.start[0] = bkd + w.b0;
         pa.start[1] = bkd + nbt + w.b0;
@@ -1134,7 +1143,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(D.ccfirst.ensure(4 * ccf.size()));
       CK(cudaMemcpyAsync(D.ccfirst.p, ccf.data(), 4 * ccf.size(), cudaMemcpyHostToDevice, st));
       c1.batch_ovf = D.bovf.as<unsigned int>();
-      c1.dbg = dbg_stats;
+      c1.dbg = dbg_stats ? dbg_stats + 16 : nullptr;
       c1.ovf_trigger = ovf_trigger;
       c1.zero_keys = D.zkeys.as<unsigned long long>();
       if (profile) CK(cudaEventRecord(D.pev[0], st));
@@ -1218,7 +1227,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
       pa.batch_ovf = D.bovf.as<unsigned int>();
       pa.zero_keys = D.zkeys.as<unsigned long long>();
-      pa.dbg = dbg_stats;
+      pa.dbg = dbg_stats ? dbg_stats + 32 : nullptr;
       pa.ovf_trigger = ovf_trigger;
       pa.hits = D.hits.as<HitRec>();
       pa.nhits = D.nhits.as<unsigned long long>();
@@ -1463,8 +1472,13 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   CK(cudaEventRecord(D.ev[3], st));
   CK(cudaEventSynchronize(D.ev[3]));
   if (dbg_stats) {
-    unsigned long long dv[16];
-    CK(cudaMemcpy(dv, dbg_stats, 128, cudaMemcpyDeviceToHost));
+    unsigned long long dva[48];
+    CK(cudaMemcpy(dva, dbg_stats, 3 * 128, cudaMemcpyDeviceToHost));
+    for (int blk = 1; blk < 3; ++blk)
+      fprintf(stderr, "[msp dbg] %s: rounds %llu staged %llu overflow %llu spilled %llu capacity-overflow %llu\n",
+              blk == 1 ? "level-1 scatter" : "level-2/partitioned", dva[16 * blk], dva[16 * blk + 1], dva[16 * blk + 2],
+              dva[16 * blk + 13], dva[16 * blk + 12]);
+    unsigned long long *dv = dva;
     int nov = 0;
     for (uint32_t g = 0; g < P.G; ++g) nov += dropped[g];
     fprintf(stderr, "[msp dbg] scatter rounds %llu staged %llu overflow %llu; keys/round %.0f; overflowed batches %d of %u; "
@@ -1473,6 +1487,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
             dv[6] / 1.965e6);
     fprintf(stderr, "[msp dbg] join buckets %llu: build phase %.1f SM-ms, probe phase %.1f SM-ms, mean stash %.2f\n",
             dv[11], dv[8] / 1.965e6, dv[9] / 1.965e6, dv[11] ? (double)dv[10] / dv[11] : 0.0);
+    fprintf(stderr, "[msp dbg] overflow events: region capacity %llu, spilled keys %llu, join stash %llu\n",
+            dv[12], dv[13], dv[14]);
   }
   S.dev_ms_total = elapsed_ms(D.ev[0], D.ev[3]);
   S.exact_hits = (int64_t)sols.size();

@@ -156,6 +156,20 @@ def test_two_level_huge_batch_path(m, s, wave_keys):
         assert getattr(got.stats, k) == getattr(ref.stats, k), k
 
 
+@pytest.mark.parametrize("m,s", [(5, 1), (6, 4), (7, 1)])
+def test_persistent_pipeline_matches_per_wave_launches(m, s):
+    """The persistent wave pipeline (k_waves) and per-wave scatter + join launches agree exactly."""
+    inst = msb.generate_instance(m, 100, s)
+    ref = _solve_all(inst)
+    opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_WAVE_LAUNCHES)
+    rc, xb, st = _native.solve_raw(inst.a, inst.d, opts)
+    assert rc == 0, _native.last_error()
+    got = sorted((tuple(int(v) for v in r) for r in xb), key=msb.solution_encoding)
+    assert got == ref.solutions
+    for k in STAT_KEYS:
+        assert st[k] == getattr(ref.stats, k), k
+
+
 def test_global_table_join_path_matches():
     """The fallback global-hash-table join gives identical results to the partitioned join."""
     for (m, s) in ((4, 11), (5, 1), (6, 4)):
@@ -190,6 +204,19 @@ def test_m7_s1_full_against_reference():
         assert getattr(res.stats, k) == rec["stats"][k], k
     ref_rows = rec["batches"]
     assert res.stats.row1_candidate_pairs == sum(b[1] * b[2] for b in ref_rows)
+
+
+@pytest.mark.slow
+def test_m8_s1_full_against_golden():
+    """(8,70) s1 full enumeration (two-level huge-batch path + persistent waves) against the pinned
+    oracle's full run (tests/golden/make_golden_oracle.py): solutions and every counter."""
+    rec = load_golden("solve_8_100_1.json")
+    inst = inst_from(rec["instance"])
+    res = _solve_all(inst)
+    assert _strings(res.solutions) == rec["solutions"]
+    for k in STAT_KEYS:
+        assert getattr(res.stats, k) == rec["stats"][k], k
+    assert res.stats.row1_candidate_pairs == rec["row1_candidate_pairs"]
 
 
 def test_cancel_word_stops_the_solve(tmp_path):
