@@ -167,6 +167,8 @@ struct WaveDesc {
   uint32_t unit0;                      // its units in the UnitInfo array
   uint32_t b0, nb;                     // its buckets (per role) in the bucket arrays
   uint32_t njoin;                      // its join tasks (ceil(nb / kJoinGroup))
+  uint32_t kind;                       // 0: tile scatter chunks; 1: level-2 (coarse region) chunks
+  uint32_t src0;                       // kind 1: its sources in the RescatterSrc array
   uint32_t pad;
 };
 struct WavesArgs {
@@ -176,6 +178,7 @@ struct WavesArgs {
   unsigned long long *scratch[kWaveBuffers];  // wave w uses buffer w % kWaveBuffers
   uint32_t *fill[kWaveBuffers];
   const WaveDesc *waves;
+  const RescatterSrc *srcs;            // level-2 sources (kind 1 waves)
   const unsigned long long *chunks;    // scatter chunks of all waves
   const unsigned long long *tasks;     // join << 63 | wave << 32 | chunk or first bucket
   uint32_t ntasks;

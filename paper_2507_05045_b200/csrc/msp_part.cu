@@ -434,42 +434,53 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
 // ranges of ONE source (a coarse region of one role, whose keys spread uniformly over its NF fine
 // buckets); slots past the region's fill are empty.  Fine bucket = floor(frac * NF / 2^32), frac
 // = the key's position inside its coarse bucket (the low word of hi * NC).
+// One level-2 work chunk: slots [s0, s1) of ONE source (a coarse region of one role, whose keys
+// spread uniformly over its NF fine buckets), re-partitioned by the CTA.  Ends with a barrier.
+__device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, const RescatterSrc &src, uint32_t s0,
+                                                uint32_t s1) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  volatile uint32_t *round_end = &g.round_end;
+  constexpr int N = 2;
+  const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
+  uint32_t C, cmagic;
+  stage_geometry(NB, C, cmagic);
+  uint32_t idx = s0 + warp * 32 + lane;
+  const uint32_t stride = kScatterThreads;
+  while (true) {
+    while (idx - lane < s1 && !*round_end) {
+      unsigned long long key[N];
+      uint32_t j[N];
+      bool ok[N];
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        const uint32_t x = idx + u * stride;
+        ok[u] = x < s1;
+        key[u] = ok[u] ? __ldcs(src.keys + x) : 0ull;
+        ok[u] = ok[u] && key[u] != 0ull;  // run pads
+        j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
+      }
+      stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, NB * C * 7 / 8, key, j, ok);
+      idx += N * stride;
+    }
+    const bool more = __syncthreads_or(idx - lane < s1);
+    flush_round(g, S, ebase, NB, C, cmagic);
+    if (!more) break;
+  }
+}
+
+// Level 2 of the huge-batch path as its own launch (MSP_FLAG_WAVE_LAUNCHES): stream already-hashed
+// keys back from coarse bucket regions (HBM) and re-partition them into fine buckets (L2 scratch)
+// for k_join; chunks from a global counter.
 __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_rescatter(const RescatterArgs R, const PartArgs S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage &g = *reinterpret_cast<Stage *>(smem_raw);
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   stage_init(g);
   __syncthreads();
-  volatile uint32_t *round_end = &g.round_end;
-  constexpr int N = 2;
   for (uint32_t c = next_chunk(g, R.chunk_ctr); c < R.nchunks; c = next_chunk(g, R.chunk_ctr)) {
     const unsigned long long cw = __ldg(R.chunks + c);
     const RescatterSrc &src = R.src[(uint32_t)(cw >> 48)];
     const uint32_t s0 = (uint32_t)cw, s1 = min(s0 + (uint32_t)((cw >> 32) & 0xFFFFu) * 32u, min(*src.fill, src.cap));
-    const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
-    uint32_t C, cmagic;
-    stage_geometry(NB, C, cmagic);
-    uint32_t idx = s0 + warp * 32 + lane;
-    const uint32_t stride = kScatterThreads;
-    while (true) {
-      while (idx - lane < s1 && !*round_end) {
-        unsigned long long key[N];
-        uint32_t j[N];
-        bool ok[N];
-#pragma unroll
-        for (int u = 0; u < N; ++u) {
-          const uint32_t x = idx + u * stride;
-          ok[u] = x < s1;
-          key[u] = ok[u] ? __ldcs(src.keys + x) : 0ull;
-          j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
-        }
-        stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, NB * C * 7 / 8, key, j, ok);
-        idx += N * stride;
-      }
-      const bool more = __syncthreads_or(idx - lane < s1);
-      flush_round(g, S, ebase, NB, C, cmagic);
-      if (!more) break;
-    }
+    rescatter_chunk(g, S, src, s0, s1);
   }
 }
 
@@ -739,14 +750,21 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
       __syncthreads();
       if (tid == 0) atomicAdd(W.join_done + w, 1u);
       if (tid == 0 && W.pa.dbg) { const long long now = clock64(); atomicAdd(W.pa.dbg + 5, (unsigned long long)(now - t_prev)); t_prev = now; }
-    } else {  // scatter chunk idx of the wave
-      ScatterArgs A = W.sc;
-      A.tiles = W.sc.tiles + wd.tile0;
+    } else {  // scatter chunk idx of the wave (tiles, or a level-2 slot range of a coarse region)
       stage_init(g);
       __syncthreads();
       const unsigned long long cw = __ldg(W.chunks + wd.chunk0 + idx);
-      const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
-      scatter_chunk<MC>(g, ybuf, A, S, dg, W.sc.units[wd.unit0 + unit], t0, n, dacc);
+      if (wd.kind) {
+        const RescatterSrc &src = W.srcs[wd.src0 + (uint32_t)(cw >> 48)];
+        const uint32_t s0 = (uint32_t)cw;
+        const uint32_t s1 = min(s0 + (uint32_t)((cw >> 32) & 0xFFFFu) * 32u, min(*src.fill, src.cap));
+        rescatter_chunk(g, S, src, s0, s1);
+      } else {
+        ScatterArgs A = W.sc;
+        A.tiles = W.sc.tiles + wd.tile0;
+        const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
+        scatter_chunk<MC>(g, ybuf, A, S, dg, W.sc.units[wd.unit0 + unit], t0, n, dacc);
+      }
       __threadfence();
       __syncthreads();
       if (tid == 0) atomicAdd(W.scat_done + w, 1u);

@@ -55,10 +55,11 @@ struct DBuf {
   size_t cap = 0;
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap) return cudaSuccess;
+    const size_t grow = cap < (256ull << 20) ? 2 * cap : 0;  // geometric for small buffers: few regrowths
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
-    size_t c = std::max<size_t>(bytes + bytes / 4, 256);
+    size_t c = std::max<size_t>(std::max(bytes + bytes / 4, grow), 256);
     cudaError_t e = cudaMalloc(&p, c);
     if (e == cudaSuccess) cap = c;
     return e;
@@ -88,9 +89,16 @@ struct Device {
   DBuf scratch2, fill2, scratch3, fill3;
   DBuf tdesc, gstb, gsu, uinfo, chunks, cchunks, l2chunks, cctr, cfirst, ccfirst, tchunks, wdesc, wctr, tasks;
   uint32_t cctr_next = 0;  // next unused chunk counter in cctr (zeroed per solve)
+  // pinned staging ring for the per-launch metadata uploads: a cudaMemcpyAsync from pageable memory
+  // waits for the stream to drain first, which would idle the GPU between launches
+  unsigned char *ring = nullptr;
+  size_t ring_cap = 0, ring_off = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
+    if (ring) cudaFreeHost(ring);
+    ring = nullptr;
+    ring_cap = ring_off = 0;
     DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err, &nitem, &ibase, &items, &ictr,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
@@ -784,6 +792,28 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     return MSP_OK;
   };
   const bool periodic = deadline || opt->mode == MSP_MODE_FIRST || opt->cancel;
+  // asynchronous metadata upload through the pinned ring (wraps after a stream sync)
+  auto upload = [&](void *dst, const void *src, size_t bytes) -> int {
+    if (!bytes) return MSP_OK;
+    constexpr size_t kRing = 64ull << 20;
+    if (bytes > kRing) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      return MSP_OK;
+    }
+    if (!D.ring) {
+      CK(cudaMallocHost(&D.ring, kRing));
+      D.ring_cap = kRing;
+      D.ring_off = 0;
+    }
+    if (D.ring_off + bytes > D.ring_cap) {  // every earlier copy out of the ring is done after this
+      CK(cudaStreamSynchronize(st));
+      D.ring_off = 0;
+    }
+    memcpy(D.ring + D.ring_off, src, bytes);
+    CK(cudaMemcpyAsync(dst, D.ring + D.ring_off, bytes, cudaMemcpyHostToDevice, st));
+    D.ring_off = (D.ring_off + bytes + 255) & ~(size_t)255;
+    return MSP_OK;
+  };
   // buckets per role of one partitioned wave (scatter entries = 2x): fewer entries give longer
   // runs per round; MSP_WAVE_BUCKETS overrides for tuning
   uint32_t wave_buckets = kMaxWaveBuckets;
@@ -808,6 +838,74 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     dbg_stats = D.dbg.as<unsigned long long>();
   }
   if (const char *ev = getenv("MSP_WAVE_BUCKETS")) wave_buckets = (uint32_t)std::max(1, std::min(kMaxWaveBuckets, atoi(ev)));
+
+  // Launches of the persistent wave pipeline (msp_part.cu k_waves) over `wds` (descriptors and
+  // chunks already on the device in W): tasks S(0) S(1) J(0) S(2) J(1) ... J(last), one launch per
+  // segment of waves (16 when checkpoints are due, else all).  `pairs` per wave for profiling.
+  auto run_pipeline = [&](WavesArgs &W, const std::vector<WaveDesc> &wds, const std::vector<uint64_t> &pairs,
+                          bool timed) -> int {
+    CK(D.wctr.ensure(4 * (1 + 2 * wds.size())));
+    CK(cudaMemsetAsync(D.wctr.p, 0, 4 * (1 + 2 * wds.size()), st));
+    W.task_ctr = D.wctr.as<unsigned int>();
+    W.scat_done = W.task_ctr + 1;
+    W.join_done = W.scat_done + wds.size();
+    const size_t seg = periodic ? 16 : wds.size();
+    for (size_t s0 = 0; s0 < wds.size() && !stopped; s0 += seg) {
+      const size_t s1 = std::min(wds.size(), s0 + seg);
+      std::vector<unsigned long long> tasks;  // S(s0) S(s0+1) J(s0) S(s0+2) J(s0+1) ... J(s1-1)
+      auto push_join = [&](size_t w) {
+        for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks.push_back((1ull << 63) | ((unsigned long long)w << 32) | b);
+      };
+      for (size_t w = s0; w < s1; ++w) {
+        for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks.push_back(((unsigned long long)w << 32) | c);
+        if (w > s0) push_join(w - 1);
+      }
+      push_join(s1 - 1);
+      CK(D.tasks.ensure(8 * tasks.size()));
+      if (int ru_ = upload(D.tasks.p, tasks.data(), 8 * tasks.size())) return ru_;
+      CK(cudaMemsetAsync(W.task_ctr, 0, 4, st));
+      W.tasks = D.tasks.as<unsigned long long>();
+      W.ntasks = (uint32_t)tasks.size();
+      if (profile && timed) CK(cudaEventRecord(D.pev[0], st));
+      CK(launch_waves(P.mc, W, D.num_sms, st));
+      S.kernel_launches += 1;
+      if (profile && timed) {
+        CK(cudaEventRecord(D.pev[1], st));
+        CK(cudaEventSynchronize(D.pev[1]));
+        hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
+        S.hot_launches += 1;
+        for (size_t w = s0; w < s1; ++w) S.hot_pairs += (int64_t)pairs[w];
+      }
+      if (periodic) {
+        bool stop_now = false;
+        const int r1 = checkpoint(stop_now);
+        if (r1) return r1;
+        if (stop_now) stopped = true;
+      }
+    }
+    return MSP_OK;
+  };
+  // three scratch buffers (+ fill counters, zeroed per solve) for the pipeline
+  bool fill3_zeroed = false;
+  auto ensure_pipeline_buffers = [&](uint64_t scratch_keys) -> int {
+    if (int r1 = ensure_wave_buffers(scratch_keys)) return r1;
+    CK(D.scratch3.ensure(8 * (scratch_keys + kSinkSlots)));
+    void *f3 = D.fill3.p;
+    CK(D.fill3.ensure(4 * 2 * kMaxWaveBuckets));
+    if (f3 != D.fill3.p || !fill3_zeroed) {
+      CK(cudaMemsetAsync(D.fill3.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+      fill3_zeroed = true;
+    }
+    return MSP_OK;
+  };
+  auto pipeline_base = [&](WavesArgs &W) {
+    W.scratch[0] = D.scratch.as<unsigned long long>();
+    W.scratch[1] = D.scratch2.as<unsigned long long>();
+    W.scratch[2] = D.scratch3.as<unsigned long long>();
+    W.fill[0] = D.fill.as<uint32_t>();
+    W.fill[1] = D.fill2.as<uint32_t>();
+    W.fill[2] = D.fill3.as<uint32_t>();
+  };
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
   std::vector<uint32_t> part_b, huge_b, global_b;
@@ -888,12 +986,12 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       for (const PWave &w : pw)
         for (size_t i = w.u0; i < w.u1; ++i) uinfo[i] = make_info(units[i], (uint32_t)w.nb);
       CK(D.uinfo.ensure(sizeof(UnitInfo) * uinfo.size()));
-      CK(cudaMemcpyAsync(D.uinfo.p, uinfo.data(), sizeof(UnitInfo) * uinfo.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.uinfo.p, uinfo.data(), sizeof(UnitInfo) * uinfo.size())) return ru_;
       CK(D.bk.ensure(4 * 5 * nbt));
       std::vector<uint32_t> bkimg;
       bkimg.reserve(5 * nbt);
       for (auto *v : {&bstart[0], &bstart[1], &bcap[0], &bcap[1], &bgid}) bkimg.insert(bkimg.end(), v->begin(), v->end());
-      CK(cudaMemcpyAsync(D.bk.p, bkimg.data(), 4 * bkimg.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.bk.p, bkimg.data(), 4 * bkimg.size())) return ru_;
       // per wave: each CTA's equal share of the wave's tiles, cut at unit boundaries
       const uint32_t nct = (uint32_t)D.num_sms * kScatterCtasHost;
       std::vector<unsigned long long> chimg;
@@ -913,15 +1011,15 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         cfirst.insert(cfirst.end(), f.begin(), f.end());
       }
       CK(D.chunks.ensure(8 * std::max<size_t>(1, chimg.size())));
-      CK(cudaMemcpyAsync(D.chunks.p, chimg.data(), 8 * chimg.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.chunks.p, chimg.data(), 8 * chimg.size())) return ru_;
       CK(D.cfirst.ensure(4 * std::max<size_t>(1, cfirst.size())));
-      CK(cudaMemcpyAsync(D.cfirst.p, cfirst.data(), 4 * cfirst.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.cfirst.p, cfirst.data(), 4 * cfirst.size())) return ru_;
       // K3b: every partitioned batch side's warp tiles, one launch
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(all_tiles, 1)));
       CK(D.gstb.ensure(8 * gs_tb.size()));
       CK(D.gsu.ensure(4 * gs_unit.size()));
-      CK(cudaMemcpyAsync(D.gstb.p, gs_tb.data(), 8 * gs_tb.size(), cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(D.gsu.p, gs_unit.data(), 4 * gs_unit.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.gstb.p, gs_tb.data(), 8 * gs_tb.size())) return ru_;
+      if (int ru_ = upload(D.gsu.p, gs_unit.data(), 4 * gs_unit.size())) return ru_;
       TileGenArgs tg{};
       tg.rects = P.base.rects;
       tg.rect_lo = 0;
@@ -970,69 +1068,24 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
           wd.njoin = (uint32_t)((w.nb + kJoinGroup - 1) / kJoinGroup);
         }
         CK(D.tchunks.ensure(8 * std::max<size_t>(1, tch.size())));
-        CK(cudaMemcpyAsync(D.tchunks.p, tch.data(), 8 * tch.size(), cudaMemcpyHostToDevice, st));
+        if (int ru_ = upload(D.tchunks.p, tch.data(), 8 * tch.size())) return ru_;
         CK(D.wdesc.ensure(sizeof(WaveDesc) * wds.size()));
-        CK(cudaMemcpyAsync(D.wdesc.p, wds.data(), sizeof(WaveDesc) * wds.size(), cudaMemcpyHostToDevice, st));
-        CK(D.wctr.ensure(4 * (1 + 2 * pw.size())));
-        CK(cudaMemsetAsync(D.wctr.p, 0, 4 * (1 + 2 * pw.size()), st));
+        if (int ru_ = upload(D.wdesc.p, wds.data(), sizeof(WaveDesc) * wds.size())) return ru_;
+        rc = ensure_pipeline_buffers(max_scratch);
+        if (rc) return rc;
         WavesArgs W{};
         W.sc = sa;
         W.sc.tiles = D.tdesc.as<TileDesc>();
         W.sc.units = D.uinfo.as<UnitInfo>();
         W.pa = pa;
         W.bstart0 = bkd; W.bstart1 = bkd + nbt; W.bcap0 = bkd + 2 * nbt; W.bcap1 = bkd + 3 * nbt; W.bgid = bkd + 4 * nbt;
-        {  // a third scratch buffer (the per-wave launch path uses two)
-          uint64_t mx = 0;
-          for (const PWave &w : pw) mx = std::max(mx, w.scratch);
-          CK(D.scratch3.ensure(8 * (mx + kSinkSlots)));
-          CK(D.fill3.ensure(4 * 2 * kMaxWaveBuckets));
-          CK(cudaMemsetAsync(D.fill3.p, 0, 4 * 2 * kMaxWaveBuckets, st));
-        }
-        W.scratch[0] = D.scratch.as<unsigned long long>();
-        W.scratch[1] = D.scratch2.as<unsigned long long>();
-        W.scratch[2] = D.scratch3.as<unsigned long long>();
-        W.fill[0] = D.fill.as<uint32_t>();
-        W.fill[1] = D.fill2.as<uint32_t>();
-        W.fill[2] = D.fill3.as<uint32_t>();
+        pipeline_base(W);
         W.waves = D.wdesc.as<WaveDesc>();
         W.chunks = D.tchunks.as<unsigned long long>();
-        W.task_ctr = D.wctr.as<unsigned int>();
-        W.scat_done = W.task_ctr + 1;
-        W.join_done = W.scat_done + pw.size();
-        const size_t seg = periodic ? 16 : pw.size();
-        for (size_t s0 = 0; s0 < pw.size() && !stopped; s0 += seg) {
-          const size_t s1 = std::min(pw.size(), s0 + seg);
-          std::vector<unsigned long long> tasks;  // S(s0) S(s0+1) J(s0) S(s0+2) J(s0+1) ... J(s1-1)
-          auto push_join = [&](size_t w) {
-            for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks.push_back((1ull << 63) | ((unsigned long long)w << 32) | b);
-          };
-          for (size_t w = s0; w < s1; ++w) {
-            for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks.push_back(((unsigned long long)w << 32) | c);
-            if (w > s0) push_join(w - 1);
-          }
-          push_join(s1 - 1);
-          CK(D.tasks.ensure(8 * tasks.size()));
-          CK(cudaMemcpyAsync(D.tasks.p, tasks.data(), 8 * tasks.size(), cudaMemcpyHostToDevice, st));
-          CK(cudaMemsetAsync(W.task_ctr, 0, 4, st));
-          W.tasks = D.tasks.as<unsigned long long>();
-          W.ntasks = (uint32_t)tasks.size();
-          if (profile) CK(cudaEventRecord(D.pev[0], st));
-          CK(launch_waves(P.mc, W, D.num_sms, st));
-          S.kernel_launches += 1;
-          if (profile) {
-            CK(cudaEventRecord(D.pev[1], st));
-            CK(cudaEventSynchronize(D.pev[1]));
-            hot_ms += elapsed_ms(D.pev[0], D.pev[1]);
-            S.hot_launches += 1;
-            for (size_t w = s0; w < s1; ++w) S.hot_pairs += (int64_t)pw[w].pairs;
-          }
-          if (periodic) {
-            bool stop_now = false;
-            rc = checkpoint(stop_now);
-            if (rc) return rc;
-            if (stop_now) stopped = true;
-          }
-        }
+        std::vector<uint64_t> wpairs;
+        for (const PWave &w : pw) wpairs.push_back(w.pairs);
+        rc = run_pipeline(W, wds, wpairs, true);
+        if (rc) return rc;
       }
       for (size_t wi = 0; per_wave && wi < pw.size(); ++wi) {
         const PWave &w = pw[wi];
@@ -1079,6 +1132,24 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   if (!stopped && !huge_b.empty()) {
     constexpr uint64_t kCoarseTarget = 2ull << 20;  // build keys per coarse bucket
     CK(D.cfill.ensure(4 * 2 * kMaxWaveBuckets));
+    {  // size the big per-batch buffers once for the largest batch (a regrowth stalls the stream)
+      uint64_t mcb = 0, mcp = 0, mt = 0;
+      for (uint32_t g : huge_b) {
+        const int bs = P.nr[g] <= P.nl[g] ? 1 : 0;
+        const uint64_t nb = bs ? P.nr[g] : P.nl[g], np = bs ? P.nl[g] : P.nr[g];
+        uint32_t cbits = pow2ceil((nb + kCoarseTarget - 1) / kCoarseTarget);
+        cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, 10));
+        const double mb = (double)nb / (1u << cbits), mp = (double)np / (1u << cbits);
+        mcb = std::max<uint64_t>(mcb, (uint64_t)even_up(mb + 7.0 * std::sqrt(mb) + 16) << cbits);
+        mcp = std::max<uint64_t>(mcp, (uint64_t)even_up(mp + 7.0 * std::sqrt(mp) + 16) << cbits);
+        mt = std::max<uint64_t>(mt, std::max(P.tiles[2 * (size_t)g], P.tiles[2 * (size_t)g + 1]));
+      }
+      CK(D.cscratch[0].ensure(8 * (mcb + kSinkSlots)));
+      CK(D.cscratch[1].ensure(8 * (mcp + kSinkSlots)));
+      CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, mt)));
+      rc = ensure_pipeline_buffers(2 * key_budget + 4 * kMaxWaveBuckets * 64ull);
+      if (rc) return rc;
+    }
     for (size_t hi_ = 0; hi_ < huge_b.size() && !stopped; ++hi_) {
       rc = join_streams();  // the previous batch's joins still read the wave buffers
       if (rc) return rc;
@@ -1106,7 +1177,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(D.cscratch[0].ensure(8 * (cb * NC + kSinkSlots)));
       CK(D.cscratch[1].ensure(8 * (cp * NC + kSinkSlots)));
       CK(D.cbk.ensure(4 * cbk.size()));
-      CK(cudaMemcpyAsync(D.cbk.p, cbk.data(), 4 * cbk.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.cbk.p, cbk.data(), 4 * cbk.size())) return ru_;
       CK(cudaMemsetAsync(D.cfill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
       UnitDesc lu[2];
       uint64_t ltiles[2];
@@ -1121,7 +1192,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       }
       UnitInfo li[2] = {make_info(lu[0], NC), make_info(lu[1], NC)};
       CK(D.hunits.ensure(sizeof(UnitInfo) * 2));
-      CK(cudaMemcpyAsync(D.hunits.p, li, sizeof(UnitInfo) * 2, cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.hunits.p, li, sizeof(UnitInfo) * 2)) return ru_;
       const uint32_t *cbkd = D.cbk.as<uint32_t>();
       PartArgs c1{};
       c1.gid = cbkd + 4 * NC;
@@ -1139,9 +1210,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         ccf.insert(ccf.end(), f.begin(), f.end());
       }
       CK(D.cchunks.ensure(8 * std::max<size_t>(1, cch.size())));
-      CK(cudaMemcpyAsync(D.cchunks.p, cch.data(), 8 * cch.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.cchunks.p, cch.data(), 8 * cch.size())) return ru_;
       CK(D.ccfirst.ensure(4 * ccf.size()));
-      CK(cudaMemcpyAsync(D.ccfirst.p, ccf.data(), 4 * ccf.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.ccfirst.p, ccf.data(), 4 * ccf.size())) return ru_;
       c1.batch_ovf = D.bovf.as<unsigned int>();
       c1.dbg = dbg_stats ? dbg_stats + 16 : nullptr;
       c1.ovf_trigger = ovf_trigger;
@@ -1218,8 +1289,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       if (rc) return rc;
       CK(D.l2bk.ensure(4 * fimg.size()));
       CK(D.l2src.ensure(sizeof(RescatterSrc) * srcs.size()));
-      CK(cudaMemcpyAsync(D.l2bk.p, fimg.data(), 4 * fimg.size(), cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(D.l2src.p, srcs.data(), sizeof(RescatterSrc) * srcs.size(), cudaMemcpyHostToDevice, st));
+      if (int ru_ = upload(D.l2bk.p, fimg.data(), 4 * fimg.size())) return ru_;
+      if (int ru_ = upload(D.l2src.p, srcs.data(), sizeof(RescatterSrc) * srcs.size())) return ru_;
       const uint32_t *fb = D.l2bk.as<uint32_t>();
       PartArgs pa{};
       pa.scratch = D.scratch.as<unsigned long long>();
@@ -1247,8 +1318,37 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       }
       l2off.push_back(l2ch.size());
       CK(D.l2chunks.ensure(8 * std::max<size_t>(1, l2ch.size())));
-      CK(cudaMemcpyAsync(D.l2chunks.p, l2ch.data(), 8 * l2ch.size(), cudaMemcpyHostToDevice, st));
-      for (size_t wi = 0; wi < lw.size(); ++wi) {
+      if (int ru_ = upload(D.l2chunks.p, l2ch.data(), 8 * l2ch.size())) return ru_;
+      if (!(opt->flags & MSP_FLAG_WAVE_LAUNCHES)) {  // level-2 waves through the persistent pipeline
+        rc = join_streams();  // (the previous batch's joins may still read the wave buffers)
+        if (rc) return rc;
+        rc = ensure_pipeline_buffers(max_scr);
+        if (rc) return rc;
+        std::vector<WaveDesc> wds(lw.size());
+        for (size_t wi = 0; wi < lw.size(); ++wi) {
+          WaveDesc &wd = wds[wi];
+          wd.kind = 1;
+          wd.chunk0 = (uint32_t)l2off[wi];
+          wd.nchunks = (uint32_t)(l2off[wi + 1] - l2off[wi]);
+          wd.src0 = (uint32_t)lw[wi].s0;
+          wd.b0 = (uint32_t)lw[wi].b0;
+          wd.nb = (uint32_t)lw[wi].nb;
+          wd.njoin = (uint32_t)((lw[wi].nb + kJoinGroup - 1) / kJoinGroup);
+        }
+        CK(D.wdesc.ensure(sizeof(WaveDesc) * wds.size()));
+        if (int ru_ = upload(D.wdesc.p, wds.data(), sizeof(WaveDesc) * wds.size())) return ru_;
+        WavesArgs W{};
+        W.sc = scatter_base(P, A);
+        W.pa = pa;
+        W.bstart0 = fb; W.bstart1 = fb + nft; W.bcap0 = fb + 2 * nft; W.bcap1 = fb + 3 * nft; W.bgid = fb + 4 * nft;
+        pipeline_base(W);
+        W.waves = D.wdesc.as<WaveDesc>();
+        W.srcs = D.l2src.as<RescatterSrc>();
+        W.chunks = D.l2chunks.as<unsigned long long>();
+        rc = run_pipeline(W, wds, std::vector<uint64_t>(lw.size(), 0), false);  // (timed per batch below)
+        if (rc) return rc;
+      }
+      for (size_t wi = 0; (opt->flags & MSP_FLAG_WAVE_LAUNCHES) && wi < lw.size(); ++wi) {
         const L2Wave &w = lw[wi];
 
         pa.start[0] = fb + w.b0;
