@@ -274,7 +274,7 @@ def main() -> int:
     h2d = 8 * inst.m * inst.n + 8 * inst.m
     d2h = inst.n * max(1, len(ref_sols)) + 256  # solution bit vectors + stats record
 
-    # ---------------- dominant kernel: per-launch CUDA-event timing of the join waves (profile pass)
+    # ---------------- dominant kernel: CUDA-event timing of the persistent wave pipeline (profile pass)
     _, pst = step(flags=_native.MSP_FLAG_PROFILE)
     hot_ms = float(pst.get("dev_ms_hot", 0.0))
     hot_launches = int(pst.get("hot_launches", 0))
@@ -295,7 +295,8 @@ def main() -> int:
     achieved_hbm = 8.0 * hot_pairs / (hot_ms * 1e-3) / 1e9 if hot_ms else None
     roofline = {
         "bound": "int32",
-        "kernel": "k_scatter + k_join (one partitioned join wave = scatter launch + join launch)",
+        "kernel": "k_waves (persistent pipeline: scatter chunks + bucket joins of every partitioned wave, "
+                  "one launch per solve)",
         "achieved": achieved_int, "peak": int_peak / 1e9 if int_peak > 0 else None,
         "unit": "Gop/s", "frac": (achieved_int / (int_peak / 1e9)) if (achieved_int and int_peak > 0) else None,
         "peak_source": "measured on this GPU: msp_int32_peak (FNV fold instruction mix)",
@@ -304,11 +305,11 @@ def main() -> int:
                        "pairs": hot_pairs},
         "traffic": None,
     }
-    try:  # DRAM bytes per wave from the committed ncu --set full capture (profiles/README.md)
-        with open(os.path.join(HERE, "profiles", "r1b_kernels.json")) as fh:
+    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/README.md)
+        with open(os.path.join(HERE, "profiles", "r1d_kernels.json")) as fh:
             tr = json.load(fh)["traffic"]
-        roofline["traffic"] = {"dram_bytes_per_wave": tr["wave_dram_bytes"],
-                               "algorithmic_bytes_per_wave": tr["algorithmic_bytes_per_wave"],
+        roofline["traffic"] = {"dram_bytes_per_launch": tr["launch_dram_bytes"],
+                               "algorithmic_bytes_per_launch": tr["algorithmic_bytes_per_launch"],
                                "source": tr["source"]}
     except (OSError, KeyError, ValueError):
         pass

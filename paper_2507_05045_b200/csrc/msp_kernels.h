@@ -160,7 +160,8 @@ cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 // Persistent pipeline of partitioned waves (msp_part.cu k_waves): scatter chunks of wave w + 1 and
 // join bucket groups of wave w from one task queue, one CTA per SM.
 constexpr uint32_t kJoinGroup = 6;     // buckets per join task
-constexpr uint32_t kWaveBuffers = 3;   // scratch buffers of the pipeline
+constexpr uint32_t kWaveBuffers = 4;   // scratch buffers of the pipeline
+constexpr uint32_t kWaveLookahead = 2; // task order S(w + 2) J(w): joins trail scatters by 2 waves
 struct WaveDesc {
   uint32_t tile0;                      // first tile of the wave in the tile array
   uint32_t chunk0, nchunks;            // its scatter chunks (wave-relative tiles) in the chunk array

@@ -440,12 +440,18 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
                                                 uint32_t s1) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   volatile uint32_t *round_end = &g.round_end;
-  constexpr int N = 2;
+  constexpr int N = 8;  // keys per lane per step; the next step's keys are in flight meanwhile (HBM)
   const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
   uint32_t C, cmagic;
   stage_geometry(NB, C, cmagic);
-  uint32_t idx = s0 + warp * 32 + lane;
   const uint32_t stride = kScatterThreads;
+  uint32_t idx = s0 + warp * 32 + lane;
+  unsigned long long nxt[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const uint32_t x = idx + u * stride;
+    nxt[u] = x < s1 ? __ldcs(src.keys + x) : 0ull;
+  }
   while (true) {
     while (idx - lane < s1 && !*round_end) {
       unsigned long long key[N];
@@ -453,10 +459,13 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
       bool ok[N];
 #pragma unroll
       for (int u = 0; u < N; ++u) {
-        const uint32_t x = idx + u * stride;
-        ok[u] = x < s1;
-        key[u] = ok[u] ? __ldcs(src.keys + x) : 0ull;
-        ok[u] = ok[u] && key[u] != 0ull;  // run pads
+        key[u] = nxt[u];
+        const uint32_t x = idx + (N + u) * stride;
+        nxt[u] = x < s1 ? __ldcs(src.keys + x) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < N; ++u) {
+        ok[u] = key[u] != 0ull;  // past the fill, or a run pad
         j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
       }
       stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, NB * C * 7 / 8, key, j, ok);
@@ -680,10 +689,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
 // ---------------------------------------------------------------- persistent wave pipeline
 
 // All partitioned waves of a solve in ONE launch, one CTA per SM: CTAs pull tasks in queue order
-// S(0) S(1) J(0) S(2) J(1) ... where S(w) are wave w's scatter chunks and J(w) its join bucket
-// groups.  J(w) waits for every chunk of S(w) (scat_done[w]); S(w) waits for J(w-3) (join_done),
-// the last reader of its scratch buffer w % 3 (three buffers, so S(w) never waits on the joins
-// handed out just before it).  Every wait points at tasks earlier in the queue,
+// S(0) S(1) S(2) J(0) S(3) J(1) ... where S(w) are wave w's scatter chunks and J(w) its join bucket
+// groups, ordered S(w + 2) before J(w).  J(w) waits for every chunk of S(w) (scat_done[w]); S(w)
+// waits for J(w-4) (join_done), the last reader of its scratch buffer w % 4 (four buffers, so S(w)
+// never waits on the joins handed out just before it).  Every wait points at tasks earlier in the queue,
 // already held by resident CTAs, so the pipeline cannot deadlock; joins of wave w run on some SMs
 // while others scatter wave w + 1, and no wave ends in a launch tail.
 template <int MC>

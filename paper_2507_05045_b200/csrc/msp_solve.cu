@@ -86,7 +86,7 @@ struct Device {
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
-  DBuf scratch2, fill2, scratch3, fill3;
+  DBuf scratch2, fill2, scratch3, fill3, scratch4, fill4;
   DBuf tdesc, gstb, gsu, uinfo, chunks, cchunks, l2chunks, cctr, cfirst, ccfirst, tchunks, wdesc, wctr, tasks;
   uint32_t cctr_next = 0;  // next unused chunk counter in cctr (zeroed per solve)
   // pinned staging ring for the per-launch metadata uploads: a cudaMemcpyAsync from pageable memory
@@ -103,7 +103,7 @@ struct Device {
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
                    &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
-                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &scratch3, &fill3, &tdesc, &gstb, &gsu, &uinfo,
+                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &scratch3, &fill3, &scratch4, &fill4, &tdesc, &gstb, &gsu, &uinfo,
                    &chunks, &cchunks, &l2chunks, &cctr, &cfirst, &ccfirst, &tchunks, &wdesc, &wctr, &tasks};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
@@ -852,15 +852,15 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     const size_t seg = periodic ? 16 : wds.size();
     for (size_t s0 = 0; s0 < wds.size() && !stopped; s0 += seg) {
       const size_t s1 = std::min(wds.size(), s0 + seg);
-      std::vector<unsigned long long> tasks;  // S(s0) S(s0+1) J(s0) S(s0+2) J(s0+1) ... J(s1-1)
+      std::vector<unsigned long long> tasks;  // S(s0) S(s0+1) S(s0+2) J(s0) S(s0+3) J(s0+1) ... J(s1-1)
       auto push_join = [&](size_t w) {
         for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks.push_back((1ull << 63) | ((unsigned long long)w << 32) | b);
       };
       for (size_t w = s0; w < s1; ++w) {
         for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks.push_back(((unsigned long long)w << 32) | c);
-        if (w > s0) push_join(w - 1);
+        if (w >= s0 + kWaveLookahead) push_join(w - kWaveLookahead);
       }
-      push_join(s1 - 1);
+      for (size_t w = s1 > s0 + kWaveLookahead ? s1 - kWaveLookahead : s0; w < s1; ++w) push_join(w);
       CK(D.tasks.ensure(8 * tasks.size()));
       if (int ru_ = upload(D.tasks.p, tasks.data(), 8 * tasks.size())) return ru_;
       CK(cudaMemsetAsync(W.task_ctr, 0, 4, st));
@@ -885,15 +885,18 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
     return MSP_OK;
   };
-  // three scratch buffers (+ fill counters, zeroed per solve) for the pipeline
+  // kWaveBuffers scratch buffers (+ fill counters, zeroed per solve) for the pipeline
   bool fill3_zeroed = false;
   auto ensure_pipeline_buffers = [&](uint64_t scratch_keys) -> int {
     if (int r1 = ensure_wave_buffers(scratch_keys)) return r1;
+    void *f3 = D.fill3.p, *f4 = D.fill4.p;
     CK(D.scratch3.ensure(8 * (scratch_keys + kSinkSlots)));
-    void *f3 = D.fill3.p;
+    CK(D.scratch4.ensure(8 * (scratch_keys + kSinkSlots)));
     CK(D.fill3.ensure(4 * 2 * kMaxWaveBuckets));
-    if (f3 != D.fill3.p || !fill3_zeroed) {
+    CK(D.fill4.ensure(4 * 2 * kMaxWaveBuckets));
+    if (f3 != D.fill3.p || f4 != D.fill4.p || !fill3_zeroed) {
       CK(cudaMemsetAsync(D.fill3.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+      CK(cudaMemsetAsync(D.fill4.p, 0, 4 * 2 * kMaxWaveBuckets, st));
       fill3_zeroed = true;
     }
     return MSP_OK;
@@ -902,9 +905,11 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     W.scratch[0] = D.scratch.as<unsigned long long>();
     W.scratch[1] = D.scratch2.as<unsigned long long>();
     W.scratch[2] = D.scratch3.as<unsigned long long>();
+    W.scratch[3] = D.scratch4.as<unsigned long long>();
     W.fill[0] = D.fill.as<uint32_t>();
     W.fill[1] = D.fill2.as<uint32_t>();
     W.fill[2] = D.fill3.as<uint32_t>();
+    W.fill[3] = D.fill4.as<uint32_t>();
   };
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
@@ -1575,9 +1580,11 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     unsigned long long dva[48];
     CK(cudaMemcpy(dva, dbg_stats, 3 * 128, cudaMemcpyDeviceToHost));
     for (int blk = 1; blk < 3; ++blk)
-      fprintf(stderr, "[msp dbg] %s: rounds %llu staged %llu overflow %llu spilled %llu capacity-overflow %llu\n",
-              blk == 1 ? "level-1 scatter" : "level-2/partitioned", dva[16 * blk], dva[16 * blk + 1], dva[16 * blk + 2],
-              dva[16 * blk + 13], dva[16 * blk + 12]);
+      fprintf(stderr, "[msp dbg] %s: rounds %llu staged %llu overflow %llu spilled %llu capacity-overflow %llu; "
+              "SM-ms (pipeline) scatter %.1f join %.1f wait %.1f, join phases %.1f / %.1f\n",
+              blk == 1 ? "level-1 scatter" : "level-2", dva[16 * blk], dva[16 * blk + 1], dva[16 * blk + 2],
+              dva[16 * blk + 13], dva[16 * blk + 12], dva[16 * blk + 4] / 1.965e6, dva[16 * blk + 5] / 1.965e6,
+              dva[16 * blk + 6] / 1.965e6, dva[16 * blk + 8] / 1.965e6, dva[16 * blk + 9] / 1.965e6);
     unsigned long long *dv = dva;
     int nov = 0;
     for (uint32_t g = 0; g < P.G; ++g) nov += dropped[g];
