@@ -2,16 +2,18 @@
 //
 // Same semantics as fastval._join_pairs (fastval.py:47-108): every left key is joined with every
 // unfiltered right key of the same batch and all full-64-bit-hash-equal pairs are counted
-// (hash_hits) and reported for exact confirmation.  Instead of bucket chains in DRAM, one wave of
-// batches is joined in two launches:
+// (hash_hits) and reported for exact confirmation.  Instead of bucket chains in DRAM, waves of
+// batches are partitioned and joined:
 //
-//   k_scatter  enumerate + hash (msp_tile.cuh), stage 4096 keys per CTA round in shared memory,
-//              counting-sort them by bucket (top bits of the key within the batch), reserve space
-//              per bucket with one global atomic, and write bucket-contiguous runs into an
-//              L2-resident scratch.  Right pairs that overshoot d are counted, not written.
-//   k_join     one CTA per bucket: insert the build side's keys (the smaller side of the batch)
-//              into a 16K-slot (key, count) table in shared memory, stream the probe side's keys
-//              through it, count hash hits, record each hit key once for recovery.
+//   scatter_chunk  enumerate + hash (msp_tile.cuh) a chunk of one batch side's tiles and partition
+//                  the keys by bucket (top of the key) through a shared-memory stage in which a
+//                  key's slot is its rank inside its bucket entry (no sort), flushing each round
+//                  as one coalesced run per bucket into the wave's scratch.  Right pairs that
+//                  overshoot d are counted, not written.
+//   join_bucket    one CTA per bucket: insert the build side's keys (the smaller side of the batch)
+//                  into a 16K-slot table in shared memory, stream the probe side's keys through
+//                  it, count hash hits, record each hit key once for recovery.
+//   k_waves        the persistent pipeline that runs both as tasks of one launch (one CTA per SM).
 //
 // The per-bucket capacity is sized from the exact batch counts (mean + 7 sigma); a bucket that
 // overflows (duplicate-heavy instances) marks its batch, which the host re-joins with the global
@@ -37,6 +39,10 @@ constexpr int kOvf = 2048 / kScatterCtas;                       // keys ranked p
 constexpr int kOvfTrigger = kOvf * 3 / 8;                       // a round ends at this many (default)
 constexpr int kMaxNB = kMaxWaveBuckets;                         // entries of one unit
 constexpr uint32_t kDrop = 0xFFFFFFFFu;
+#ifndef MSP_SCATTER_KEYS
+#define MSP_SCATTER_KEYS 4
+#endif
+constexpr int kUS = MSP_SCATTER_KEYS;                           // keys per lane per scatter step
 
 // Reservation of n slots at *p, result left in flight in r (predicated: no-op when n == 0, so no
 // select has to wait for the atomic's return value).
@@ -65,7 +71,7 @@ struct __align__(16) Stage {
   uint32_t nstaged, pad[2];          // keys staged this round (fill trigger)
 };
 
-size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kU) * sw * 4; }
+size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kUS) * sw * 4; }
 
 __device__ __forceinline__ void stage_init(Stage &g) {
   for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
@@ -274,7 +280,7 @@ __device__ __forceinline__ void tile_vecs(const ScatterArgs &A, uint32_t side, c
   load_vec<SW>(yt, d.y + min(lane, qn - 1u), yv);
 }
 
-// kU keys of the current tile (loop entries q .. q+kU-1) into the stage.
+// kUS keys of the current tile (loop entries q .. q+kUS-1) into the stage.
 template <int MC, bool RIGHT>
 __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uint32_t *ybuf,
                                           const uint32_t (&lv)[stride_for(MC)],
@@ -283,13 +289,13 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
                                           const UnitInfo &ui, uint32_t nbk, uint32_t diag,
                                           unsigned long long &filt, unsigned long long &dacc) {
   constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
-  unsigned long long key[kU];
-  uint32_t j[kU];
-  bool ok[kU];
+  unsigned long long key[kUS];
+  uint32_t j[kUS];
+  bool ok[kUS];
 #pragma unroll
-  for (int u = 0; u < kU; ++u) {
+  for (int u = 0; u < kUS; ++u) {
     uint32_t yv[SW];
-    lds_vec<SW>(ybuf + (q + u) * SW, yv);  // ybuf holds kTQ + kU entries: reads past qn are padding
+    lds_vec<SW>(ybuf + (q + u) * SW, yv);  // ybuf holds kTQ + kUS entries: reads past qn are padding
     uint32_t sv[NW];
 #pragma unroll
     for (int k = 0; k < NW; ++k) sv[k] = lv[k] + yv[k];
@@ -318,9 +324,9 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
   }
   if (diag) {
 #pragma unroll
-    for (int u = 0; u < kU; ++u) dacc ^= ok[u] ? key[u] : 0ull;
+    for (int u = 0; u < kUS; ++u) dacc ^= ok[u] ? key[u] : 0ull;
   } else {
-    stage_keys<kU>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, nbk * C * 7 / 8,
+    stage_keys<kUS>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, nbk * C * 7 / 8,
                    key, j, ok);
   }
 }
@@ -377,7 +383,7 @@ __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const Sc
         hash_step<MC, true>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
       else
         hash_step<MC, false>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
-      q += kU;
+      q += kUS;
       if (q >= qn) {  // next tile: everything it needs was loaded one (vectors) or two tiles ago
         t = tn;
         tn = tnn;
@@ -412,9 +418,9 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage &g = *reinterpret_cast<Stage *>(smem_raw);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kU) * SW;
+  uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kUS) * SW;
   stage_init(g);
-  for (uint32_t i = lane; i < (uint32_t)((kTQ + kU) * SW); i += 32) ybuf[i] = 0;
+  for (uint32_t i = lane; i < (uint32_t)((kTQ + kUS) * SW); i += 32) ybuf[i] = 0;
   uint32_t dg[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = A.dpack[k];
@@ -703,8 +709,8 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
   JoinSmem &T = *reinterpret_cast<JoinSmem *>(smem_raw);  // (union with the stage)
   __shared__ unsigned long long s_task;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kU) * SW;
-  for (uint32_t i = lane; i < (uint32_t)((kTQ + kU) * SW); i += 32) ybuf[i] = 0;
+  uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem_raw + sizeof(Stage)) + warp * (kTQ + kUS) * SW;
+  for (uint32_t i = lane; i < (uint32_t)((kTQ + kUS) * SW); i += 32) ybuf[i] = 0;
   uint32_t dg[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) dg[k] = W.sc.dpack[k];
