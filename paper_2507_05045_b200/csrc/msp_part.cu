@@ -539,16 +539,11 @@ __device__ __forceinline__ JoinHash join_hash(unsigned long long k) {
   return h;
 }
 
-__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {  // nonzero iff some byte of x is 0
-  return (x - 0x01010101u) & ~x & 0x80808080u;
+// 0x80 in exactly the bytes of x that are zero (no false positives, unlike the borrow trick).
+__device__ __forceinline__ unsigned long long zero_byte_mask(unsigned long long x) {
+  constexpr unsigned long long k7F = 0x7F7F7F7F7F7F7F7Full;
+  return ~(((x & k7F) + k7F) | x | k7F);
 }
-__device__ __forceinline__ bool any_lane_eq(unsigned long long w, uint32_t pat) {
-  return (zero_bytes((uint32_t)w ^ pat) | zero_bytes((uint32_t)(w >> 32) ^ pat)) != 0u;
-}
-__device__ __forceinline__ bool bucket_full(unsigned long long w) {
-  return (zero_bytes((uint32_t)w) | zero_bytes((uint32_t)(w >> 32))) == 0u;
-}
-
 __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   const JoinHash h = join_hash(k);
   uint32_t b = h.b1, s = atomicAdd(&T.cnt[b], 1u);
@@ -562,29 +557,35 @@ __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   }
 }
 
-__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, unsigned long long w, uint32_t fp,
-                                                unsigned long long k, uint32_t &c, uint32_t &first) {
-#pragma unroll
-  for (int s = 0; s < kJWays; ++s)
-    if (((w >> (8 * s)) & 0xFFu) == fp && T.key[b][s] == k) {
+// Copies of k among the slots of bucket b whose fingerprint byte matches (one iteration per match:
+// usually none, so a warp rarely runs the key comparisons at all).
+__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, unsigned long long w,
+                                                unsigned long long pat, unsigned long long k, uint32_t &c,
+                                                uint32_t &first) {
+  unsigned long long m = zero_byte_mask(w ^ pat);
+  while (m) {
+    const uint32_t s = (uint32_t)(__ffsll((long long)m) - 1) >> 3;
+    if (T.key[b][s] == k) {
       if (!c) first = b * kJWays + s;
       ++c;
     }
+    m &= m - 1;
+  }
 }
 
 // Multiplicity of k in the table; `first` = slot id of its first copy (b1, then b2, then stash).
 __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long long k, uint32_t nstash,
                                                uint32_t &first) {
   const JoinHash h = join_hash(k);
-  const uint32_t pat = h.fp * 0x01010101u;
+  const unsigned long long pat = h.fp * 0x0101010101010101ull;
   const unsigned long long w1 = T.fp[h.b1];
   uint32_t c = 0;
   first = 0xFFFFFFFFu;
-  if (any_lane_eq(w1, pat)) count_in_bucket(T, h.b1, w1, h.fp, k, c, first);
-  if (bucket_full(w1)) {  // k may have moved on to b2 (and, if b2 is full too, to the stash)
+  count_in_bucket(T, h.b1, w1, pat, k, c, first);
+  if (!zero_byte_mask(w1)) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
     const unsigned long long w2 = T.fp[h.b2];
-    if (any_lane_eq(w2, pat)) count_in_bucket(T, h.b2, w2, h.fp, k, c, first);
-    if (bucket_full(w2))
+    count_in_bucket(T, h.b2, w2, pat, k, c, first);
+    if (!zero_byte_mask(w2))
       for (uint32_t i = 0; i < nstash; ++i)
         if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
   }
@@ -716,37 +717,57 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
   for (int k = 0; k < NW; ++k) dg[k] = W.sc.dpack[k];
   unsigned long long dacc = 0;
   long long t_prev = clock64();
-  // thread 0 keeps the NEXT task (index claimed and word loaded) in flight while the CTA works
-  unsigned long long tk_next = ~0ull;
-  if (tid == 0) {
+  // Thread 0 keeps the NEXT task in flight while the CTA works: its index (atomic), word, wave
+  // descriptor, chunk word and dependency target are loaded a whole task ahead; at the switch it
+  // waits for the dependency (acquire load) and hands everything over through shared memory.
+  struct Next { unsigned long long tk, cw; WaveDesc wd; uint32_t need; const unsigned int *ctr; };
+  __shared__ unsigned long long s_cw;
+  __shared__ WaveDesc s_wd;
+  auto fetch = [&](Next &x) {
     const uint32_t i = atomicAdd(W.task_ctr, 1u);
-    tk_next = i < W.ntasks ? W.tasks[i] : ~0ull;
-  }
+    x.tk = i < W.ntasks ? W.tasks[i] : ~0ull;
+    x.ctr = nullptr;
+    x.need = 0;
+    x.cw = 0;
+    if (x.tk == ~0ull) return;
+    const uint32_t w = (uint32_t)(x.tk >> 32) & 0x7FFFFFFFu;
+    x.wd = W.waves[w];
+    if (x.tk >> 63) {
+      x.ctr = W.scat_done + w;
+      x.need = x.wd.nchunks;
+    } else {
+      x.cw = __ldg(W.chunks + x.wd.chunk0 + (uint32_t)x.tk);
+      if (w >= kWaveBuffers) {  // the last wave on this scratch buffer must be fully joined
+        x.ctr = W.join_done + w - kWaveBuffers;
+        x.need = W.waves[w - kWaveBuffers].njoin;
+      }
+    }
+  };
+  Next nx;
+  if (tid == 0) fetch(nx);
   while (true) {
     if (tid == 0) {
-      unsigned long long tk = tk_next;
-      if (tk != ~0ull) {
-        const uint32_t i = atomicAdd(W.task_ctr, 1u);
-        tk_next = i < W.ntasks ? W.tasks[i] : ~0ull;
-      }
-      if (tk != ~0ull) {  // wait for the task's dependency
-        const uint32_t w = (uint32_t)(tk >> 32) & 0x7FFFFFFFu;
-        const bool join = tk >> 63;
-        const uint32_t prev = w >= kWaveBuffers ? w - kWaveBuffers : 0u;  // last wave on this buffer
-        volatile unsigned int *ctr = join ? W.scat_done + w : (w >= kWaveBuffers ? W.join_done + prev : nullptr);
-        const uint32_t need = join ? W.waves[w].nchunks : (w >= kWaveBuffers ? W.waves[prev].njoin : 0u);
+      const Next cur = nx;
+      if (cur.tk != ~0ull) fetch(nx);
+      if (cur.ctr) {
         const long long tw = clock64();
-        if (ctr) while (*ctr < need) __nanosleep(256);
-        __threadfence();
+        uint32_t v;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cur.ctr) : "memory");
+          if (v >= cur.need) break;
+          __nanosleep(256);
+        }
         if (W.pa.dbg) atomicAdd(W.pa.dbg + 6, (unsigned long long)(clock64() - tw));
       }
-      s_task = tk;
+      s_task = cur.tk;
+      s_cw = cur.cw;
+      s_wd = cur.wd;
     }
     __syncthreads();
     const unsigned long long tk = s_task;
     if (tk == ~0ull) break;
     const uint32_t w = (uint32_t)(tk >> 32) & 0x7FFFFFFFu, idx = (uint32_t)tk;
-    const WaveDesc wd = W.waves[w];
+    const WaveDesc wd = s_wd;
     PartArgs S = W.pa;
     S.scratch = W.scratch[w % kWaveBuffers];
     S.fill[0] = W.fill[w % kWaveBuffers];
@@ -761,14 +782,13 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
     if (tk >> 63) {  // join: buckets [idx, idx + kJoinGroup) of the wave
       const uint32_t b1 = min(idx + (uint32_t)kJoinGroup, wd.nb);
       for (uint32_t b = idx; b < b1; ++b) join_bucket<kScatterThreads>(T, S, b);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) atomicAdd(W.join_done + w, 1u);
+      __syncthreads();  // (join_bucket ended with one; the CTA's writes are ordered before the release)
+      if (tid == 0) { __threadfence(); atomicAdd(W.join_done + w, 1u); }
       if (tid == 0 && W.pa.dbg) { const long long now = clock64(); atomicAdd(W.pa.dbg + 5, (unsigned long long)(now - t_prev)); t_prev = now; }
     } else {  // scatter chunk idx of the wave (tiles, or a level-2 slot range of a coarse region)
       stage_init(g);
       __syncthreads();
-      const unsigned long long cw = __ldg(W.chunks + wd.chunk0 + idx);
+      const unsigned long long cw = s_cw;
       if (wd.kind) {
         const RescatterSrc &src = W.srcs[wd.src0 + (uint32_t)(cw >> 48)];
         const uint32_t s0 = (uint32_t)cw;
@@ -780,9 +800,8 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
         const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
         scatter_chunk<MC>(g, ybuf, A, S, dg, W.sc.units[wd.unit0 + unit], t0, n, dacc);
       }
-      __threadfence();
       __syncthreads();
-      if (tid == 0) atomicAdd(W.scat_done + w, 1u);
+      if (tid == 0) { __threadfence(); atomicAdd(W.scat_done + w, 1u); }
       if (tid == 0 && W.pa.dbg) { const long long now = clock64(); atomicAdd(W.pa.dbg + 4, (unsigned long long)(now - t_prev)); t_prev = now; }
     }
   }
