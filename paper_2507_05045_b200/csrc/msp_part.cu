@@ -32,7 +32,10 @@ namespace msp {
 // write-out) overlaps the other's enumeration.
 constexpr int kScatterCtas = MSP_SCATTER_CTAS;
 static_assert(kScatterCtas == kScatterCtasHost, "scatter CTAs per SM: msp_kernels.h and msp_part.cu disagree");
-constexpr int kScatterWarps = 16 / kScatterCtas;
+#ifndef MSP_SCATTER_WARPS
+#define MSP_SCATTER_WARPS (16 / MSP_SCATTER_CTAS)
+#endif
+constexpr int kScatterWarps = MSP_SCATTER_WARPS;
 constexpr int kScatterThreads = kScatterWarps * 32;
 constexpr int kStageKeys = kScatterStageKeys;                   // stage slots of a CTA
 constexpr int kOvf = 2048 / kScatterCtas;                       // keys ranked past their entry's C slots

@@ -149,6 +149,11 @@ uint32_t pow2ceil(uint64_t v) {
   return l;
 }
 
+// Keys per partitioned wave (both roles).  Bigger waves mean fewer two-level batches and fewer,
+// fuller pipeline stages; the bucket limit (kMaxWaveBuckets per role) caps a wave near 8M build
+// keys anyway.  Four pipeline buffers of this size live in HBM (~1.4 GB).
+constexpr uint64_t kDefaultWaveKeys = 40ull << 20;
+
 // Everything msp_solve needs after K1 + K2.
 struct Plan {
   int m = 0, n = 0, mc = 0, sw = 1;
@@ -202,7 +207,7 @@ int check_instance(const msp_problem *pr, Plan &P) {
 
 // K1 + K2 on the device; ends with the batch list and tile totals on the host.
 int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uint64_t alpha_hi,
-               cudaStream_t st, int64_t &launches, uint64_t item_key_budget = 10ull << 20) {
+               cudaStream_t st, int64_t &launches, uint64_t item_key_budget = kDefaultWaveKeys) {
   const int m = P.m, n = P.n;
   CK(D.a.ensure(sizeof(uint64_t) * m * n));
   CK(D.d.ensure(sizeof(uint64_t) * m));
@@ -590,7 +595,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   if (rc) return rc;
   const double deadline = opt->time_limit_s > 0 ? t0 + opt->time_limit_s : 0;
   CK(cudaEventRecord(D.ev[0], st));
-  const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : (10ull << 20);
+  const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : kDefaultWaveKeys;
   rc = build_plan(D, pr, P, opt->alpha_lo, opt->alpha_hi, st, S.kernel_launches, key_budget);
   if (rc) return rc;
   CK(cudaGetLastError());
