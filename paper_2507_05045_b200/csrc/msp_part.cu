@@ -227,25 +227,26 @@ __device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_
 
 // ---------------------------------------------------------------- tile descriptors
 
+// One warp per rectangle, lanes over its nl x nq warp tiles (consecutive lanes write consecutive
+// 16-byte descriptors: coalesced).
 __global__ void k_tiles(const TileGenArgs a) {
-  for (uint32_t r = a.rect_lo + blockIdx.x * blockDim.x + threadIdx.x; r < a.rect_hi; r += gridDim.x * blockDim.x) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t wpg = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t r = a.rect_lo + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.rect_hi; r += wpg) {
     const RectDesc R = a.rects[r];
     const uint32_t gs = R.gs();
     const uint32_t unit = a.gs_unit ? a.gs_unit[gs] : 0u;
     if (unit == 0xFFFFFFFFu) continue;
     TileDesc *out = a.out + (a.gs_tile_base ? a.gs_tile_base[gs] : 0ull) + R.tile_off;
     const uint32_t lx = R.lane_is_x() ? 1u : 0u;
-    for (uint32_t lc = 0; lc < R.nl; ++lc) {
+    const uint32_t nt = R.nl * R.nq;
+    for (uint32_t t = lane; t < nt; t += 32) {
+      const uint32_t lc = t / R.nq, qc = t - lc * R.nq;
       const uint32_t ln = min(32u, R.L - lc * 32);
-      for (uint32_t qc = 0; qc < R.nq; ++qc) {
-        const uint32_t qn = min((uint32_t)kTQ, R.Q - qc * kTQ);
-        TileDesc t;
-        t.lane0 = R.lane_start + lc * 32;
-        t.loop0 = R.loop_start + qc * kTQ;
-        t.meta = unit | ((ln - 1) << 8) | ((qn - 1) << 13) | (lx << 18);
-        t.pad = 0;
-        *out++ = t;
-      }
+      const uint32_t qn = min((uint32_t)kTQ, R.Q - qc * kTQ);
+      const uint4 v = make_uint4(R.lane_start + lc * 32, R.loop_start + qc * kTQ,
+                                 unit | ((ln - 1) << 8) | ((qn - 1) << 13) | (lx << 18), 0u);
+      *reinterpret_cast<uint4 *>(out + t) = v;
     }
   }
 }
@@ -253,8 +254,8 @@ __global__ void k_tiles(const TileGenArgs a) {
 void launch_tiles(const TileGenArgs &a, cudaStream_t st) {
   const uint32_t n = a.rect_hi - a.rect_lo;
   if (!n) return;
-  const uint32_t blocks = (n + 127) / 128;
-  k_tiles<<<blocks < 1184 ? blocks : 1184, 128, 0, st>>>(a);
+  const uint32_t blocks = (n + 7) / 8;  // 8 warps per block
+  k_tiles<<<blocks < 2368 ? blocks : 2368, 256, 0, st>>>(a);
 }
 
 // ---------------------------------------------------------------- scatter (enumerate + hash + partition)
