@@ -503,6 +503,9 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_rescatter(con
   }
 }
 
+#ifndef MSP_JOIN_U
+#define MSP_JOIN_U 4
+#endif
 constexpr int kJoinThreads = 1024;
 constexpr int kJoinSlots = 1 << kJoinSlotsLog2;        // 16K key slots
 constexpr int kJWays = 8;                               // slots per table bucket
@@ -604,7 +607,7 @@ __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long 
 template <int NT>
 __device__ __forceinline__ void join_bucket(JoinSmem &T, const PartArgs &S, uint32_t b) {
   const uint32_t tid = threadIdx.x;
-  constexpr int U = 8;  // keys loaded per thread before the table operations
+  constexpr int U = MSP_JOIN_U;  // keys loaded per thread before the table operations
   long long tp0 = 0, tp1 = 0, tp2 = 0;
   if (S.dbg && tid == 0) tp0 = clock64();
   for (uint32_t i = tid; i < (uint32_t)kJBuckets; i += NT) { T.cnt[i] = 0u; T.fp[i] = 0ull; }
