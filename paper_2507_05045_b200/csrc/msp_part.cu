@@ -42,6 +42,9 @@ constexpr int kOvf = 2048 / kScatterCtas;                       // keys ranked p
 constexpr int kOvfTrigger = kOvf * 3 / 8;                       // a round ends at this many (default)
 constexpr int kMaxNB = kMaxWaveBuckets;                         // entries of one unit
 constexpr uint32_t kDrop = 0xFFFFFFFFu;
+#ifndef MSP_RESCATTER_N
+#define MSP_RESCATTER_N 4
+#endif
 #ifndef MSP_SCATTER_KEYS
 #define MSP_SCATTER_KEYS 4
 #endif
@@ -450,7 +453,7 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
                                                 uint32_t s1) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   volatile uint32_t *round_end = &g.round_end;
-  constexpr int N = 8;  // keys per lane per step; the next step's keys are in flight meanwhile (HBM)
+  constexpr int N = MSP_RESCATTER_N;  // keys per lane per step; the next step's keys are in flight meanwhile (HBM)
   const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
   uint32_t C, cmagic;
   stage_geometry(NB, C, cmagic);
