@@ -219,6 +219,29 @@ def test_m8_s1_full_against_golden():
     assert res.stats.row1_candidate_pairs == rec["row1_candidate_pairs"]
 
 
+@pytest.mark.parametrize("seed", [1, 2])
+def test_planted_m6_matches_oracle(seed):
+    """BASELINE configs[1]: planted-feasible (6,50) instances (SURVEY.md §8(d) recipe): the planted x*
+    is found and solutions + every counter equal the pinned oracle's."""
+    inst, x = msb.plant_instance(6, 100, seed)
+    res = _solve_all(inst)
+    assert tuple(x) in res.solutions
+    ref = O.solve(inst.a, inst.d, mode="all", workers=8)
+    assert res.solutions == ref.solutions
+    for k in STAT_KEYS:
+        assert getattr(res.stats, k) == ref.stats[k], k
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("m,seed", [(7, 3), (8, 1)])
+def test_planted_large_found(m, seed):
+    """Planted (7,60) and (8,70) instances: the planted x* is among the (verified) solutions."""
+    inst, x = msb.plant_instance(m, 100, seed)
+    res = _solve_all(inst)
+    assert tuple(x) in res.solutions
+    assert all(msb.verify_solution(inst, s) for s in res.solutions)
+
+
 def test_cancel_word_stops_the_solve(tmp_path):
     """msp_options.cancel: a set word stops the solve (stats.cancelled, no solutions); unset is inert."""
     from paper_2507_05045_b200.distributed import CancelFlag
