@@ -134,6 +134,25 @@ def test_random_instances_match_oracle():
             assert getattr(res.stats, k) == ref.stats[k], (seed, k)
 
 
+def test_stress_duplicates_and_tiny_waves():
+    """Duplicate-heavy instances (m = 1, tiny K: many equal keys in a bucket -> stage overflow,
+    spills, join stash and the global-table fallback) and tiny wave budgets (many pipeline waves,
+    two-level batches), each against the oracle."""
+    from paper_2507_05045_b200.solver import native_solve
+
+    for seed in range(12):
+        m = 1 + seed % 3
+        n = 14 + seed % 5
+        inst = seeded_instance(9100 + seed, m=m, n=n, k=3 + seed % 6, d_mode="half")
+        ref = O.solve(inst.a, inst.d, mode="all")
+        for wk in (0, 4096, 50000):
+            sols, st = native_solve(inst, "all", None, brute_force_max_n=0, wave_keys=wk,
+                                    flags=_native.MSP_FLAG_FORCE_TABLE_PATH)
+            assert sorted(sols, key=msb.solution_encoding) == ref.solutions, (seed, wk)
+            for k in STAT_KEYS:
+                assert st[k] == ref.stats[k], (seed, wk, k)
+
+
 def test_small_waves_force_multi_pass_join():
     """A tiny wave budget forces batches to split into hash-range passes: results unchanged."""
     inst = msb.generate_instance(6, 100, 4)
