@@ -85,7 +85,10 @@ constexpr int kMaxWaveBuckets = 1024;  // buckets per role per wave
 #define MSP_SCATTER_CTAS 1
 #endif
 constexpr int kScatterCtasHost = MSP_SCATTER_CTAS;  // resident k_scatter CTAs per SM (grid = SMs x this)
-constexpr int kScatterStageKeys = 20480 / MSP_SCATTER_CTAS;  // stage slots of a scatter CTA
+#ifndef MSP_STAGE_KEYS
+#define MSP_STAGE_KEYS (23552 / MSP_SCATTER_CTAS)
+#endif
+constexpr int kScatterStageKeys = MSP_STAGE_KEYS;  // stage slots of a scatter CTA
 constexpr int kJoinSlotsLog2 = 14;     // shared-memory join table: 16K (key, count) slots
 constexpr uint32_t kBucketTarget = 1u << (kJoinSlotsLog2 - 1);  // mean build keys per bucket
 struct PartArgs {

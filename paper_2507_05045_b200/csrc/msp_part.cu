@@ -38,7 +38,10 @@ static_assert(kScatterCtas == kScatterCtasHost, "scatter CTAs per SM: msp_kernel
 constexpr int kScatterWarps = MSP_SCATTER_WARPS;
 constexpr int kScatterThreads = kScatterWarps * 32;
 constexpr int kStageKeys = kScatterStageKeys;                   // stage slots of a CTA
-constexpr int kOvf = 2048 / kScatterCtas;                       // keys ranked past their entry's C slots
+#ifndef MSP_OVF_KEYS
+#define MSP_OVF_KEYS (1024 / MSP_SCATTER_CTAS)
+#endif
+constexpr int kOvf = MSP_OVF_KEYS;                              // keys ranked past their entry's C slots
 constexpr int kOvfTrigger = kOvf * 3 / 8;                       // a round ends at this many (default)
 constexpr int kMaxNB = kMaxWaveBuckets;                         // entries of one unit
 constexpr uint32_t kDrop = 0xFFFFFFFFu;

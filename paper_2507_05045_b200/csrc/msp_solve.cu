@@ -1154,6 +1154,15 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         mcp = std::max<uint64_t>(mcp, (uint64_t)even_up(mp + 7.0 * std::sqrt(mp) + 16) << cbits);
         mt = std::max<uint64_t>(mt, std::max(P.tiles[2 * (size_t)g], P.tiles[2 * (size_t)g + 1]));
       }
+      {  // the coarse regions of the largest batch must fit next to everything else
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        const uint64_t need = 8 * (mcb + mcp + 2 * kSinkSlots), have = free_b + D.cscratch[0].cap + D.cscratch[1].cap;
+        if (need > have) {
+          set_err("largest batch needs %.1f GB of coarse scratch, %.1f GB available", need / 1e9, have / 1e9);
+          return MSP_UNSUPPORTED;
+        }
+      }
       CK(D.cscratch[0].ensure(8 * (mcb + kSinkSlots)));
       CK(D.cscratch[1].ensure(8 * (mcp + kSinkSlots)));
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, mt)));

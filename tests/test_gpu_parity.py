@@ -153,6 +153,24 @@ def test_stress_duplicates_and_tiny_waves():
                 assert st[k] == ref.stats[k], (seed, wk, k)
 
 
+def test_many_rows_match_oracle():
+    """m = 10, 12, 16 (8-word companion vectors: the largest stage + loop-buffer layout) vs the oracle."""
+    from paper_2507_05045_b200.solver import native_solve
+
+    for seed, m in ((1, 10), (2, 12), (3, 16), (4, 10), (5, 14)):
+        inst = seeded_instance(500 + seed, m=m, n=26, k=20)
+        if seed >= 4:  # planted: d = A x* for a fixed x*, so the instance is feasible
+            x = [(j * 7 + seed) % 3 == 0 for j in range(inst.n)]
+            rows = inst.a.tolist()
+            inst = msb.MspInstance(rows, [sum(r[j] for j in range(inst.n) if x[j]) for r in rows], k_bound=20)
+        ref = O.solve(inst.a, inst.d, mode="all")
+        assert seed < 4 or ref.solutions
+        sols, st = native_solve(inst, "all", None, brute_force_max_n=0, flags=_native.MSP_FLAG_FORCE_TABLE_PATH)
+        assert sorted(sols, key=msb.solution_encoding) == ref.solutions, m
+        for k in STAT_KEYS:
+            assert st[k] == ref.stats[k], (m, k)
+
+
 def test_small_waves_force_multi_pass_join():
     """A tiny wave budget forces batches to split into hash-range passes: results unchanged."""
     inst = msb.generate_instance(6, 100, 4)
