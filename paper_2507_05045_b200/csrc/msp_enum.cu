@@ -80,7 +80,7 @@ template <int KIND>
 __device__ __forceinline__ void sink_batch(const JoinTable &jt, const UnitDesc &d, const uint64_t (&key)[kU],
                                            bool (&ok)[kU], const RectDesc &R, const uint32_t (&lidx)[kU],
                                            const uint32_t (&qidx)[kU], const EnumArgs &A,
-                                           unsigned long long &hits) {
+                                           unsigned long long &hits, const uint32_t *rfilt = nullptr) {
 #pragma unroll
   for (int u = 0; u < kU; ++u)
     if (ok[u] && d.npass > 1 && pass_of(key[u], d.npass) != d.pass) ok[u] = false;
@@ -149,6 +149,8 @@ __device__ __forceinline__ void sink_batch(const JoinTable &jt, const UnitDesc &
       bool present;
       if (key[u] == 0) {
         present = d.flags & 1u;
+      } else if (!((rfilt[key[u] >> 53] >> ((key[u] >> 48) & 31u)) & 1u)) {
+        present = false;  // no hit key of the launch starts with these 16 bits (shared-memory filter)
       } else {
         uint32_t slot;
         present = table_find(jt, d, key[u], home_slot(key[u], d.region_log2), slot);
@@ -246,6 +248,18 @@ __global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTab
 
   __shared__ __align__(16) uint32_t ybuf_all[8][kTQ * stride_for(MC)];
   __shared__ unsigned long long stage_all[kBulk ? 8 : 1][kBulk ? kEnumStage : 1];
+  // hit recovery: a 64K-bit filter of the hit keys' top 16 bits, so almost every key is rejected
+  // by one shared load instead of a global hash-table probe
+  __shared__ uint32_t rfilt[KIND == SINK_RECOVER ? 2048 : 1];
+  if constexpr (KIND == SINK_RECOVER) {
+    for (uint32_t i = threadIdx.x; i < 2048u; i += blockDim.x) rfilt[i] = 0u;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < jt.nkeys; i += blockDim.x) {
+      const unsigned long long k = jt.keys[i];
+      if (k) atomicOr(&rfilt[k >> 53], 1u << ((k >> 48) & 31u));
+    }
+    __syncthreads();
+  }
   unsigned long long *stage = stage_all[kBulk ? wl : 0];
   for (uint64_t chunk = wid; chunk < A.nchunks; chunk += nwarps) {
     TileWalker W;
@@ -279,7 +293,7 @@ __global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTab
           step_keys<MC>(W, C, dg, filt, [&](int u, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
             kk[u] = key; okk[u] = ok; li[u] = lidx; qi[u] = qidx;
           });
-          sink_batch<KIND>(jt, W.d, kk, okk, W.R, li, qi, A, hits);
+          sink_batch<KIND>(jt, W.d, kk, okk, W.R, li, qi, A, hits, rfilt);
         }
       }
       const UnitDesc dprev = W.d;

@@ -68,6 +68,7 @@ struct JoinTable {
   HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;
   PairRec *recs; unsigned long long *nrecs; uint64_t rec_cap;
   int *err;
+  uint32_t nkeys;              // recovery: slots of `keys` (all regions), scanned for the filter
 };
 
 void launch_merge_step(const MergeArgs &a, uint32_t max_n, cudaStream_t st);

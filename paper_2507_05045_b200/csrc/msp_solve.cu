@@ -734,6 +734,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(cudaMemcpyAsync(D.runits.p, ru.data(), sizeof(UnitDesc) * ru.size(), cudaMemcpyHostToDevice, st));
     JoinTable rj = jt;
     rj.keys = D.rkeys.as<unsigned long long>();
+    rj.nkeys = (uint32_t)slots;
     EnumArgs RA = P.base;
     RA.batch_filtered = D.rfilt.as<unsigned long long>();
     RA.batch_hits = D.rhits.as<unsigned long long>();
