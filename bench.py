@@ -306,7 +306,7 @@ def main() -> int:
         "traffic": None,
     }
     try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/README.md)
-        with open(os.path.join(HERE, "profiles", "r1e_kernels.json")) as fh:
+        with open(os.path.join(HERE, "profiles", "r1f_kernels.json")) as fh:
             tr = json.load(fh)["traffic"]
         roofline["traffic"] = {"dram_bytes_per_launch": tr["launch_dram_bytes"],
                                "algorithmic_bytes_per_launch": tr["algorithmic_bytes_per_launch"],

@@ -1141,7 +1141,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   //      side's region indices stay 32-bit); level 2 streams coarse buckets back, re-partitions
   //      them into fine buckets in the L2 scratch and joins them (k_rescatter + k_join).
   if (!stopped && !huge_b.empty()) {
-    constexpr uint64_t kCoarseTarget = 2ull << 20;  // build keys per coarse bucket
+    uint64_t kCoarseTarget = 2ull << 20;  // build keys per coarse bucket (MSP_COARSE_TARGET: tuning)
+    if (const char *ev = getenv("MSP_COARSE_TARGET")) kCoarseTarget = std::max<uint64_t>(65536, strtoull(ev, nullptr, 10));
     CK(D.cfill.ensure(4 * 2 * kMaxWaveBuckets));
     {  // size the big per-batch buffers once for the largest batch (a regrowth stalls the stream)
       uint64_t mcb = 0, mcp = 0, mt = 0;
