@@ -552,10 +552,18 @@ __device__ __forceinline__ JoinHash join_hash(unsigned long long k) {
   return h;
 }
 
-// 0x80 in exactly the bytes of x that are zero (no false positives, unlike the borrow trick).
+// 0x80 in exactly the bytes of x that are zero (no false positives, unlike the borrow trick).  Per
+// 32-bit half: (x & 0x7F..) + 0x7F.. never carries across a byte, so the halves are independent.
+__device__ __forceinline__ uint32_t zero_byte_mask32(uint32_t x) {
+  return ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);
+}
 __device__ __forceinline__ unsigned long long zero_byte_mask(unsigned long long x) {
-  constexpr unsigned long long k7F = 0x7F7F7F7F7F7F7F7Full;
-  return ~(((x & k7F) + k7F) | x | k7F);
+  return ((unsigned long long)zero_byte_mask32((uint32_t)(x >> 32)) << 32) | zero_byte_mask32((uint32_t)x);
+}
+// Some byte of w is zero (an empty slot): the borrow trick, exact for presence.
+__device__ __forceinline__ bool has_zero_byte(unsigned long long w) {
+  const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+  return (((lo - 0x01010101u) & ~lo) | ((hi - 0x01010101u) & ~hi)) & 0x80808080u;
 }
 __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   const JoinHash h = join_hash(k);
@@ -595,10 +603,10 @@ __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long 
   uint32_t c = 0;
   first = 0xFFFFFFFFu;
   count_in_bucket(T, h.b1, w1, pat, k, c, first);
-  if (!zero_byte_mask(w1)) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
+  if (!has_zero_byte(w1)) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
     const unsigned long long w2 = T.fp[h.b2];
     count_in_bucket(T, h.b2, w2, pat, k, c, first);
-    if (!zero_byte_mask(w2))
+    if (!has_zero_byte(w2))
       for (uint32_t i = 0; i < nstash; ++i)
         if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
   }
