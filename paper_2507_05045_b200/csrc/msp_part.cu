@@ -110,21 +110,21 @@ __device__ __noinline__ void stage_spill(Stage &g, const PartArgs &S, uint32_t e
 // Stage N keys per lane into their entries j (local to the chunk's unit): rank (shared atomics,
 // all issued before any dependent store), store into the entry's slots.  Keys ranked past C go to
 // the overflow list with (entry, rank): one warp-aggregated reservation per warp step.  The round
-// ends once the list passes `trig` (many small entries overflow early) or some entry reaches rank
-// `ftrig` (few big entries all fill at once: stop before the warps in flight overflow).
+// ends once the list passes `trig` (few big entries... many small ones overflow early) or the stage
+// holds `ftrig` keys (few big entries all fill at once: stop before the warps in flight overflow).
 template <int N>
 __device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t lane, uint32_t C,
                                            uint32_t trig, uint32_t ftrig,
                                            const unsigned long long (&key)[N], const uint32_t (&j)[N],
                                            const bool (&ok)[N]) {
-  uint32_t r[N];
-  bool fill = false;
+  uint32_t r[N], nok = 0;
 #pragma unroll
   for (int u = 0; u < N; ++u) {
     r[u] = ok[u] ? atomicAdd(&g.cnt[j[u]], 1u) : 0u;
-    fill |= ok[u] && r[u] == ftrig;  // an entry reached the fill mark: with keys spread uniformly
-  }                                  // over the entries, the stage is about that full
-  if (fill) *(volatile uint32_t *)&g.round_end = 1u;
+    nok += ok[u] ? 1u : 0u;
+  }
+  const uint32_t wok = __reduce_add_sync(0xffffffffu, nok);
+  if (lane == 0 && wok && atomicAdd(&g.nstaged, wok) + wok >= ftrig) *(volatile uint32_t *)&g.round_end = 1u;
   uint32_t nov = 0;
 #pragma unroll
   for (int u = 0; u < N; ++u) {
@@ -223,10 +223,6 @@ __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_
   if (tid == 0) { g.novf = 0u; g.round_end = 0u; g.ove_spill = 0u; g.nstaged = 0u; }
   __syncthreads();
 }
-
-// Rank at which an entry ends the round: 7/8 of its slots when entries are big (their fill is a
-// good estimate of the stage's); none for small entries, where the overflow trigger fires first.
-__device__ __forceinline__ uint32_t fill_mark(uint32_t C) { return C >= 128 ? C * 7 / 8 : 0xFFFFFFFFu; }
 
 // Per-chunk stage geometry: C slots per entry and ceil(2^32 / C) (s / C == umulhi(s, cmagic) for
 // every slot index s < kStageKeys).
@@ -340,7 +336,7 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
 #pragma unroll
     for (int u = 0; u < kUS; ++u) dacc ^= ok[u] ? key[u] : 0ull;
   } else {
-    stage_keys<kUS>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, fill_mark(C),
+    stage_keys<kUS>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, nbk * C * 7 / 8,
                    key, j, ok);
   }
 }
@@ -488,7 +484,7 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
         ok[u] = key[u] != 0ull;  // past the fill, or a run pad
         j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
       }
-      stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, fill_mark(C), key, j, ok);
+      stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, NB * C * 7 / 8, key, j, ok);
       idx += N * stride;
     }
     const bool more = __syncthreads_or(idx - lane < s1);
