@@ -198,10 +198,14 @@ __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_
   }
   __syncthreads();
   const uint32_t tot = NB * C;  // (NB * C <= kStageKeys; a dropped entry has run.y == 0)
-  for (uint32_t s = tid; s < tot; s += kScatterThreads) {
-    const uint32_t j = __umulhi(s, cmagic), i = s - j * C;
-    const uint2 run = g.run[j];
-    if (i < run.y) __stcg(S.scratch + run.x + i, g.key[s]);
+  for (uint32_t s0 = tid; s0 < tot; s0 += 2 * kScatterThreads) {  // two slots in flight per thread
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t s = s0 + h * kScatterThreads;
+      const uint32_t j = __umulhi(s, cmagic), i = s - j * C;
+      const uint2 run = s < tot ? g.run[j] : make_uint2(0u, 0u);
+      if (i < run.y) __stcg(S.scratch + run.x + i, g.key[s]);
+    }
   }
   if (g.ove_spill) {  // ranks past C whose keys were spilled stay empty: pad every rank past C
     __syncthreads();   // with key 0 (readers skip it), then write the listed overflow keys
@@ -302,6 +306,7 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
   unsigned long long key[kUS];
   uint32_t j[kUS];
   bool ok[kUS];
+  uint32_t nzero = 0;
 #pragma unroll
   for (int u = 0; u < kUS; ++u) {
     uint32_t yv[SW];
@@ -325,13 +330,12 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
       fold(lo, hi, (c & 1) ? (w >> 16) & (RIGHT ? 0x7FFFu : 0xFFFFu) : w & (RIGHT ? 0x7FFFu : 0xFFFFu));
     }
     key[u] = ((unsigned long long)hi << 32) | lo;
-    if (in && (hi | lo) == 0u) {  // a real key 0: counted per (batch, side), never staged
-      atomicAdd(S.zero_keys + 2 * ui.gid + (RIGHT ? 1u : 0u), 1ull);
-      in = false;
-    }
-    ok[u] = in;
+    const bool z = in && (hi | lo) == 0u;  // a real key 0: counted per (batch, side), never staged
+    nzero += z ? 1u : 0u;
+    ok[u] = in && !z;
     j[u] = __umulhi(hi, nbk);  // bucket within the unit = floor(hi * NB / 2^32)
   }
+  if (nzero) atomicAdd(S.zero_keys + 2 * ui.gid + (RIGHT ? 1u : 0u), (unsigned long long)nzero);
   if (diag) {
 #pragma unroll
     for (int u = 0; u < kUS; ++u) dacc ^= ok[u] ? key[u] : 0ull;
@@ -560,11 +564,9 @@ __device__ __forceinline__ uint32_t zero_byte_mask32(uint32_t x) {
 __device__ __forceinline__ unsigned long long zero_byte_mask(unsigned long long x) {
   return ((unsigned long long)zero_byte_mask32((uint32_t)(x >> 32)) << 32) | zero_byte_mask32((uint32_t)x);
 }
-// Some byte of w is zero (an empty slot): the borrow trick, exact for presence.
-__device__ __forceinline__ bool has_zero_byte(unsigned long long w) {
-  const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
-  return (((lo - 0x01010101u) & ~lo) | ((hi - 0x01010101u) & ~hi)) & 0x80808080u;
-}
+// Bucket full: slots are claimed in order 0..7 (one atomic count per bucket) and every claim below 8
+// writes its fingerprint before the build/probe barrier, so the bucket is full iff slot 7 is set.
+__device__ __forceinline__ bool bucket_full(unsigned long long w) { return (uint32_t)(w >> 56) != 0u; }
 __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   const JoinHash h = join_hash(k);
   uint32_t b = h.b1, s = atomicAdd(&T.cnt[b], 1u);
@@ -603,10 +605,10 @@ __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long 
   uint32_t c = 0;
   first = 0xFFFFFFFFu;
   count_in_bucket(T, h.b1, w1, pat, k, c, first);
-  if (!has_zero_byte(w1)) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
+  if (bucket_full(w1)) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
     const unsigned long long w2 = T.fp[h.b2];
     count_in_bucket(T, h.b2, w2, pat, k, c, first);
-    if (!has_zero_byte(w2))
+    if (bucket_full(w2))
       for (uint32_t i = 0; i < nstash; ++i)
         if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
   }
