@@ -549,8 +549,7 @@ __device__ __forceinline__ JoinHash join_hash(unsigned long long k) {
   const uint32_t t = (uint32_t)k * 0x9E3779B1u, hi = (uint32_t)(k >> 32);
   JoinHash h;
   h.b1 = t >> 21;
-  h.b2 = (t >> 10) & (kJBuckets - 1);
-  if (h.b2 == h.b1) h.b2 ^= 1u;
+  h.b2 = h.b1 ^ (((t >> 10) & (kJBuckets - 1)) | 1u);  // != b1
   h.fp = (hi >> 8) & 0xFFu;
   if (h.fp == 0) h.fp = 1;  // 0 marks an empty slot
   return h;
@@ -596,14 +595,22 @@ __device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, u
   }
 }
 
+// Some byte of x is zero: the borrow trick, exact for presence (not for which bytes).
+__device__ __forceinline__ bool any_zero_byte(unsigned long long x) {
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  return (((lo - 0x01010101u) & ~lo) | ((hi - 0x01010101u) & ~hi)) & 0x80808080u;
+}
+
 // Multiplicity of k in the table; `first` = slot id of its first copy (b1, then b2, then stash).
+// Fast path (almost every probe): no fingerprint byte of b1 matches and b1 is not full.
 __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long long k, uint32_t nstash,
                                                uint32_t &first) {
   const JoinHash h = join_hash(k);
   const unsigned long long pat = h.fp * 0x0101010101010101ull;
   const unsigned long long w1 = T.fp[h.b1];
-  uint32_t c = 0;
   first = 0xFFFFFFFFu;
+  if (!any_zero_byte(w1 ^ pat) && !bucket_full(w1)) return 0u;
+  uint32_t c = 0;
   count_in_bucket(T, h.b1, w1, pat, k, c, first);
   if (bucket_full(w1)) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
     const unsigned long long w2 = T.fp[h.b2];
