@@ -130,6 +130,13 @@ struct TileGenArgs {
   TileDesc *out;
 };
 void launch_tiles(const TileGenArgs &a, cudaStream_t st);
+
+// Bucket regions of one partitioned batch in its wave's scratch: buckets [b0, b0 + nb) of the launch;
+// bucket k's build region starts at base + k(cb + cp) (cb slots), its probe region right after (cp).
+struct BucketRun { uint32_t b0, nb, base, cb, cp, gid; };
+// Expands BucketRuns into the five per-bucket arrays (start build, start probe, cap build, cap probe,
+// batch id) at out, out + nbt, ..., out + 4 nbt.
+void launch_expand_buckets(const BucketRun *runs, uint32_t nruns, uint32_t *out, uint32_t nbt, cudaStream_t st);
 struct ScatterArgs {
   const uint32_t *comp[4];             // companion tables A, B, C, D
   uint32_t dpack[8];                   // d rows 1..m-1 packed, +0x8000 guard per half

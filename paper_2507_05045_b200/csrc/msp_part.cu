@@ -268,6 +268,26 @@ void launch_tiles(const TileGenArgs &a, cudaStream_t st) {
   k_tiles<<<blocks < 2368 ? blocks : 2368, 256, 0, st>>>(a);
 }
 
+// One block per batch: its buckets' region starts, capacities and batch id.
+__global__ void k_expand_buckets(const BucketRun *runs, uint32_t nruns, uint32_t *out, uint32_t nbt) {
+  for (uint32_t r = blockIdx.x; r < nruns; r += gridDim.x) {
+    const BucketRun R = runs[r];
+    for (uint32_t k = threadIdx.x; k < R.nb; k += blockDim.x) {
+      const uint32_t b = R.b0 + k, s0 = R.base + k * (R.cb + R.cp);
+      out[b] = s0;
+      out[nbt + b] = s0 + R.cb;
+      out[2 * nbt + b] = R.cb;
+      out[3 * nbt + b] = R.cp;
+      out[4 * nbt + b] = R.gid;
+    }
+  }
+}
+
+void launch_expand_buckets(const BucketRun *runs, uint32_t nruns, uint32_t *out, uint32_t nbt, cudaStream_t st) {
+  if (!nruns) return;
+  k_expand_buckets<<<nruns < 4096 ? nruns : 4096, 256, 0, st>>>(runs, nruns, out, nbt);
+}
+
 // ---------------------------------------------------------------- scatter (enumerate + hash + partition)
 
 __device__ __forceinline__ uint4 ld_tile(const TileDesc *t, uint32_t i, uint32_t n) {

@@ -81,7 +81,7 @@ struct Device {
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
   DBuf rkeys, runits, rfilt, rhits;
-  DBuf bfilt, bhits, bovf, scratch, bk, fill, zkeys, dbg;
+  DBuf bfilt, bhits, bovf, scratch, bk, bruns, fill, zkeys, dbg;
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
@@ -102,7 +102,7 @@ struct Device {
     DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err, &nitem, &ibase, &items, &ictr,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
-                   &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &fill, &cscratch[0], &cscratch[1],
+                   &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &bruns, &fill, &cscratch[0], &cscratch[1],
                    &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &scratch3, &fill3, &scratch4, &fill4, &tdesc, &gstb, &gsu, &uinfo,
                    &chunks, &cchunks, &l2chunks, &cctr, &cfirst, &ccfirst, &tchunks, &wdesc, &wctr, &tasks};
     for (DBuf *b : all) b->release();
@@ -568,6 +568,18 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   msp_stats &S = res->stats;
   std::vector<std::vector<uint8_t>> sols;
   const bool profile = opt->flags & MSP_FLAG_PROFILE;
+  // MSP_TIMELINE: host time and stream time of the solve's phase boundaries (GPU idle = gaps)
+  struct TLMark { const char *name; double host_ms; cudaEvent_t ev; };
+  std::vector<TLMark> tl;
+  const bool tl_on = getenv("MSP_TIMELINE") != nullptr;
+  auto hmark = [&](const char *name) {  // host-only timestamp
+    if (tl_on) fprintf(stderr, "[msp timeline]   %-16s host %8.3f ms\n", name, 1e3 * (now_s() - t0));
+  };
+  auto mark = [&](const char *name) {
+    if (!tl_on) return;
+    TLMark m{name, 1e3 * (now_s() - t0), nullptr};
+    if (cudaEventCreate(&m.ev) == cudaSuccess && cudaEventRecord(m.ev, st) == cudaSuccess) tl.push_back(m);
+  };
   const int bf_max = opt->brute_force_max_n < 0 ? 12 : opt->brute_force_max_n;
   auto emit = [&](void) -> int {
     res->n_solutions = (int64_t)sols.size();
@@ -600,6 +612,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   if (rc) return rc;
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.ev[1], st));
+  mark("plan done");
   S.t_build = now_s() - t0;
   S.peak_table_entries = 0;
   for (int t = 0; t < 4; ++t) S.peak_table_entries += (int64_t)1 << P.b[t];
@@ -873,7 +886,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       W.tasks = D.tasks.as<unsigned long long>();
       W.ntasks = (uint32_t)tasks.size();
       if (profile && timed) CK(cudaEventRecord(D.pev[0], st));
+      mark("k_waves launch");
       CK(launch_waves(P.mc, W, D.num_sms, st));
+      mark("k_waves returned");
       S.kernel_launches += 1;
       if (profile && timed) {
         CK(cudaEventRecord(D.pev[1], st));
@@ -936,7 +951,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     struct PWave { size_t u0, u1, b0, nb; uint64_t t0, ntiles, scratch, pairs; uint32_t g0, g1; };
     std::vector<PWave> pw;
     std::vector<UnitDesc> units;
-    std::vector<uint32_t> bstart[2], bcap[2], bgid;
+    std::vector<BucketRun> bruns;  // per batch: its buckets' regions (expanded on the device)
+    uint32_t nbt_all = 0;
     PWave cur{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     uint64_t cur_keys = 0;
     // tile list of every partitioned batch side, in (batch, side) order
@@ -947,7 +963,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       if (cur.nb == 0) return;
       cur.u1 = units.size();
       pw.push_back(cur);
-      cur = PWave{units.size(), units.size(), bgid.size(), 0, all_tiles, 0, 0, 0, 0, 0};
+      cur = PWave{units.size(), units.size(), nbt_all, 0, all_tiles, 0, 0, 0, 0, 0};
       cur_keys = 0;
     };
     for (uint32_t g : part_b) {
@@ -963,11 +979,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       const double mb = (double)nb / NB, mp = (double)np / NB;
       // capacities even: bucket regions start 16-byte aligned for the scatter's bulk copies
       const uint32_t cb = even_up(mb + 7.0 * std::sqrt(mb) + 16), cp = even_up(mp + 7.0 * std::sqrt(mp) + 16);
-      for (uint32_t k = 0; k < NB; ++k) {
-        bstart[0].push_back((uint32_t)cur.scratch); bcap[0].push_back(cb); cur.scratch += cb;
-        bstart[1].push_back((uint32_t)cur.scratch); bcap[1].push_back(cp); cur.scratch += cp;
-        bgid.push_back(g);
-      }
+      // bucket k of the batch: build region at base + k(cb + cp), probe region right after it
+      bruns.push_back(BucketRun{nbt_all, NB, (uint32_t)cur.scratch, cb, cp, g});
+      cur.scratch += (uint64_t)NB * (cb + cp);
+      nbt_all += NB;
       for (int side = 0; side < 2; ++side) {
         UnitDesc u = make_unit(P, g, side, 0);
         u.region_base = cur.nb;
@@ -986,11 +1001,12 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       cur_keys += nb + np;
     }
     flush();
+    hmark("waves packed");
     S.waves += (int32_t)pw.size();
     if (!pw.empty()) {
       uint64_t max_scratch = 0;
       for (const PWave &w : pw) max_scratch = std::max(max_scratch, w.scratch);
-      const size_t nbt = bgid.size();
+      const size_t nbt = nbt_all;
       rc = ensure_wave_buffers(max_scratch);
       if (rc) return rc;
       std::vector<UnitInfo> uinfo(units.size());
@@ -999,16 +1015,19 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(D.uinfo.ensure(sizeof(UnitInfo) * uinfo.size()));
       if (int ru_ = upload(D.uinfo.p, uinfo.data(), sizeof(UnitInfo) * uinfo.size())) return ru_;
       CK(D.bk.ensure(4 * 5 * nbt));
-      std::vector<uint32_t> bkimg;
-      bkimg.reserve(5 * nbt);
-      for (auto *v : {&bstart[0], &bstart[1], &bcap[0], &bcap[1], &bgid}) bkimg.insert(bkimg.end(), v->begin(), v->end());
-      if (int ru_ = upload(D.bk.p, bkimg.data(), 4 * bkimg.size())) return ru_;
+      CK(D.bruns.ensure(sizeof(BucketRun) * bruns.size()));
+      if (int ru_ = upload(D.bruns.p, bruns.data(), sizeof(BucketRun) * bruns.size())) return ru_;
+      launch_expand_buckets(D.bruns.as<BucketRun>(), (uint32_t)bruns.size(), D.bk.as<uint32_t>(), (uint32_t)nbt, st);
+      ++S.kernel_launches;
+      hmark("buckets uploaded");
       // per wave: each CTA's equal share of the wave's tiles, cut at unit boundaries
       const uint32_t nct = (uint32_t)D.num_sms * kScatterCtasHost;
       std::vector<unsigned long long> chimg;
       std::vector<uint32_t> cfirst;
       std::vector<size_t> choff, cfoff;
+      const bool per_wave = opt->flags & MSP_FLAG_WAVE_LAUNCHES;
       for (const PWave &w : pw) {
+        if (!per_wave) break;  // (static CTA chunks: per-wave launch path only)
         choff.push_back(chimg.size());
         cfoff.push_back(cfirst.size());
         std::vector<uint64_t> ub{0};
@@ -1021,6 +1040,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         for (uint32_t &x : f) x -= (uint32_t)choff.back();
         cfirst.insert(cfirst.end(), f.begin(), f.end());
       }
+      hmark("chunks built");
       CK(D.chunks.ensure(8 * std::max<size_t>(1, chimg.size())));
       if (int ru_ = upload(D.chunks.p, chimg.data(), 8 * chimg.size())) return ru_;
       CK(D.cfirst.ensure(4 * std::max<size_t>(1, cfirst.size())));
@@ -1038,6 +1058,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       tg.gs_tile_base = D.gstb.as<uint64_t>();
       tg.gs_unit = D.gsu.as<uint32_t>();
       tg.out = D.tdesc.as<TileDesc>();
+      mark("tiles launch");
       launch_tiles(tg, st);
       ++S.kernel_launches;
       const uint32_t *bkd = D.bk.as<uint32_t>();
@@ -1054,7 +1075,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
       ScatterArgs sa = scatter_base(P, A);
-      const bool per_wave = opt->flags & MSP_FLAG_WAVE_LAUNCHES;
       if (!per_wave) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
         std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
         std::vector<WaveDesc> wds(pw.size());
@@ -1406,6 +1426,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
 
   rc = join_streams();
   if (rc) return rc;
+  mark("joins queued");
 
   // ---- overflowed partitioned batches are re-joined with the global table
   unsigned long long n_v2_hits = 0;
@@ -1582,8 +1603,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       hv.insert(hv.end(), t2.begin(), t2.end());
     }
     hv.insert(hv.end(), zero_hits.begin(), zero_hits.end());
+    mark("recovery start");
     rc = recover(hv);
     if (rc) return rc;
+    mark("recovery done");
     if (opt->mode == MSP_MODE_ALL && recovered_hh != S.hash_hits) {
       set_err("internal error: recovered hash hits %lld != join hash hits %lld", (long long)recovered_hh,
               (long long)S.hash_hits);
@@ -1592,6 +1615,14 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   }
   CK(cudaEventRecord(D.ev[3], st));
   CK(cudaEventSynchronize(D.ev[3]));
+  for (const TLMark &m : tl) {
+    float g = 0;
+    cudaEventElapsedTime(&g, D.ev[0], m.ev);
+    fprintf(stderr, "[msp timeline] %-18s host %8.3f ms  stream %8.3f ms\n", m.name, m.host_ms, g);
+    cudaEventDestroy(m.ev);
+  }
+  if (tl_on) fprintf(stderr, "[msp timeline] %-18s host %8.3f ms  stream %8.3f ms\n", "end", 1e3 * (now_s() - t0),
+                     elapsed_ms(D.ev[0], D.ev[3]));
   if (dbg_stats) {
     unsigned long long dva[48];
     CK(cudaMemcpy(dva, dbg_stats, 3 * 128, cudaMemcpyDeviceToHost));
