@@ -306,7 +306,10 @@ def main() -> int:
         "traffic": None,
     }
     try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/README.md)
-        with open(os.path.join(HERE, "profiles", "r1f_kernels.json")) as fh:
+        import glob
+        caps = sorted(glob.glob(os.path.join(HERE, "profiles", "r*_kernels.json")),
+                      key=lambda f: (len(os.path.basename(f)), os.path.basename(f)))  # latest capture
+        with open(caps[-1]) as fh:
             tr = json.load(fh)["traffic"]
         roofline["traffic"] = {"dram_bytes_per_launch": tr["launch_dram_bytes"],
                                "algorithmic_bytes_per_launch": tr["algorithmic_bytes_per_launch"],
