@@ -872,6 +872,11 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     for (size_t s0 = 0; s0 < wds.size() && !stopped; s0 += seg) {
       const size_t s1 = std::min(wds.size(), s0 + seg);
       std::vector<unsigned long long> tasks;  // S(s0) S(s0+1) S(s0+2) J(s0) S(s0+3) J(s0+1) ... J(s1-1)
+      {
+        size_t nt = 0;
+        for (size_t w = s0; w < s1; ++w) nt += wds[w].nchunks + (wds[w].nb + kJoinGroup - 1) / kJoinGroup;
+        tasks.reserve(nt);
+      }
       auto push_join = [&](size_t w) {
         for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks.push_back((1ull << 63) | ((unsigned long long)w << 32) | b);
       };
@@ -1077,6 +1082,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       ScatterArgs sa = scatter_base(P, A);
       if (!per_wave) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
         std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
+        tch.reserve(all_tiles / kTaskTiles + units.size());
         std::vector<WaveDesc> wds(pw.size());
         for (size_t wi = 0; wi < pw.size(); ++wi) {
           const PWave &w = pw[wi];
