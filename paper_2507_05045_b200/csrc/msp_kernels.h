@@ -170,7 +170,10 @@ cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 
 // Persistent pipeline of partitioned waves (msp_part.cu k_waves): scatter chunks of wave w + 1 and
 // join bucket groups of wave w from one task queue, one CTA per SM.
-constexpr uint32_t kJoinGroup = 6;     // buckets per join task
+#ifndef MSP_JOIN_GROUP
+#define MSP_JOIN_GROUP 6
+#endif
+constexpr uint32_t kJoinGroup = MSP_JOIN_GROUP;  // buckets per join task
 constexpr uint32_t kWaveBuffers = 4;   // scratch buffers of the pipeline
 constexpr uint32_t kWaveLookahead = 2; // task order S(w + 2) J(w): joins trail scatters by 2 waves
 struct WaveDesc {

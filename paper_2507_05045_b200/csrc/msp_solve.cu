@@ -531,7 +531,17 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 uint32_t even_up(double x) { const uint32_t v = (uint32_t)x; return v + (v & 1u); }
 
 constexpr uint32_t kChunkCounters = 1u << 16;
-constexpr uint64_t kTaskTiles = 96;  // tiles per scatter task of the persistent wave pipeline
+// Tiles per scatter task of the persistent wave pipeline: a wave's tiles over about one task per SM
+// (fewer, longer tasks: fewer partial rounds and task switches, every SM still scatters the wave),
+// at least kTaskTilesMin.  MSP_TASK_TILES fixes it (tuning).
+#ifndef MSP_TASK_TILES
+#define MSP_TASK_TILES 0
+#endif
+constexpr uint64_t kTaskTiles = MSP_TASK_TILES;
+constexpr uint64_t kTaskTilesMin = 96;
+#ifndef MSP_TASKS_PER_SM
+#define MSP_TASKS_PER_SM 1
+#endif
 
 // Static split of a launch's tiles (units given as consecutive tile ranges [ub[i], ub[i+1])) over
 // `nct` CTAs: CTA b gets tiles [b*T/nct, (b+1)*T/nct), cut at unit boundaries into chunks.
@@ -1082,7 +1092,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       ScatterArgs sa = scatter_base(P, A);
       if (!per_wave) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
         std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
-        tch.reserve(all_tiles / kTaskTiles + units.size());
+        tch.reserve(all_tiles / kTaskTilesMin + units.size());
         std::vector<WaveDesc> wds(pw.size());
         for (size_t wi = 0; wi < pw.size(); ++wi) {
           const PWave &w = pw[wi];
@@ -1090,10 +1100,13 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
           wd.tile0 = (uint32_t)w.t0;
           wd.chunk0 = (uint32_t)tch.size();
           uint64_t t = 0;
+          const uint64_t ntask = (uint64_t)D.num_sms * MSP_TASKS_PER_SM;
+          const uint64_t tt = kTaskTiles ? kTaskTiles
+                                         : std::min<uint64_t>(0xFFFF, std::max(kTaskTilesMin, (w.ntiles + ntask - 1) / ntask));
           for (size_t i = w.u0; i < w.u1; ++i) {
             const uint64_t nt = P.tiles[2 * (size_t)units[i].gid + units[i].side];
-            for (uint64_t k = 0; k < nt; k += kTaskTiles) {
-              const uint64_t c = std::min<uint64_t>(kTaskTiles, nt - k);
+            for (uint64_t k = 0; k < nt; k += tt) {
+              const uint64_t c = std::min<uint64_t>(tt, nt - k);
               tch.push_back((t + k) | (c << 32) | ((unsigned long long)(i - w.u0) << 48));
             }
             t += nt;
