@@ -81,7 +81,12 @@ void launch_rects(const RectArgs &a, uint32_t max_groups, cudaStream_t st);
 void launch_brute(const BruteArgs &a, cudaStream_t st);
 
 // Partitioned join (msp_part.cu).  Buckets of one wave, per role (0 = build, 1 = probe).
-constexpr int kMaxWaveBuckets = 1024;  // buckets per role per wave
+#ifndef MSP_MAX_WAVE_BUCKETS
+#define MSP_MAX_WAVE_BUCKETS 2048
+#endif
+constexpr int kMaxWaveBuckets = MSP_MAX_WAVE_BUCKETS;  // buckets per role per wave (ebase: 12 bits)
+constexpr int kMaxUnitBuckets = 1024;  // buckets of one batch side (stage entries; UnitInfo: 11 bits)
+static_assert(2 * kMaxWaveBuckets <= 4096 && kMaxUnitBuckets < 2048, "UnitInfo.ent field widths");
 #ifndef MSP_SCATTER_CTAS
 #define MSP_SCATTER_CTAS 1
 #endif

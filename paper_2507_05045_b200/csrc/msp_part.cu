@@ -43,7 +43,7 @@ constexpr int kStageKeys = kScatterStageKeys;                   // stage slots o
 #endif
 constexpr int kOvf = MSP_OVF_KEYS;                              // keys ranked past their entry's C slots
 constexpr int kOvfTrigger = kOvf * 3 / 8;                       // a round ends at this many (default)
-constexpr int kMaxNB = kMaxWaveBuckets;                         // entries of one unit
+constexpr int kMaxNB = kMaxUnitBuckets;                         // entries of one unit
 constexpr uint32_t kDrop = 0xFFFFFFFFu;
 #ifndef MSP_RESCATTER_N
 #define MSP_RESCATTER_N 4

@@ -341,7 +341,7 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   for (size_t i = 0; i < 2 * (size_t)P.G; ++i) {
     const size_t g = i / 2;  // items only for batches the partitioned waves can hold
     const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
-    const bool fits = nb + np <= item_key_budget && ((nb + kBucketTarget - 1) / kBucketTarget) <= (uint64_t)kMaxWaveBuckets;
+    const bool fits = nb + np <= item_key_budget && ((nb + kBucketTarget - 1) / kBucketTarget) <= (uint64_t)kMaxUnitBuckets;
     P.item_base[i + 1] = P.item_base[i] + (fits ? nitem[i] : 0u);
   }
   CK(D.items.ensure(8 * std::max<uint64_t>(P.item_base.back(), 1)));
@@ -955,7 +955,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     const uint64_t nbk = std::max<uint64_t>(1, (nb + kBucketTarget - 1) / kBucketTarget);
     if (opt->flags & MSP_FLAG_JOIN_GLOBAL)
       global_b.push_back(g);
-    else if (nbk > (uint64_t)wave_buckets || nb + np > key_budget)
+    else if (nbk > (uint64_t)std::min<uint32_t>(wave_buckets, kMaxUnitBuckets) || nb + np > key_budget)
       huge_b.push_back(g);
     else
       part_b.push_back(g);
@@ -1304,7 +1304,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       }
       // level 2 waves over the coarse buckets
       const uint32_t NF = (uint32_t)std::max<uint64_t>(1, (uint64_t)std::ceil(mb / kBucketTarget));
-      if (NF > (uint32_t)kMaxWaveBuckets) { set_err("coarse bucket too large for one level-2 wave"); return MSP_UNSUPPORTED; }
+      if (NF > (uint32_t)kMaxUnitBuckets) { set_err("coarse bucket too large for one level-2 wave"); return MSP_UNSUPPORTED; }
       const double fmb = mb / NF, fmp = mp / NF;
       const uint32_t fcb = even_up(fmb + 7.0 * std::sqrt(fmb) + 16), fcp = even_up(fmp + 7.0 * std::sqrt(fmp) + 16);
       struct L2Wave { size_t s0, ns, b0, nb; uint64_t total, scratch; };
