@@ -84,9 +84,9 @@ void launch_brute(const BruteArgs &a, cudaStream_t st);
 #ifndef MSP_MAX_WAVE_BUCKETS
 #define MSP_MAX_WAVE_BUCKETS 2048
 #endif
-constexpr int kMaxWaveBuckets = MSP_MAX_WAVE_BUCKETS;  // buckets per role per wave (ebase: 12 bits)
+constexpr int kMaxWaveBuckets = MSP_MAX_WAVE_BUCKETS;  // buckets per role per wave (ebase: 13 bits)
 constexpr int kMaxUnitBuckets = 1024;  // buckets of one batch side (stage entries; UnitInfo: 11 bits)
-static_assert(2 * kMaxWaveBuckets <= 4096 && kMaxUnitBuckets < 2048, "UnitInfo.ent field widths");
+static_assert(2 * kMaxWaveBuckets <= 8192 && kMaxUnitBuckets < 2048, "UnitInfo.ent field widths");
 #ifndef MSP_SCATTER_CTAS
 #define MSP_SCATTER_CTAS 1
 #endif
@@ -117,7 +117,7 @@ constexpr uint32_t kSinkSlots = 64;    // scratch slack past the last region
 constexpr int kMaxUnits = 128;         // units per scatter launch (64 batches per wave)
 struct UnitInfo {
   uint32_t h0lo, h0hi;                 // FNV state after coordinate 0 (alpha)
-  uint32_t ent;                        // first (role, bucket) entry | buckets NB << 12 | side << 23
+  uint32_t ent;                        // first (role, bucket) entry | buckets NB << 13 | side << 24
                                        // (bucket of a key = floor(hi32 * NB / 2^32))
   uint32_t gid;                        // batch index within the solve
 };

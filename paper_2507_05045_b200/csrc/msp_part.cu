@@ -360,7 +360,7 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
 #pragma unroll
     for (int u = 0; u < kUS; ++u) dacc ^= ok[u] ? key[u] : 0ull;
   } else {
-    stage_keys<kUS>(g, S, ui.ent & 0xFFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, nbk * C * 7 / 8,
+    stage_keys<kUS>(g, S, ui.ent & 0x1FFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, nbk * C * 7 / 8,
                    key, j, ok);
   }
 }
@@ -378,7 +378,7 @@ __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const Sc
   constexpr int SW = stride_for(MC);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   volatile uint32_t *round_end = &g.round_end;
-  const uint32_t ebase = ui.ent & 0xFFFu, nbk = (ui.ent >> 12) & 0x7FFu, side = (ui.ent >> 23) & 1u;
+  const uint32_t ebase = ui.ent & 0x1FFFu, nbk = (ui.ent >> 13) & 0x7FFu, side = (ui.ent >> 24) & 1u;
   const bool right = side != 0;
   uint32_t C, cmagic;
   stage_geometry(nbk, C, cmagic);

@@ -401,7 +401,7 @@ UnitInfo make_info(const UnitDesc &u, uint32_t nb) {
   i.h0lo = (uint32_t)u.h0;
   i.h0hi = (uint32_t)(u.h0 >> 32);
   const uint32_t ebase = ((u.flags >> 1) & 1u) * nb + u.region_base;
-  i.ent = ebase | (u.region_log2 << 12) | (u.side << 23);
+  i.ent = ebase | (u.region_log2 << 13) | (u.side << 24);  // 13 | 11 | 1 bits
   i.gid = u.gid;
   return i;
 }
