@@ -180,7 +180,11 @@ cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st);
 #endif
 constexpr uint32_t kJoinGroup = MSP_JOIN_GROUP;  // buckets per join task
 constexpr uint32_t kWaveBuffers = 4;   // scratch buffers of the pipeline
-constexpr uint32_t kWaveLookahead = 2; // task order S(w + 2) J(w): joins trail scatters by 2 waves
+#ifndef MSP_WAVE_LOOKAHEAD
+#define MSP_WAVE_LOOKAHEAD 2
+#endif
+constexpr uint32_t kWaveLookahead = MSP_WAVE_LOOKAHEAD;  // task order S(w + 2) J(w): joins trail scatters by 2 waves
+static_assert(kWaveLookahead + 1 <= kWaveBuffers, "S(w + L) must follow J(w - 1) in the queue");
 struct WaveDesc {
   uint32_t tile0;                      // first tile of the wave in the tile array
   uint32_t chunk0, nchunks;            // its scatter chunks (wave-relative tiles) in the chunk array
