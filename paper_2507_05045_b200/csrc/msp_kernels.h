@@ -96,7 +96,13 @@ constexpr int kScatterCtasHost = MSP_SCATTER_CTAS;  // resident k_scatter CTAs p
 #endif
 constexpr int kScatterStageKeys = MSP_STAGE_KEYS;  // stage slots of a scatter CTA
 constexpr int kJoinSlotsLog2 = 14;     // shared-memory join table: 16K (key, count) slots
-constexpr uint32_t kBucketTarget = 1u << (kJoinSlotsLog2 - 1);  // mean build keys per bucket
+#ifndef MSP_BUCKET_TARGET
+#define MSP_BUCKET_TARGET 6144u
+#endif
+constexpr uint32_t kBucketTarget = MSP_BUCKET_TARGET;  // mean build keys per bucket (16K-slot table: load 3/8; 4K/5K/8K/10K/12K measured slower)
+// Largest mean per bucket (table load 1/2): a batch side whose build keys need more than
+// kMaxUnitBuckets buckets of this size takes the two-level path, whose fine buckets use this size.
+constexpr uint32_t kBucketTargetMax = 1u << (kJoinSlotsLog2 - 1);
 struct PartArgs {
   unsigned long long *scratch;
   const uint32_t *start[2];   // bucket region start in scratch

@@ -341,7 +341,7 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   for (size_t i = 0; i < 2 * (size_t)P.G; ++i) {
     const size_t g = i / 2;  // items only for batches the partitioned waves can hold
     const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
-    const bool fits = nb + np <= item_key_budget && ((nb + kBucketTarget - 1) / kBucketTarget) <= (uint64_t)kMaxUnitBuckets;
+    const bool fits = nb + np <= item_key_budget && ((nb + kBucketTargetMax - 1) / kBucketTargetMax) <= (uint64_t)kMaxUnitBuckets;
     P.item_base[i + 1] = P.item_base[i] + (fits ? nitem[i] : 0u);
   }
   CK(D.items.ensure(8 * std::max<uint64_t>(P.item_base.back(), 1)));
@@ -952,7 +952,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   std::vector<uint32_t> part_b, huge_b, global_b;
   for (uint32_t g = 0; g < P.G; ++g) {
     const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
-    const uint64_t nbk = std::max<uint64_t>(1, (nb + kBucketTarget - 1) / kBucketTarget);
+    const uint64_t nbk = std::max<uint64_t>(1, (nb + kBucketTargetMax - 1) / kBucketTargetMax);
     if (opt->flags & MSP_FLAG_JOIN_GLOBAL)
       global_b.push_back(g);
     else if (nbk > (uint64_t)std::min<uint32_t>(wave_buckets, kMaxUnitBuckets) || nb + np > key_budget)
@@ -984,7 +984,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     for (uint32_t g : part_b) {
       const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
       const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
-      const uint32_t NB = (uint32_t)std::max<uint64_t>(1, (nb + kBucketTarget - 1) / kBucketTarget);
+      const uint32_t NB = (uint32_t)std::max<uint64_t>(  // <= kMaxUnitBuckets by the classification
+          1, std::min<uint64_t>(std::min<uint32_t>(wave_buckets, kMaxUnitBuckets), (nb + kBucketTarget - 1) / kBucketTarget));
       if (cur.nb + NB > wave_buckets || cur_keys + nb + np > key_budget ||
           (cur.nb && g != cur.g1) ||  // waves hold consecutive batches (contiguous tile ranges)
           units.size() - cur.u0 + 2 > (size_t)kMaxUnits) {
@@ -1303,7 +1304,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         S.kernel_launches += 2;
       }
       // level 2 waves over the coarse buckets
-      const uint32_t NF = (uint32_t)std::max<uint64_t>(1, (uint64_t)std::ceil(mb / kBucketTarget));
+      const uint32_t NF = (uint32_t)std::max<uint64_t>(1, (uint64_t)std::ceil(mb / kBucketTargetMax));
       if (NF > (uint32_t)kMaxUnitBuckets) { set_err("coarse bucket too large for one level-2 wave"); return MSP_UNSUPPORTED; }
       const double fmb = mb / NF, fmp = mp / NF;
       const uint32_t fcb = even_up(fmb + 7.0 * std::sqrt(fmb) + 16), fcp = even_up(fmp + 7.0 * std::sqrt(fmp) + 16);
