@@ -48,8 +48,10 @@ enum msp_flags {
   MSP_FLAG_JOIN_GLOBAL = 1u << 2,  /* force the global-hash-table join (fallback path) */
   MSP_FLAG_DIAG_HASH_ONLY = 1u << 3, /* diagnostic timing: global path kernels hash but do not join
                                        (results invalid; never set in a real solve) */
-  MSP_FLAG_WAVE_LAUNCHES = 1u << 4  /* partitioned waves as per-wave scatter + join launches instead
+  MSP_FLAG_WAVE_LAUNCHES = 1u << 4, /* partitioned waves as per-wave scatter + join launches instead
                                        of the persistent pipeline (parity testing) */
+  MSP_FLAG_BATCH_STATS = 1u << 5    /* fill msp_result.batch_stats: one row per batch, the per-batch
+                                       ValidationStats of validate_chunked (validate.py:63-71,316-379) */
 };
 
 typedef struct {
@@ -78,7 +80,9 @@ typedef struct {
   int64_t batches, candidates_left, candidates_right, filtered_residuals, hash_hits, exact_hits;
   uint64_t row1_pairs_lo, row1_pairs_hi; /* sum over batches of n_left*n_right (128-bit) */
   int64_t peak_table_entries, peak_heap1, peak_heap2;
-  double t_build, t_enumerate, t_validate, t_total; /* host wall seconds */
+  double t_build, t_enumerate, t_validate, t_total; /* host wall seconds: t_build = K1 quarter tables
+                              (incl. t_init), t_enumerate = the alpha plan (replaces the heap stream),
+                              t_validate = join waves + recovery + confirmation */
   int32_t fallback;  /* 0 none, 1 brute-force */
   int32_t waves;     /* join waves executed */
   int64_t kernel_launches; /* kernels this call launched */
@@ -91,6 +95,8 @@ typedef struct {
   int64_t hot_bytes;       /* algorithmic HBM/L2 bytes of those launches */
   int32_t cancelled;       /* 1: stopped early by msp_options.cancel (counters are partial) */
   int32_t reserved;
+  double t_init;           /* host seconds of one-time CUDA init inside this call (context + device
+                              state of a first call on the device; 0 afterwards) */
 } msp_stats;
 
 typedef struct {
@@ -98,6 +104,9 @@ typedef struct {
   int32_t n;               /* solution length */
   uint8_t *xbits;          /* n_solutions x n, 0/1, unsorted (host sorts by solution_encoding) */
   msp_stats stats;
+  int64_t n_batch_stats;   /* MSP_FLAG_BATCH_STATS: rows of batch_stats (= stats.batches), else 0 */
+  int64_t *batch_stats;    /* n_batch_stats x 5, alpha-ascending: (alpha, n_left, n_right,
+                              filtered_residuals, hash_hits) of each batch of the stream */
 } msp_result;
 
 /* Full solve of one instance (or of the alpha band of one shard).  Blocking. */

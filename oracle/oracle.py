@@ -18,8 +18,8 @@ LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(HERE, "msp_oracle.c")
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+    srcs = [os.path.join(HERE, f) for f in ("msp_oracle.c", "msp_oracle_groups.cc", "Makefile")]
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(map(os.path.getmtime, srcs)):
         subprocess.check_call(["make", "-s", "-C", HERE])
     return LIB_PATH
 
@@ -64,6 +64,15 @@ class Result(C.Structure):
     ]
 
 
+class GroupResult(C.Structure):
+    _fields_ = [
+        ("n_left", C.c_int64), ("n_right", C.c_int64), ("filtered", C.c_int64),
+        ("hash_hits", C.c_int64), ("exact_hits", C.c_int64), ("passes", C.c_int64),
+        ("n_hit_keys", C.c_int64), ("hit_keys", C.POINTER(C.c_uint64)),
+        ("n_solutions", C.c_int64), ("xbits", C.POINTER(C.c_uint8)),
+    ]
+
+
 _lib = None
 
 
@@ -90,6 +99,10 @@ def lib():
         L.oracle_stream.restype = C.c_int64
         L.oracle_stream.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                     C.c_int64, C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_int64)]
+        L.oracle_alpha_group.restype = C.c_int
+        L.oracle_alpha_group.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                         C.c_uint64, C.c_int, C.c_int, C.POINTER(GroupResult)]
+        L.oracle_group_result_free.argtypes = [C.POINTER(GroupResult)]
         _lib = L
     return _lib
 
@@ -196,4 +209,27 @@ def stream(a, d):
         lp = pairs[pos:pos + nl].tolist(); pos += nl
         rp = pairs[pos:pos + nr].tolist(); pos += nr
         out.append((al, be, lp, rp))
+    return out
+
+
+def alpha_group(a, d, alpha: int, threads: int = 0, passes: int = 0) -> dict:
+    """One alpha-group (batch) of the instance through the streaming CPU restatement
+    (msp_oracle_groups.cc): validate_chunked's per-batch counters + solutions, for batches too big
+    to materialise.  Keys: n_left, n_right, filtered, hash_hits, exact_hits, hit_keys, solutions."""
+    a = _u64(a)
+    d = _u64(d)
+    m, n = a.shape
+    res = GroupResult()
+    rc = lib().oracle_alpha_group(m, n, _ptr(a), _ptr(d), alpha, threads, passes, C.byref(res))
+    try:
+        if rc:
+            raise ValueError("oracle_alpha_group failed")
+        ns = res.n_solutions
+        xb = np.ctypeslib.as_array(res.xbits, shape=(ns * n,)).reshape(ns, n).copy() if ns else np.zeros((0, n), np.uint8)
+        keys = (np.ctypeslib.as_array(res.hit_keys, shape=(res.n_hit_keys,)).tolist() if res.n_hit_keys else [])
+        out = {k: int(getattr(res, k)) for k in ("n_left", "n_right", "filtered", "hash_hits", "exact_hits", "passes")}
+    finally:
+        lib().oracle_group_result_free(C.byref(res))
+    out["hit_keys"] = [int(k) for k in keys]
+    out["solutions"] = sorted("".join(str(int(v)) for v in row) for row in xb)
     return out

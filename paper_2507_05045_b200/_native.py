@@ -27,6 +27,7 @@ MSP_FLAG_FORCE_TABLE_PATH = 1 << 1
 MSP_FLAG_JOIN_GLOBAL = 1 << 2
 MSP_FLAG_DIAG_HASH_ONLY = 1 << 3
 MSP_FLAG_WAVE_LAUNCHES = 1 << 4
+MSP_FLAG_BATCH_STATS = 1 << 5
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -60,11 +61,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     if not os.path.exists(nvcc):
         nvcc = "nvcc"
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+
     tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-shared", "-o", tmp, *srcs]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    with tempfile.TemporaryDirectory(prefix="msp_build_") as td:
+        objs = [os.path.join(td, os.path.basename(f) + ".o") for f in srcs]
+        cmds = [[nvcc, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", "-o", o, f] for f, o in zip(srcs, objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c), file=sys.stderr)
+        with ThreadPoolExecutor(max_workers=len(cmds)) as ex:  # one nvcc per translation unit
+            for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+                f.result()
+        subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -101,13 +111,14 @@ class Stats(C.Structure):
         ("dev_ms_total", C.c_double), ("dev_ms_tables", C.c_double), ("dev_ms_join", C.c_double),
         ("dev_ms_hot", C.c_double), ("hot_launches", C.c_int64), ("hot_pairs", C.c_int64),
         ("hot_bytes", C.c_int64),
-        ("cancelled", C.c_int32), ("reserved", C.c_int32),
+        ("cancelled", C.c_int32), ("reserved", C.c_int32), ("t_init", C.c_double),
     ]
 
 
 class Result(C.Structure):
     _fields_ = [("n_solutions", C.c_int64), ("n", C.c_int32),
-                ("xbits", C.POINTER(C.c_uint8)), ("stats", Stats)]
+                ("xbits", C.POINTER(C.c_uint8)), ("stats", Stats),
+                ("n_batch_stats", C.c_int64), ("batch_stats", C.POINTER(C.c_int64))]
 
 
 _lib = None
@@ -189,6 +200,10 @@ def solve_raw(a, d, opts: Options, alpha: int | None = None):
               if ns else np.zeros((0, n), np.uint8))
         st = {name: getattr(res.stats, name) for name, _ in Stats._fields_}
         st["row1_candidate_pairs"] = (st.pop("row1_pairs_hi") << 64) | st.pop("row1_pairs_lo")
+        nb = res.n_batch_stats if rc == MSP_OK else 0
+        if nb:  # (alpha, n_left, n_right, filtered_residuals, hash_hits) per batch
+            st["batch_stats"] = [tuple(int(v) for v in row) for row in
+                                 np.ctypeslib.as_array(res.batch_stats, shape=(nb * 5,)).reshape(nb, 5)]
     finally:
         L.msp_result_free(C.byref(res))
     return rc, xb, st
@@ -199,14 +214,17 @@ def alpha_plan(a, d, device: int = 0):
     L = load()
     pa = _ProblemArrays(a, d)
     cap = 1 << 16
-    bufs = [np.zeros(cap, np.uint64) for _ in range(4)]
-    ptrs = [b.ctypes.data_as(C.POINTER(C.c_uint64)) for b in bufs]
-    nb = L.msp_alpha_plan(C.byref(pa.prob), device, cap, *ptrs)
-    if nb < 0:
-        raise RuntimeError(f"msp_alpha_plan failed ({-nb}): {last_error()}")
-    if nb > cap:
-        raise RuntimeError("too many batches for the plan buffer")
-    return [tuple(int(b[i]) for b in bufs) for i in range(nb)]
+    while True:
+        bufs = [np.zeros(cap, np.uint64) for _ in range(4)]
+        ptrs = [b.ctypes.data_as(C.POINTER(C.c_uint64)) for b in bufs]
+        nb = L.msp_alpha_plan(C.byref(pa.prob), device, cap, *ptrs)
+        if nb < 0:
+            raise RuntimeError(f"msp_alpha_plan failed ({-nb}): {last_error()}")
+        if nb <= cap:
+            break
+        cap = nb  # msp_alpha_plan returns the true count: retry with room for every batch
+    cols = [b[:nb].tolist() for b in bufs]
+    return list(zip(*cols))
 
 
 def build_tables(a, d, device: int = 0):

@@ -77,10 +77,6 @@ struct RectDesc {
   __device__ __forceinline__ uint32_t gs() const { return gs_x >> 1; }
 };
 
-// Work item: up to kItemTiles consecutive warp tiles of one rectangle, packed in 64 bits:
-// rectangle index (32) | first tile within the rectangle (24) | tile count (8).
-constexpr uint32_t kItemTiles = 1;
-
 struct EnumArgs {
   TableDev tab[4];
   YRuns yr[2];               // [0] = B runs, [1] = D runs
@@ -91,10 +87,6 @@ struct EnumArgs {
   uint64_t chunk_tiles;      // tiles per warp work item
   uint64_t nchunks;
   uint32_t dpack[8];         // d rows 1..m-1 packed, +0x8000 guard per half (right side)
-  const uint64_t *items;     // work items of all (batch, side), grouped by gs = 2*batch + side
-  uint64_t item_lo, item_hi; // this launch's item range
-  uint32_t gs_base;          // units[gs - gs_base] describes the unit of an item's rectangle
-  unsigned long long *item_ctr;  // dynamic item counter of this launch (zeroed per solve)
   uint32_t diag;             // MSP_FLAG_DIAG_HASH_ONLY: hash without staging (timing only)
   unsigned long long *batch_filtered; // per batch (gid)
   unsigned long long *batch_hits;     // per batch (gid)

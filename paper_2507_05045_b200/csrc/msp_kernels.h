@@ -46,9 +46,8 @@ struct RectSide {
 };
 struct RectArgs {
   RectSide s[2]; const uint64_t *alpha; uint64_t target; const uint32_t *count;
-  unsigned long long *tiles; uint32_t *nrect; uint32_t *nitem;  // count mode outputs, per (batch, side)
+  unsigned long long *tiles; uint32_t *nrect;  // count mode outputs, per (batch, side)
   const uint32_t *rect_base; RectDesc *rects;  // write mode (rects != nullptr)
-  const uint64_t *item_base; uint64_t *items;  // write mode: work items (kItemTiles tiles each)
   int *err;
 };
 

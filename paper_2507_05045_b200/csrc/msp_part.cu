@@ -20,7 +20,10 @@
 // table path (msp_enum.cu), so results never depend on the partitioning.
 #include <cstdint>
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <type_traits>
+#include <utility>
 #include "msp_common.cuh"
 #include "msp_kernels.h"
 #include "msp_tile.cuh"
@@ -858,15 +861,24 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
   if (dacc == 0x123456789ull) W.sc.batch_filtered[0] = dacc;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel): the attribute belongs
+// to each device's context, so a process that solves on several devices must set it on each.
+cudaError_t smem_attr(const void *fn, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void *>> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, fn})) return cudaSuccess;
+  if (cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)) return e;
+  done.insert({dev, fn});
+  return cudaSuccess;
+}
+
 template <int MC>
 static cudaError_t launch_scatter_mc(const ScatterArgs &a, const PartArgs &p, int grid, cudaStream_t st) {
-  static bool configured = false;
   const size_t sm = scatter_smem_bytes(stride_for(MC));
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_scatter<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = smem_attr((const void *)k_scatter<MC>, sm)) return e;
   k_scatter<MC><<<grid, kScatterThreads, sm, st>>>(a, p);
   return cudaGetLastError();
 }
@@ -887,13 +899,8 @@ cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, i
 
 template <int MC>
 static cudaError_t launch_waves_mc(const WavesArgs &w, int grid, cudaStream_t st) {
-  static bool configured = false;
   const size_t sm = std::max(scatter_smem_bytes(stride_for(MC)), sizeof(JoinSmem));
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_waves<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = smem_attr((const void *)k_waves<MC>, sm)) return e;
   k_waves<MC><<<grid, kScatterThreads, sm, st>>>(w);
   return cudaGetLastError();
 }
@@ -911,13 +918,8 @@ cudaError_t launch_waves(int mc, const WavesArgs &w, int num_sms, cudaStream_t s
 }
 
 cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st) {
-  static bool configured = false;
   const size_t sm = sizeof(Stage);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_rescatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = smem_attr((const void *)k_rescatter, sm)) return e;
   if (!r.nchunks) return cudaSuccess;
   const uint32_t slots = (uint32_t)num_sms * kScatterCtas;
   const int grid = (int)(r.nchunks < slots ? r.nchunks : slots);
@@ -926,13 +928,8 @@ cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_
 }
 
 cudaError_t launch_join(const PartArgs &p, int num_sms, cudaStream_t st) {
-  static bool configured = false;
   const size_t sm = join_smem_bytes();
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  if (cudaError_t e = smem_attr((const void *)k_join, sm)) return e;
   if (p.nb == 0) return cudaSuccess;
   const uint32_t grid = p.nb < (uint32_t)num_sms ? p.nb : (uint32_t)num_sms;
   k_join<<<grid, kJoinThreads, sm, st>>>(p);

@@ -76,7 +76,7 @@ struct Device {
   DBuf a, d;
   DBuf tw[4], tm[4], tw2[4], tm2[4], comp[4], rs[4], re[4];
   DBuf yw[2], ys[2], yl[2], yn;
-  DBuf hl, hr, galpha, gnl, gnr, gcount, rects, nrect, rbase, tiles, err, nitem, ibase, items, ictr;
+  DBuf hl, hr, galpha, gnl, gnr, gcount, rects, nrect, rbase, tiles, err;
   DBuf units, ufilt, uhits;
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
@@ -84,6 +84,7 @@ struct Device {
   DBuf bfilt, bhits, bovf, scratch, bk, bruns, fill, zkeys, dbg;
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
+  uint64_t hit_cap = 0;  // distinct hit keys the hit list holds (grown on overflow, fastval.py:126-139)
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
   DBuf scratch2, fill2, scratch3, fill3, scratch4, fill4;
@@ -99,7 +100,7 @@ struct Device {
     if (ring) cudaFreeHost(ring);
     ring = nullptr;
     ring_cap = ring_off = 0;
-    DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err, &nitem, &ibase, &items, &ictr,
+    DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
                    &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &bruns, &fill, &cscratch[0], &cscratch[1],
@@ -115,14 +116,16 @@ struct Device {
 std::mutex g_devices_mu;
 std::map<int, Device *> g_devices;
 
-int get_device(int dev, Device **out) {
+int get_device(int dev, Device **out, double *t_init = nullptr) {
   std::lock_guard<std::mutex> lk(g_devices_mu);
   auto it = g_devices.find(dev);
   if (it != g_devices.end()) { *out = it->second; return MSP_OK; }
+  const double t0 = now_s();
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (dev < 0 || dev >= ndev) { set_err("device %d out of range (%d devices)", dev, ndev); return MSP_INVALID_ARGUMENT; }
   CK(cudaSetDevice(dev));
+  CK(cudaFree(nullptr));  // create the primary context now (its cost is reported as t_init)
   Device *D = new Device();
   D->dev = dev;
   CK(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
@@ -135,6 +138,7 @@ int get_device(int dev, Device **out) {
   CK(cudaEventCreateWithFlags(&D->ev_x, cudaEventDisableTiming));
   g_devices[dev] = D;
   *out = D;
+  if (t_init) *t_init = now_s() - t0;
   return MSP_OK;
 }
 
@@ -164,7 +168,6 @@ struct Plan {
   uint32_t G = 0;
   std::vector<uint64_t> alpha, nl, nr, tiles;  // tiles[2g + side]
   std::vector<uint32_t> rect_base, nrect;      // [2g + side]
-  std::vector<uint64_t> item_base;             // [2g + side], + total
   EnumArgs base{};
   int merge_w_cur[4] = {0, 0, 0, 0};  // which ping-pong buffer holds the final table
 };
@@ -207,7 +210,7 @@ int check_instance(const msp_problem *pr, Plan &P) {
 
 // K1 + K2 on the device; ends with the batch list and tile totals on the host.
 int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uint64_t alpha_hi,
-               cudaStream_t st, int64_t &launches, uint64_t item_key_budget = kDefaultWaveKeys) {
+               cudaStream_t st, int64_t &launches, double *t_tables = nullptr) {
   const int m = P.m, n = P.n;
   CK(D.a.ensure(sizeof(uint64_t) * m * n));
   CK(D.d.ensure(sizeof(uint64_t) * m));
@@ -260,6 +263,10 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   launch_pack(pa, maxsize, st);
   launch_runs(ra, maxsize, st);
   launches += 2;
+  if (t_tables) {  // K1 done: the stats split t_build (tables) from t_enumerate (the plan)
+    CK(cudaStreamSynchronize(st));
+    *t_tables = now_s();
+  }
   // ---- K2: Y-run lists, convolution, batch list
   CK(D.yn.ensure(8));
   YRunArgs ya{};
@@ -300,9 +307,7 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   // ---- rectangle lists per (batch, side): count pass, one sync, write pass
   CK(D.tiles.ensure(16 * (size_t)P.G));
   CK(D.nrect.ensure(8 * (size_t)P.G));
-  CK(D.nitem.ensure(8 * (size_t)P.G));
   CK(D.rbase.ensure(8 * (size_t)P.G));
-  CK(D.ibase.ensure(8 * (2 * (size_t)P.G + 1)));
   CK(D.err.ensure(16));
   CK(cudaMemsetAsync(D.err.p, 0, 16, st));
   RectArgs ra2{};
@@ -316,18 +321,16 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   ra2.count = D.gcount.as<uint32_t>();
   ra2.tiles = D.tiles.as<unsigned long long>();
   ra2.nrect = D.nrect.as<uint32_t>();
-  ra2.nitem = D.nitem.as<uint32_t>();
   ra2.err = D.err.as<int>();
   launch_rects(ra2, P.G, st);
   ++launches;
   int err = 0;
-  std::vector<uint32_t> nrect(2 * (size_t)P.G), nitem(2 * (size_t)P.G);
+  std::vector<uint32_t> nrect(2 * (size_t)P.G);
   CK(cudaMemcpyAsync(P.alpha.data(), D.galpha.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.nl.data(), D.gnl.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.nr.data(), D.gnr.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(P.tiles.data(), D.tiles.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(nrect.data(), D.nrect.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(nitem.data(), D.nitem.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (err) { set_err("tile count of one batch side exceeds 2^32"); return MSP_UNSUPPORTED; }
@@ -337,20 +340,9 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   for (size_t i = 0; i < 2 * (size_t)P.G; ++i) { P.rect_base[i] = (uint32_t)nrt; nrt += nrect[i]; }
   if (nrt > 0xFFFFFFFFull) { set_err("rectangle list too large"); return MSP_UNSUPPORTED; }
   CK(D.rects.ensure(sizeof(RectDesc) * std::max<uint64_t>(nrt, 1)));
-  P.item_base.assign(2 * (size_t)P.G + 1, 0);
-  for (size_t i = 0; i < 2 * (size_t)P.G; ++i) {
-    const size_t g = i / 2;  // items only for batches the partitioned waves can hold
-    const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
-    const bool fits = nb + np <= item_key_budget && ((nb + kBucketTargetMax - 1) / kBucketTargetMax) <= (uint64_t)kMaxUnitBuckets;
-    P.item_base[i + 1] = P.item_base[i] + (fits ? nitem[i] : 0u);
-  }
-  CK(D.items.ensure(8 * std::max<uint64_t>(P.item_base.back(), 1)));
-  CK(cudaMemcpyAsync(D.rbase.p, P.rect_base.data(), 8 * (size_t)P.G, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(D.ibase.p, P.item_base.data(), 8 * (2 * (size_t)P.G + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(D.rbase.p, P.rect_base.data(), 4 * 2 * (size_t)P.G, cudaMemcpyHostToDevice, st));
   ra2.rect_base = D.rbase.as<uint32_t>();
   ra2.rects = D.rects.as<RectDesc>();
-  ra2.item_base = D.ibase.as<uint64_t>();
-  ra2.items = D.items.as<uint64_t>();
   launch_rects(ra2, P.G, st);
   ++launches;
   // ---- launch-invariant enumeration arguments
@@ -361,7 +353,6 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   for (int s = 0; s < 2; ++s)
     A.yr[s] = YRuns{D.yw[s].as<uint32_t>(), D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), P.ny[s]};
   A.rects = D.rects.as<RectDesc>();
-  A.items = D.items.as<uint64_t>();
   for (int k = 0; k < 8; ++k) {
     const int c0 = 2 * k + 1, c1 = 2 * k + 2;  // rows c0, c1 (1-based companion rows)
     const uint32_t lo = (c0 < m ? (uint32_t)pr->d[c0] : 0u) + 0x8000u;
@@ -531,6 +522,9 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 uint32_t even_up(double x) { const uint32_t v = (uint32_t)x; return v + (v & 1u); }
 
 constexpr uint32_t kChunkCounters = 1u << 16;
+// Internal status: the hit list overflowed; msp_solve re-runs the (deterministic) solve with the
+// grown list, as fastval.join_pairs regrows its output buffer (fastval.py:126-139).
+constexpr int kRetryHits = 100;
 // Tiles per scatter task of the persistent wave pipeline: a wave's tiles over about one task per SM
 // (fewer, longer tasks: fewer partial rounds and task switches, every SM still scatters the wave),
 // at least kTaskTilesMin.  MSP_TASK_TILES fixes it (tuning).
@@ -569,7 +563,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   if (!pr || !opt || !res) { set_err("null argument"); return MSP_INVALID_ARGUMENT; }
   res->n = pr->n;
   Device *Dp = nullptr;
-  int rc = get_device(opt->device, &Dp);
+  int rc = get_device(opt->device, &Dp, &res->stats.t_init);
   if (rc) return rc;
   Device &D = *Dp;
   std::lock_guard<std::mutex> lk(D.mu);
@@ -618,12 +612,14 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   const double deadline = opt->time_limit_s > 0 ? t0 + opt->time_limit_s : 0;
   CK(cudaEventRecord(D.ev[0], st));
   const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : kDefaultWaveKeys;
-  rc = build_plan(D, pr, P, opt->alpha_lo, opt->alpha_hi, st, S.kernel_launches, key_budget);
+  double t_tables = 0;
+  rc = build_plan(D, pr, P, opt->alpha_lo, opt->alpha_hi, st, S.kernel_launches, &t_tables);
   if (rc) return rc;
   CK(cudaGetLastError());
   CK(cudaEventRecord(D.ev[1], st));
   mark("plan done");
-  S.t_build = now_s() - t0;
+  S.t_build = t_tables - t0;
+  S.t_enumerate = now_s() - t_tables;
   S.peak_table_entries = 0;
   for (int t = 0; t < 4; ++t) S.peak_table_entries += (int64_t)1 << P.b[t];
   S.peak_heap1 = (int64_t)1 << P.b[1];
@@ -653,7 +649,11 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   CK(cudaMemsetAsync(D.bovf.p, 0, 4 * G1, st));
   CK(D.zkeys.ensure(16 * G1));
   CK(cudaMemsetAsync(D.zkeys.p, 0, 16 * G1, st));
-  const uint64_t hit_cap = 1 << 20;
+  if (!D.hit_cap) {
+    D.hit_cap = 1 << 20;
+    if (const char *ev = getenv("MSP_HIT_CAP")) D.hit_cap = std::max<uint64_t>(16, strtoull(ev, nullptr, 10));  // (tests)
+  }
+  const uint64_t hit_cap = D.hit_cap;
   CK(D.hits.ensure(sizeof(HitRec) * hit_cap));
   CK(D.nhits.ensure(8));
   CK(D.nrecs.ensure(8));
@@ -803,7 +803,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
     if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
-    if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
+    if (nh > hit_cap) { D.hit_cap = 2 * nh; return kRetryHits; }  // regrow the hit list and re-run
     if (opt->cancel && *opt->cancel) {  // another rank confirmed a solution (first mode)
       S.cancelled = 1;
       stop_now = true;
@@ -1017,6 +1017,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       cur_keys += nb + np;
     }
     flush();
+    if (all_tiles > 0xFFFFFFFFull) {  // WaveDesc.tile0 and the chunk words index tiles with 32 bits
+      set_err("partitioned batches hold %llu warp tiles (> 2^32)", (unsigned long long)all_tiles);
+      return MSP_UNSUPPORTED;
+    }
     hmark("waves packed");
     S.waves += (int32_t)pw.size();
     if (!pw.empty()) {
@@ -1598,6 +1602,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   S.dev_ms_tables = elapsed_ms(D.ev[0], D.ev[1]);
   S.dev_ms_join = elapsed_ms(D.ev[1], D.ev[2]);
   S.dev_ms_hot = hot_ms;
+  S.hot_bytes = 8 * S.hot_pairs;  // algorithmic bytes: one 64-bit key written or read per candidate pair
   if (err) { set_err("join table region overflow (err=%d)", err); return MSP_INTERNAL; }
   // real zero keys never reach the partitioned join (0 pads the scatter's runs): their hash hits
   // are the per-batch product, and key 0 joins the recovery set (global-table batches count their
@@ -1608,7 +1613,17 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     if (zz) { bh[g] += zz; zero_hits.push_back(HitRec{g, 0u, 0ull}); }
   }
   for (uint32_t g = 0; g < P.G; ++g) { S.filtered_residuals += (int64_t)bf[g]; S.hash_hits += (int64_t)bh[g]; }
-  if (nh > hit_cap) { set_err("more than %llu distinct hit keys", (unsigned long long)hit_cap); return MSP_INTERNAL; }
+  if ((opt->flags & MSP_FLAG_BATCH_STATS) && P.G) {  // per-batch ValidationStats (validate.py:63-71)
+    res->batch_stats = (int64_t *)malloc(sizeof(int64_t) * 5 * (size_t)P.G);
+    if (!res->batch_stats) { set_err("out of host memory"); return MSP_INTERNAL; }
+    res->n_batch_stats = P.G;
+    for (uint32_t g = 0; g < P.G; ++g) {
+      int64_t *r = res->batch_stats + 5 * (size_t)g;
+      r[0] = (int64_t)P.alpha[g]; r[1] = (int64_t)P.nl[g]; r[2] = (int64_t)P.nr[g];
+      r[3] = (int64_t)bf[g]; r[4] = (int64_t)bh[g];
+    }
+  }
+  if (nh > hit_cap) { D.hit_cap = 2 * nh; return kRetryHits; }  // regrow the hit list and re-run
   if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
   if (!stopped) {
     // hits recorded by the partitioned join of dropped batches are superseded by their re-join
@@ -1666,7 +1681,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   }
   S.dev_ms_total = elapsed_ms(D.ev[0], D.ev[3]);
   S.exact_hits = (int64_t)sols.size();
-  S.t_enumerate = S.t_build;  // the plan replaces the heap stream
   if (opt->mode == MSP_MODE_FIRST && sols.size() > 1) sols.resize(1);
   return emit();
 }
@@ -1681,7 +1695,12 @@ extern "C" {
 int msp_solve(const msp_problem *prob, const msp_options *opt, msp_result *res) {
   try {
     int rc = msp::solve_impl(prob, opt, res);
-    if (rc && res) { free(res->xbits); res->xbits = nullptr; res->n_solutions = 0; }
+    for (int attempt = 0; rc == msp::kRetryHits && attempt < 8; ++attempt) {
+      msp_result_free(res);
+      rc = msp::solve_impl(prob, opt, res);
+    }
+    if (rc == msp::kRetryHits) { msp::set_err("hit list regrowth did not converge"); rc = MSP_INTERNAL; }
+    if (rc && res) msp_result_free(res);
     return rc;
   } catch (const std::exception &e) {
     msp::set_err("exception: %s", e.what());
@@ -1694,6 +1713,9 @@ void msp_result_free(msp_result *res) {
   free(res->xbits);
   res->xbits = nullptr;
   res->n_solutions = 0;
+  free(res->batch_stats);
+  res->batch_stats = nullptr;
+  res->n_batch_stats = 0;
 }
 
 int msp_join_alpha(const msp_problem *prob, const msp_options *opt, uint64_t alpha, msp_result *res) {

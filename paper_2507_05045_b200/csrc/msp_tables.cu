@@ -184,7 +184,7 @@ __global__ void k_rects(RectArgs p) {
   const uint64_t xw_total = side == 0 ? p.alpha[g] : p.target - p.alpha[g];
   const bool write = p.rects != nullptr;
   RectDesc *out = write ? p.rects + p.rect_base[(size_t)g * 2 + side] : nullptr;
-  uint64_t tbase = 0, ibase = 0;
+  uint64_t tbase = 0;
   uint32_t rbase = 0;
   const size_t gs = (size_t)g * 2 + side;
   for (uint32_t r0 = 0; r0 < ny; r0 += blockDim.x) {
@@ -204,11 +204,9 @@ __global__ void k_rects(RectArgs p) {
         }
       }
     }
-    uint32_t ttot, rtot, itot;
-    const uint32_t nit = (tiles + kItemTiles - 1) / kItemTiles;
+    uint32_t ttot, rtot;
     const uint32_t tpos = block_excl_scan(tiles, ttot);
     const uint32_t rpos = block_excl_scan(tiles > 0, rtot);
-    const uint32_t ipos = block_excl_scan(nit, itot);
     if (write && tiles) {
       RectDesc R;
       const bool lx = xl >= yl;
@@ -221,22 +219,13 @@ __global__ void k_rects(RectArgs p) {
       R.nl = (R.L + 31) / 32;
       R.nq = (R.Q + kTQ - 1) / kTQ;
       out[rbase + rpos] = R;
-      const uint64_t ridx = p.rect_base[gs] + rbase + rpos;
-      uint64_t *it = p.items + p.item_base[gs] + ibase + ipos;
-      const uint32_t emit = p.item_base[gs + 1] > p.item_base[gs] ? nit : 0u;  // huge batches: none
-      for (uint32_t k = 0; k < emit; ++k) {
-        const uint32_t t0 = k * kItemTiles, nt = min(kItemTiles, tiles - t0);
-        it[k] = ridx | ((uint64_t)t0 << 32) | ((uint64_t)nt << 56);
-      }
     }
     tbase += ttot;
     rbase += rtot;
-    ibase += itot;
   }
   if (!write && threadIdx.x == 0) {
     p.tiles[gs] = tbase;
     p.nrect[gs] = rbase;
-    p.nitem[gs] = (uint32_t)ibase;
     if (tbase > 0xFFFFFFFFull) atomicOr(p.err, 2);
   }
 }

@@ -92,70 +92,6 @@ struct TileWalker {
   }
 };
 
-// Walks this launch's work items statically strided over all warps of the grid (warp w takes
-// items w, w + W, w + 2W, ...), prefetching the next item word and rectangle descriptor while the
-// current item is processed: no search, no atomics, no dependent loads on the critical path.
-// Same tile interface as TileWalker.
-struct ItemWalker {
-  uint32_t t, tend, lc, qc;
-  bool ok;
-  UnitDesc d;
-  RectDesc R;
-  uint64_t next_i, stride;
-  uint64_t nit;      // prefetched item word (valid iff next_i < item_hi)
-  RectDesc nrect;
-
-  __device__ __forceinline__ void prefetch(const EnumArgs &A) {
-    if (next_i < A.item_hi) {
-      nit = __ldg(reinterpret_cast<const unsigned long long *>(A.items) + next_i);
-      nrect = load_rect(A.rects + (uint32_t)nit);
-    }
-  }
-  __device__ __forceinline__ void init(const EnumArgs &A, uint64_t warp_id, uint64_t nwarps) {
-    next_i = A.item_lo + warp_id;
-    stride = nwarps;
-    ok = false;
-    prefetch(A);
-  }
-  __device__ __forceinline__ bool grab(const EnumArgs &A, uint32_t) {
-    ok = next_i < A.item_hi;
-    if (!ok) return false;
-    R = nrect;
-    t = (uint32_t)(nit >> 32) & 0xFFFFFFu;
-    tend = t + (uint32_t)(nit >> 56);
-    d = A.units[R.gs() - A.gs_base];
-    lc = t / R.nq;
-    qc = t - lc * R.nq;
-    next_i += stride;
-    prefetch(A);
-    return true;
-  }
-  __device__ __forceinline__ bool valid() const { return ok; }
-  __device__ __forceinline__ const uint32_t *x_comp(const EnumArgs &A) const {
-    return d.side ? A.tab[2].comp : A.tab[0].comp;
-  }
-  __device__ __forceinline__ const uint32_t *y_comp(const EnumArgs &A) const {
-    return d.side ? A.tab[3].comp : A.tab[1].comp;
-  }
-  __device__ __forceinline__ const uint32_t *lane_comp(const EnumArgs &A) const {
-    return R.lane_is_x() ? x_comp(A) : y_comp(A);
-  }
-  __device__ __forceinline__ const uint32_t *loop_comp(const EnumArgs &A) const {
-    return R.lane_is_x() ? y_comp(A) : x_comp(A);
-  }
-  // Next tile; returns true when the unit may have changed (caller flushes per-unit counters).
-  __device__ __forceinline__ bool advance(const EnumArgs &A, uint32_t lane, uint32_t &old_gid) {
-    old_gid = d.gid;
-    if (++t < tend) {
-      if (++qc == R.nq) { qc = 0; ++lc; }
-      return false;
-    }
-    const uint32_t old_gs = R.gs();
-    grab(A, lane);
-    return !ok || R.gs() != old_gs;
-  }
-};
-
 // Resumable per-lane state of the walker's current tile: the lane's companion vector, the tile's
 // loop vectors (staged once per tile in the warp's shared-memory slot `ybuf`, one coalesced load)
 // and the next loop entry.  step_keys() produces up to kU keys per call (warp-uniform), so a

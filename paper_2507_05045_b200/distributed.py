@@ -166,6 +166,30 @@ def cuda_band_solver(device: int, time_limit: float | None = None, wave_keys: in
     return run
 
 
+def merge_band_results(inst: MspInstance, sols: list[tuple[int, ...]], per_band: list[dict],
+                       mode: str = "all") -> SolveResult:
+    """Merge the bands' solutions and counters into one SolveResult (the reference's in-process
+    merge: _merge_vstats solver.py:284-289, results sorted solver.py:238-241,415-418).  Counters
+    add up over bands (every batch lives in exactly one band); the table peaks are per solve."""
+    stats = SolveStats(engine="cuda")
+    for k in ("batches", "candidates_left", "candidates_right", "filtered_residuals", "hash_hits",
+              "exact_hits", "kernel_launches", "waves", "row1_candidate_pairs"):
+        setattr(stats, k, sum(int(r.get(k, 0)) for r in per_band))
+    for k in ("peak_table_entries", "peak_heap1", "peak_heap2"):
+        setattr(stats, k, max((int(r.get(k, 0)) for r in per_band), default=0))
+    stats.cancelled_ranks = int(sum(int(r.get("cancelled", 0)) for r in per_band))
+    sols = list(sols)
+    for x in sols:
+        if not verify_solution(inst, x):
+            raise RuntimeError("internal error: candidate failed original-system verification")
+    sols.sort(key=solution_encoding)
+    if len(set(sols)) != len(sols):
+        raise RuntimeError("internal error: duplicate solutions emitted")
+    if mode == "first":
+        sols = sols[:1]
+    return SolveResult("feasible" if sols else "infeasible", sols, stats)
+
+
 def solve_sharded(inst: MspInstance, cfg: SolverConfig | None = None, dist=None,
                   plan: Sequence[tuple[int, int, int, int]] | None = None,
                   band_solver: BandSolver | None = None, device=None) -> SolveResult:
@@ -199,23 +223,10 @@ def solve_sharded(inst: MspInstance, cfg: SolverConfig | None = None, dist=None,
         device = torch.device("cuda", cfg.device) if dist.get_backend() == "nccl" else torch.device("cpu")
     all_sols = _gather_solutions(sols, inst.n, dist, device)
     per_rank = _gather_counters(st, dist, device)
-    stats = SolveStats(engine="cuda")
-    for k in ("batches", "candidates_left", "candidates_right", "filtered_residuals", "hash_hits",
-              "exact_hits", "kernel_launches", "waves", "row1_candidate_pairs"):
-        setattr(stats, k, sum(r[k] for r in per_rank))
-    for k in ("peak_table_entries", "peak_heap1", "peak_heap2"):
-        setattr(stats, k, max(r[k] for r in per_rank))
-    for x in all_sols:
-        if not verify_solution(inst, x):
-            raise RuntimeError("internal error: candidate failed original-system verification")
-    all_sols.sort(key=solution_encoding)
-    if len(set(all_sols)) != len(all_sols):
-        raise RuntimeError("internal error: duplicate solutions emitted")
+    res = merge_band_results(inst, all_sols, per_rank, cfg.mode)
+    stats = res.stats
     if cancel is not None:
         dist.barrier()
-        stats.cancelled_ranks = int(sum(r.get("cancelled", 0) for r in per_rank))
         cancel.close(unlink=rank == 0)
-    if cfg.mode == "first":
-        all_sols = all_sols[:1]
     stats.t_total = time.perf_counter() - t0
-    return SolveResult("feasible" if all_sols else "infeasible", all_sols, stats)
+    return res

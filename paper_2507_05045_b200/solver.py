@@ -38,7 +38,10 @@ DEFAULT_MEMORY_BUDGET = 512 * 2**20  # validate.py:37
 
 _MODES = ("first", "all")
 _BACKENDS = ("cuda", "parallel", "serial")
-_ENGINES = (None, "auto", "cuda")
+# The reference's engine names (solver.py:158-167: "jit" numba, "python" heap twin) select the
+# enumerator it replaces; here every name runs the CUDA engine (the results are engine-independent
+# in the reference too, test_solver.py:169-186).
+_ENGINES = (None, "auto", "cuda", "jit", "python")
 
 
 class SolveTimeout(Exception):
@@ -109,6 +112,7 @@ class SolveStats:
     kernel_launches: int = 0
     cancelled_ranks: int = 0  # sharded first mode: ranks stopped early by another rank's solution
     dev_ms_total: float = 0.0
+    t_init: float = 0.0  # one-time CUDA context/device init inside this solve (first call only)
 
     def as_dict(self) -> dict:
         return {
@@ -186,7 +190,7 @@ def stats_from_native(st: dict, stats: SolveStats) -> None:
               "filtered_residuals", "peak_table_entries", "peak_heap1", "peak_heap2",
               "row1_candidate_pairs", "waves", "kernel_launches"):
         setattr(stats, k, int(st[k]))
-    for k in ("t_build", "t_enumerate", "t_validate", "dev_ms_total"):
+    for k in ("t_build", "t_enumerate", "t_validate", "dev_ms_total", "t_init"):
         setattr(stats, k, float(st[k]))
     stats.fallback = _FALLBACK.get(int(st["fallback"]), "none")
 

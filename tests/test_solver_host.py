@@ -19,7 +19,7 @@ def test_config_validation():
 
 def test_unknown_engine_rejected():
     with pytest.raises(ValueError):
-        msb.solve(msb.MspInstance([[1, 2, 3, 4]], [5]), msb.SolverConfig(mode="all"), engine="jit")
+        msb.solve(msb.MspInstance([[1, 2, 3, 4]], [5]), msb.SolverConfig(mode="all"), engine="numba-gpu")
 
 
 def test_reduce_rows_out_of_range():

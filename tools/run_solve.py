@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--planted", action="store_true")
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--wave-keys", type=int, default=0)
+    ap.add_argument("--batch-stats", action="store_true", help="record per-batch (alpha, nl, nr, filtered, hash_hits)")
     args = ap.parse_args()
     if args.planted:
         inst, x = msb.plant_instance(args.m, args.K, args.seed)
@@ -32,7 +33,8 @@ def main():
         inst, x = msb.generate_instance(args.m, args.K, args.seed), None
     t0 = time.perf_counter()
     sols, st = native_solve(inst, args.mode, None, device=args.device, wave_keys=args.wave_keys,
-                            flags=_native.MSP_FLAG_PROFILE if args.profile else 0)
+                            flags=(_native.MSP_FLAG_PROFILE if args.profile else 0)
+                            | (_native.MSP_FLAG_BATCH_STATS if args.batch_stats else 0))
     wall = time.perf_counter() - t0
     for s in sols:
         assert msb.verify_solution(inst, s)
@@ -41,7 +43,9 @@ def main():
            "mode": args.mode, "wall_s": round(wall, 3), "solutions": [msb.solution_to_string(s) for s in sols],
            "planted_found": (tuple(x) in sols) if x is not None else None,
            "pairs_per_s": (st["candidates_left"] + st["candidates_right"]) / wall,
-           "stats": {k: v for k, v in st.items()}}
+           "stats": {k: v for k, v in st.items() if k != "batch_stats"}}
+    if args.batch_stats:
+        rec["hit_batches"] = [b for b in st.get("batch_stats", []) if b[4] > 0]
     print(json.dumps(rec))
 
 
