@@ -110,9 +110,7 @@ struct PartArgs {
   const uint32_t *gid;        // batch of each bucket
   uint32_t nb;                // buckets per role
   uint32_t roles;             // roles present in the launch's entries (0 means 2)
-  unsigned long long *zero_keys;  // per (batch, side): real keys equal to 0 (never staged: 0 pads runs)
   unsigned long long *dbg;    // diagnostics (MSP_DEBUG_STATS): rounds, staged, overflow, pads
-  uint32_t ovf_trigger;       // overflow keys that end a scatter round (0: default)
   unsigned int *batch_ovf;    // per batch: a bucket overflowed -> re-join with the global table
   HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;
   unsigned long long *batch_hits;
@@ -204,8 +202,9 @@ struct WavesArgs {
   ScatterArgs sc;                      // comp, dpack, tiles (all waves), units (all waves), filters
   PartArgs pa;                         // hit list, per-batch counters, zero keys, diagnostics
   const uint32_t *bstart0, *bstart1, *bcap0, *bcap1, *bgid;  // bucket arrays of all waves
-  unsigned long long *scratch[kWaveBuffers];  // wave w uses buffer w % kWaveBuffers
-  uint32_t *fill[kWaveBuffers];
+  unsigned long long *scratch;         // kWaveBuffers buffers of scratch_stride keys: wave w uses
+  uint64_t scratch_stride;             //   buffer w % kWaveBuffers (no runtime-indexed param array)
+  uint32_t *fill;                      // kWaveBuffers x 2 x kMaxWaveBuckets fill counters
   const WaveDesc *waves;
   const RescatterSrc *srcs;            // level-2 sources (kind 1 waves)
   const unsigned long long *chunks;    // scatter chunks of all waves

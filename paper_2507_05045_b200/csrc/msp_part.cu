@@ -41,13 +41,10 @@ static_assert(kScatterCtas == kScatterCtasHost, "scatter CTAs per SM: msp_kernel
 constexpr int kScatterWarps = MSP_SCATTER_WARPS;
 constexpr int kScatterThreads = kScatterWarps * 32;
 constexpr int kStageKeys = kScatterStageKeys;                   // stage slots of a CTA
-#ifndef MSP_OVF_KEYS
-#define MSP_OVF_KEYS (1024 / MSP_SCATTER_CTAS)
-#endif
-constexpr int kOvf = MSP_OVF_KEYS;                              // keys ranked past their entry's C slots
-constexpr int kOvfTrigger = kOvf * 3 / 8;                       // a round ends at this many (default)
 constexpr int kMaxNB = kMaxUnitBuckets;                         // entries of one unit
-constexpr uint32_t kDrop = 0xFFFFFFFFu;
+#ifndef MSP_STAGE_FILL_PCT
+#define MSP_STAGE_FILL_PCT 75
+#endif
 #ifndef MSP_RESCATTER_N
 #define MSP_RESCATTER_N 4
 #endif
@@ -55,6 +52,21 @@ constexpr uint32_t kDrop = 0xFFFFFFFFu;
 #define MSP_SCATTER_KEYS 4
 #endif
 constexpr int kUS = MSP_SCATTER_KEYS;                           // keys per lane per scatter step
+
+// Shared memory of a scatter CTA (k_scatter / k_rescatter / scatter tasks of k_waves).  A CTA works
+// on one CHUNK at a time: consecutive tiles of ONE unit (one batch side), whose keys spread
+// uniformly over the unit's NB bucket entries.  A round's keys are bucketed in place: entry j owns
+// slots [j*C, j*C + C), C = kStageKeys / NB, and a key's slot is its rank within the entry (one
+// shared atomic), so the round needs no sort.  The round ends once a lane has staged its share of
+// MSP_STAGE_FILL_PCT % of the stage (no shared counter on the hot path); a key ranked past C -- rare at
+// that fill -- goes straight to its bucket region (one global atomic).  Bucket regions therefore
+// hold exactly `fill` real keys, densely: no padding, every key value (0 included) is a real key.
+// The producers' loop-vector buffers follow the struct (scatter only).
+struct __align__(16) Stage {
+  unsigned long long key[kStageKeys];
+  uint32_t cnt[kMaxNB];              // keys ranked into each entry this round (> C: the rest spilled)
+  uint32_t round_end, chunk, tctr, pad;
+};
 
 // Reservation of n slots at *p, result left in flight in r (predicated: no-op when n == 0, so no
 // select has to wait for the atomic's return value).
@@ -65,29 +77,11 @@ __device__ __forceinline__ void reserve_async(uint32_t &r, uint32_t *p, uint32_t
                : "memory");
 }
 
-// Shared memory of a scatter CTA (k_scatter / k_rescatter).  A CTA works on one CHUNK at a time:
-// consecutive tiles of ONE unit (one batch side), whose keys spread uniformly over the unit's NB
-// bucket entries.  The round's keys are bucketed in place: entry j owns slots [j*C, j*C + C),
-// C = kStageKeys / NB, and a key's slot is its rank within the entry (one shared atomic), so the
-// round needs no sort.  Keys ranked past C go to the overflow list with their (entry, rank); the
-// round ends when that list passes kOvfTrigger, or at the end of the chunk.  The producers'
-// loop-vector buffers follow the struct (k_scatter only).
-struct __align__(16) Stage {
-  unsigned long long key[kStageKeys];
-  unsigned long long ovk[kOvf];
-  uint32_t ove[kOvf];                // entry | rank << 11
-  uint32_t cnt[kMaxNB];              // keys ranked into each entry this round
-  uint2 run[kMaxNB];                 // flush: (scratch index of rank 0, staged keys to write)
-  uint32_t novf, round_end, chunk, ove_spill;  // ove_spill: some rank past C has no key this round
-  uint32_t tctr;                     // tiles of the chunk handed out past the first 2 per warp
-  uint32_t nstaged, pad[2];          // keys staged this round (fill trigger)
-};
-
 size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps * (kTQ + kUS) * sw * 4; }
 
 __device__ __forceinline__ void stage_init(Stage &g) {
   for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
-  if (threadIdx.x == 0) { g.novf = 0; g.round_end = 0; g.ove_spill = 0; g.nstaged = 0; }
+  if (threadIdx.x == 0) g.round_end = 0;
 }
 
 // The CTA's next work chunk (dynamic: one global atomic per chunk), broadcast through shared memory.
@@ -99,143 +93,114 @@ __device__ __forceinline__ uint32_t next_chunk(Stage &g, unsigned int *ctr) {
   return c;
 }
 
-// Spill of an overflow key that found the overflow list full: straight to its bucket region (one
-// global atomic + store); its rank slot of the round stays empty (the flush pads it).
-__device__ __noinline__ void stage_spill(Stage &g, const PartArgs &S, uint32_t e, unsigned long long key) {
+// Role-indexed member of a 2-array by select (a runtime index into the argument struct's array would
+// put the struct in local memory).
+template <class T>
+__device__ __forceinline__ T sel(T const (&a)[2], uint32_t role) { return role ? a[1] : a[0]; }
+
+// A key ranked past its entry's C slots: straight to its bucket region (one global atomic + store).
+__device__ __forceinline__ void stage_spill(const PartArgs &S, uint32_t e, unsigned long long key) {
   const uint32_t role = e >= S.nb, b = e - role * S.nb;
-  const uint32_t pos = atomicAdd(S.fill[role] + b, 1u);
-  if (pos < __ldg(S.cap[role] + b)) __stcg(S.scratch + __ldg(S.start[role] + b) + pos, key);
+  const uint32_t pos = atomicAdd(sel(S.fill, role) + b, 1u);
+  if (pos < __ldg(sel(S.cap, role) + b)) __stcg(S.scratch + __ldg(sel(S.start, role) + b) + pos, key);
   else atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
-  g.ove_spill = 1u;
   if (S.dbg) atomicAdd(S.dbg + 13, 1ull);
 }
 
+// r = atomicAdd(p, 1) on shared memory when `on` (predicated: no branch, no convergence barrier);
+// r = ~0 otherwise.
+__device__ __forceinline__ uint32_t atom_inc_shared_if(uint32_t *p, bool on) {
+  uint32_t r = 0xFFFFFFFFu;
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q atom.shared.add.u32 %0, [%1], 1;\n\t}"
+               : "+r"(r)
+               : "r"(a), "r"((uint32_t)on)
+               : "memory");
+  return r;
+}
+
 // Stage N keys per lane into their entries j (local to the chunk's unit): rank (shared atomics,
-// all issued before any dependent store), store into the entry's slots.  Keys ranked past C go to
-// the overflow list with (entry, rank): one warp-aggregated reservation per warp step.  The round
-// ends once the list passes `trig` (few big entries... many small ones overflow early) or the stage
-// holds `ftrig` keys (few big entries all fill at once: stop before the warps in flight overflow).
+// all issued before any dependent store), then store into the entry's slots; keys ranked past C
+// (rare) are spilled in a separate, warp-uniform pass so the common path stays branch-free.
+// `staged` counts this lane's keys of the round; at `budget` the lane ends the round for the CTA.
 template <int N>
-__device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t lane, uint32_t C,
-                                           uint32_t trig, uint32_t ftrig,
+__device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t C,
+                                           uint32_t &staged, uint32_t budget,
                                            const unsigned long long (&key)[N], const uint32_t (&j)[N],
                                            const bool (&ok)[N]) {
-  uint32_t r[N], nok = 0;
+  uint32_t r[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) r[u] = atom_inc_shared_if(&g.cnt[j[u]], ok[u]);
+  bool spill = false;
 #pragma unroll
   for (int u = 0; u < N; ++u) {
-    r[u] = ok[u] ? atomicAdd(&g.cnt[j[u]], 1u) : 0u;
-    nok += ok[u] ? 1u : 0u;
+    if (r[u] < C) g.key[j[u] * C + r[u]] = key[u];  // (r == ~0 when !ok)
+    spill |= ok[u] && r[u] >= C;
+    staged += ok[u] ? 1u : 0u;
   }
-  const uint32_t wok = __reduce_add_sync(0xffffffffu, nok);
-  if (lane == 0 && wok && atomicAdd(&g.nstaged, wok) + wok >= ftrig) *(volatile uint32_t *)&g.round_end = 1u;
-  uint32_t nov = 0;
+  if (__any_sync(0xffffffffu, spill)) {
 #pragma unroll
-  for (int u = 0; u < N; ++u) {
-    if (ok[u] && r[u] < C) g.key[j[u] * C + r[u]] = key[u];
-    nov += (ok[u] && r[u] >= C) ? 1u : 0u;
+    for (int u = 0; u < N; ++u)
+      if (ok[u] && r[u] >= C) stage_spill(S, ebase + j[u], key[u]);
   }
-  if (__any_sync(0xffffffffu, nov != 0u)) {
-    uint32_t inc = nov;  // warp inclusive scan of the lanes' overflow counts
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= (uint32_t)o) inc += y;
-    }
-    uint32_t ob = 0;
-    if (lane == 31) ob = atomicAdd(&g.novf, inc);
-    ob = __shfl_sync(0xffffffffu, ob, 31);
-    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-    uint32_t o = ob + inc - nov;
-#pragma unroll
-    for (int u = 0; u < N; ++u) {
-      if (!(ok[u] && r[u] >= C)) continue;
-      if (o < (uint32_t)kOvf) {
-        g.ovk[o] = key[u];
-        g.ove[o] = j[u] | (r[u] << 11);
-      } else {
-        stage_spill(g, S, ebase + j[u], key[u]);
-      }
-      ++o;
-    }
-    if (lane == 31 && ob + tot >= trig) *(volatile uint32_t *)&g.round_end = 1u;
-  }
+  if (staged >= budget) *(volatile uint32_t *)&g.round_end = 1u;
 }
 
-// After a barrier: reserve one scratch range per nonempty entry of the chunk's unit (entries
-// ebase .. ebase + NB - 1 of the launch; global atomics, one thread per entry), write the round's
-// runs out (slot-major, so consecutive threads store consecutive keys of a run) and the overflow
-// keys, reset the round.  Ends with a barrier.
-__device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t NB, uint32_t C,
-                                            uint32_t cmagic) {
+// Called by every thread after a barrier that ends the round: warp w owns entries w, w + W, ...
+// (W = warps); its lanes reserve one scratch range per nonempty entry (global atomics, all in
+// flight at once), then the warp writes each entry's run (consecutive lanes store consecutive
+// keys, two per lane per step) and clears the entry's count.  Ends with a barrier.
+__device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t NB, uint32_t C) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nb = S.nb;
-  constexpr int kPerT = (kMaxNB + kScatterThreads - 1) / kScatterThreads;
-  uint32_t res[kPerT], cn[kPerT];
-#pragma unroll
-  for (int k = 0; k < kPerT; ++k) {
-    const uint32_t j = tid + k * kScatterThreads;
-    cn[k] = j < NB ? g.cnt[j] : 0u;
-    res[k] = 0u;
+  constexpr uint32_t kW = kScatterThreads / 32;
+  for (uint32_t j0 = warp; j0 < NB; j0 += 32 * kW) {
+    const uint32_t j = j0 + lane * kW;
+    uint32_t n = 0, dst = 0, pos = 0;
+    uint32_t *fp = nullptr;
     if (j < NB) {
+      n = min(g.cnt[j], C);
+      g.cnt[j] = 0u;
       const uint32_t e = ebase + j, role = e >= nb;
-      reserve_async(res[k], S.fill[role] + (e - role * nb), cn[k]);
+      fp = sel(S.fill, role) + (e - role * nb);
+    }
+    reserve_async(pos, fp, n);
+    if (n) {
+      const uint32_t e = ebase + j, role = e >= nb, b = e - role * nb;
+      if (pos + n <= __ldg(sel(S.cap, role) + b)) {
+        dst = __ldg(sel(S.start, role) + b) + pos;
+      } else {
+        atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+        if (S.dbg) atomicAdd(S.dbg + 12, 1ull);
+        n = 0;
+      }
+      if (S.dbg) atomicAdd(S.dbg + 1, (unsigned long long)n);
+    }
+    uint32_t todo = __ballot_sync(0xffffffffu, n != 0u);
+    while (todo) {
+      const uint32_t src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t nn = __shfl_sync(0xffffffffu, n, src);
+      unsigned long long *to = S.scratch + __shfl_sync(0xffffffffu, dst, src);
+      const unsigned long long *from = g.key + (j0 + src * kW) * C;
+      for (uint32_t i = lane; i < nn; i += 64) {
+        const unsigned long long k0 = from[i];
+        const bool two = i + 32 < nn;
+        const unsigned long long k1 = two ? from[i + 32] : 0ull;
+        __stcg(to + i, k0);
+        if (two) __stcg(to + i + 32, k1);
+      }
     }
   }
-  unsigned long long nstaged = 0;
-#pragma unroll
-  for (int k = 0; k < kPerT; ++k) {
-    const uint32_t j = tid + k * kScatterThreads;
-    if (j >= NB) continue;
-    if (!cn[k]) { g.run[j] = make_uint2(kDrop, 0u); continue; }
-    nstaged += cn[k];
-    const uint32_t e = ebase + j, role = e >= nb, b = e - role * nb;
-    uint2 run = make_uint2(kDrop, 0u);
-    if (res[k] + cn[k] <= __ldg(S.cap[role] + b)) run = make_uint2(__ldg(S.start[role] + b) + res[k], min(cn[k], C));
-    else { atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u); if (S.dbg) atomicAdd(S.dbg + 12, 1ull); }
-    g.run[j] = run;
-  }
-  if (S.dbg) {  // diagnostics: rounds, staged keys, overflow keys
-    nstaged = warp_sum(nstaged);
-    if ((tid & 31) == 0 && nstaged) atomicAdd(S.dbg + 1, nstaged);
-    if (tid == 0) { atomicAdd(S.dbg + 0, 1ull); atomicAdd(S.dbg + 2, (unsigned long long)g.novf); }
-  }
-  __syncthreads();
-  const uint32_t tot = NB * C;  // (NB * C <= kStageKeys; a dropped entry has run.y == 0)
-  for (uint32_t s0 = tid; s0 < tot; s0 += 2 * kScatterThreads) {  // two slots in flight per thread
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t s = s0 + h * kScatterThreads;
-      const uint32_t j = __umulhi(s, cmagic), i = s - j * C;
-      const uint2 run = s < tot ? g.run[j] : make_uint2(0u, 0u);
-      if (i < run.y) __stcg(S.scratch + run.x + i, g.key[s]);
-    }
-  }
-  if (g.ove_spill) {  // ranks past C whose keys were spilled stay empty: pad every rank past C
-    __syncthreads();   // with key 0 (readers skip it), then write the listed overflow keys
-    for (uint32_t j = warp; j < NB; j += kScatterWarps) {
-      const uint32_t n = g.cnt[j], b = g.run[j].x;
-      if (b == kDrop) continue;
-      for (uint32_t i = C + lane; i < n; i += 32) __stcg(S.scratch + b + i, 0ull);
-    }
-    __syncthreads();
-  }
-  const uint32_t no = min(g.novf, (uint32_t)kOvf);
-  for (uint32_t o = tid; o < no; o += kScatterThreads) {
-    const uint32_t w = g.ove[o], j = w & 0x7FFu;
-    const uint32_t b = g.run[j].x;
-    if (b != kDrop) __stcg(S.scratch + b + (w >> 11), g.ovk[o]);
-  }
-  __syncthreads();
-  for (uint32_t j = tid; j < NB; j += kScatterThreads) g.cnt[j] = 0u;
-  if (tid == 0) { g.novf = 0u; g.round_end = 0u; g.ove_spill = 0u; g.nstaged = 0u; }
+  if (S.dbg && tid == 0) atomicAdd(S.dbg + 0, 1ull);
+  if (tid == 0) g.round_end = 0u;
   __syncthreads();
 }
 
-// Per-chunk stage geometry: C slots per entry and ceil(2^32 / C) (s / C == umulhi(s, cmagic) for
-// every slot index s < kStageKeys).
-__device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_t &cmagic) {
+// Stage slots per entry of a unit with NB buckets, and each lane's share of a round.
+__device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_t &budget) {
   C = kStageKeys / NB;
-  cmagic = (uint32_t)((0xFFFFFFFFull + C) / C);
+  budget = max(1u, NB * C * MSP_STAGE_FILL_PCT / (100u * kScatterThreads));
 }
 
 // ---------------------------------------------------------------- tile descriptors
@@ -322,14 +287,13 @@ template <int MC, bool RIGHT>
 __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uint32_t *ybuf,
                                           const uint32_t (&lv)[stride_for(MC)],
                                           const uint32_t (&dg)[words_for(MC) > 0 ? words_for(MC) : 1],
-                                          uint32_t lane, uint32_t C, uint32_t q, uint32_t qn, bool lok,
-                                          const UnitInfo &ui, uint32_t nbk, uint32_t diag,
+                                          uint32_t C, uint32_t budget, uint32_t &staged, uint32_t q,
+                                          uint32_t qn, bool lok, const UnitInfo &ui, uint32_t nbk, uint32_t diag,
                                           unsigned long long &filt, unsigned long long &dacc) {
   constexpr int SW = stride_for(MC), NW0 = words_for(MC), NW = NW0 > 0 ? NW0 : 1;
   unsigned long long key[kUS];
   uint32_t j[kUS];
   bool ok[kUS];
-  uint32_t nzero = 0;
 #pragma unroll
   for (int u = 0; u < kUS; ++u) {
     uint32_t yv[SW];
@@ -353,26 +317,22 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
       fold(lo, hi, (c & 1) ? (w >> 16) & (RIGHT ? 0x7FFFu : 0xFFFFu) : w & (RIGHT ? 0x7FFFu : 0xFFFFu));
     }
     key[u] = ((unsigned long long)hi << 32) | lo;
-    const bool z = in && (hi | lo) == 0u;  // a real key 0: counted per (batch, side), never staged
-    nzero += z ? 1u : 0u;
-    ok[u] = in && !z;
+    ok[u] = in;
     j[u] = __umulhi(hi, nbk);  // bucket within the unit = floor(hi * NB / 2^32)
   }
-  if (nzero) atomicAdd(S.zero_keys + 2 * ui.gid + (RIGHT ? 1u : 0u), (unsigned long long)nzero);
   if (diag) {
 #pragma unroll
     for (int u = 0; u < kUS; ++u) dacc ^= ok[u] ? key[u] : 0ull;
   } else {
-    stage_keys<kUS>(g, S, ui.ent & 0x1FFFu, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, nbk * C * 7 / 8,
-                   key, j, ok);
+    stage_keys<kUS>(g, S, ui.ent & 0x1FFFu, C, staged, budget, key, j, ok);
   }
 }
 
 // One work chunk: tiles [t0, n) of ONE unit (one batch side), enumerated + hashed + partitioned by
 // the CTA.  Warps take their first two tiles statically and later ones from a shared counter (so
 // they finish within one tile of each other), with the descriptor two tiles ahead and the
-// companion vectors one tile ahead in flight.  A round ends for every warp as soon as the overflow
-// list passes its trigger (the CTA flushes, then resumes mid-tile) and at the end of the chunk.
+// companion vectors one tile ahead in flight.  A round ends for every warp as soon as some lane
+// has staged its share (the CTA flushes, then resumes mid-tile) and at the end of the chunk.
 // Filtered right pairs go to batch_filtered.  Ends with a barrier (the last flush).
 template <int MC>
 __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const ScatterArgs &A, const PartArgs &S,
@@ -383,8 +343,8 @@ __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const Sc
   volatile uint32_t *round_end = &g.round_end;
   const uint32_t ebase = ui.ent & 0x1FFFu, nbk = (ui.ent >> 13) & 0x7FFu, side = (ui.ent >> 24) & 1u;
   const bool right = side != 0;
-  uint32_t C, cmagic;
-  stage_geometry(nbk, C, cmagic);
+  uint32_t C, budget, staged = 0;
+  stage_geometry(nbk, C, budget);
   if (tid == 0) g.tctr = 0;
   __syncthreads();
   auto grab = [&]() {
@@ -417,9 +377,9 @@ __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const Sc
   while (true) {
     while (have && !*round_end) {
       if (right)
-        hash_step<MC, true>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
+        hash_step<MC, true>(g, S, ybuf, lvc, dg, C, budget, staged, q, qn, lok, ui, nbk, A.diag, filt, dacc);
       else
-        hash_step<MC, false>(g, S, ybuf, lvc, dg, lane, C, q, qn, lok, ui, nbk, A.diag, filt, dacc);
+        hash_step<MC, false>(g, S, ybuf, lvc, dg, C, budget, staged, q, qn, lok, ui, nbk, A.diag, filt, dacc);
       q += kUS;
       if (q >= qn) {  // next tile: everything it needs was loaded one (vectors) or two tiles ago
         t = tn;
@@ -438,7 +398,8 @@ __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const Sc
       }
     }
     const bool more = __syncthreads_or(have);
-    flush_round(g, S, ebase, nbk, C, cmagic);
+    flush_round(g, S, ebase, nbk, C);
+    staged = 0;
     if (!more) break;
   }
   if (right) {
@@ -473,20 +434,19 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
 }
 
 // Level 2 of the huge-batch path: stream already-hashed keys back from coarse bucket regions
-// (HBM) and re-partition them into fine buckets (L2 scratch) for k_join.  Work chunks are slot
-// ranges of ONE source (a coarse region of one role, whose keys spread uniformly over its NF fine
-// buckets); slots past the region's fill are empty.  Fine bucket = floor(frac * NF / 2^32), frac
-// = the key's position inside its coarse bucket (the low word of hi * NC).
-// One level-2 work chunk: slots [s0, s1) of ONE source (a coarse region of one role, whose keys
-// spread uniformly over its NF fine buckets), re-partitioned by the CTA.  Ends with a barrier.
+// (HBM) and re-partition them into fine buckets (L2 scratch) for the join.  One work chunk: slots
+// [s0, s1) of ONE source (a coarse region of one role, holding exactly `fill` keys, which spread
+// uniformly over its NF fine buckets), re-partitioned by the CTA.  Fine bucket = floor(frac * NF /
+// 2^32), frac = the key's position inside its coarse bucket (the low word of hi * NC).  Ends with
+// a barrier.
 __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, const RescatterSrc &src, uint32_t s0,
                                                 uint32_t s1) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   volatile uint32_t *round_end = &g.round_end;
   constexpr int N = MSP_RESCATTER_N;  // keys per lane per step; the next step's keys are in flight meanwhile (HBM)
   const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
-  uint32_t C, cmagic;
-  stage_geometry(NB, C, cmagic);
+  uint32_t C, budget, staged = 0;
+  stage_geometry(NB, C, budget);
   const uint32_t stride = kScatterThreads;
   uint32_t idx = s0 + warp * 32 + lane;
   unsigned long long nxt[N];
@@ -503,19 +463,18 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
 #pragma unroll
       for (int u = 0; u < N; ++u) {
         key[u] = nxt[u];
+        ok[u] = idx + u * stride < s1;
         const uint32_t x = idx + (N + u) * stride;
         nxt[u] = x < s1 ? __ldcs(src.keys + x) : 0ull;
       }
 #pragma unroll
-      for (int u = 0; u < N; ++u) {
-        ok[u] = key[u] != 0ull;  // past the fill, or a run pad
-        j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
-      }
-      stage_keys<N>(g, S, ebase, lane, C, S.ovf_trigger ? S.ovf_trigger : kOvfTrigger, NB * C * 7 / 8, key, j, ok);
+      for (int u = 0; u < N; ++u) j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
+      stage_keys<N>(g, S, ebase, C, staged, budget, key, j, ok);
       idx += N * stride;
     }
     const bool more = __syncthreads_or(idx - lane < s1);
-    flush_round(g, S, ebase, NB, C, cmagic);
+    flush_round(g, S, ebase, NB, C);
+    staged = 0;
     if (!more) break;
   }
 }
@@ -545,69 +504,71 @@ constexpr int kJWays = 8;                               // slots per table bucke
 constexpr int kJBuckets = kJoinSlots / kJWays;          // 2K buckets of 8 slots
 constexpr int kStash = 256;                             // keys whose two buckets were both full
 constexpr int kHitWords = (kJoinSlots + kStash) / 32;
+constexpr int kJQueue = 1024;                           // deferred probes per bucket (then inline)
 
 // Shared-memory join table of one bucket: 8-slot buckets, first fit in bucket b1, then b2, then a
-// small stash.  Each slot keeps the full 64-bit key and an 8-bit fingerprint (0 = empty); the eight
-// fingerprints of a bucket are one 64-bit word.  An insert is one shared atomic + two stores; a
-// probe reads ONE fingerprint word and tests all eight lanes at once (zero-byte test), reading
-// full keys only on a fingerprint match (~3% of probes plus the true hits).  A key can sit in b2
-// only if b1 is full (no zero lane), so b2 is read only by probes whose b1 is full.  Keys arriving
-// here are FNV outputs whose top bits chose the bucket; b1/b2 come from a multiplicative mix of the
-// low word, the fingerprint from the middle of the high word.  Only counts and fingerprints are
-// cleared per bucket.
+// small stash.  Each slot keeps the full 64-bit key and a fingerprint byte 0x80 | 7 key bits (0 =
+// empty); the eight fingerprints of a bucket are one 64-bit word.  An insert is one shared atomic
+// + two stores; a probe reads ONE fingerprint word and tests all eight bytes at once, reading full
+// keys only on a fingerprint match (~2% of probes plus the true hits).  A key sits in b2 only if b1
+// was full (slot 7's marker bit, the word's sign bit), so b2 is read only by probes whose b1 is
+// full.  b1/b2 come from a multiplicative mix of the key's low word, the fingerprint from its high
+// word (whose top bits chose the partition bucket).  Only counts and fingerprints are cleared per
+// bucket.
 struct JoinSmem {
   unsigned long long key[kJBuckets][kJWays];
-  unsigned long long fp[kJBuckets];     // eight 8-bit fingerprints
+  unsigned long long fp[kJBuckets];     // eight fingerprint bytes
   uint32_t cnt[kJBuckets];              // claims (may exceed 8: failed claims move on)
   unsigned long long stash[kStash];
   uint32_t hitbits[kHitWords];
   unsigned long long bhits[kJoinThreads / 32];
-  uint32_t nstash, ovf;
+  unsigned long long queue[kJQueue];    // probe keys whose fast test did not rule out a match
+  uint32_t nstash, ovf, nq, pad;
 };
 
 size_t join_smem_bytes() { return sizeof(JoinSmem); }
 
-struct JoinHash { uint32_t b1, b2, fp; };
-__device__ __forceinline__ JoinHash join_hash(unsigned long long k) {
-  const uint32_t t = (uint32_t)k * 0x9E3779B1u, hi = (uint32_t)(k >> 32);
-  JoinHash h;
-  h.b1 = t >> 21;
-  h.b2 = h.b1 ^ (((t >> 10) & (kJBuckets - 1)) | 1u);  // != b1
-  h.fp = (hi >> 8) & 0xFFu;
-  if (h.fp == 0) h.fp = 1;  // 0 marks an empty slot
-  return h;
+__device__ __forceinline__ uint32_t jmix(unsigned long long k) { return (uint32_t)k * 0x9E3779B1u; }
+__device__ __forceinline__ uint32_t jb1(uint32_t t) { return t >> 21; }
+__device__ __forceinline__ uint32_t jb2(uint32_t t) { return (t >> 21) ^ (((t >> 10) & (kJBuckets - 1)) | 1u); }
+// fingerprint byte replicated into all four bytes of a word
+__device__ __forceinline__ uint32_t jfp4(unsigned long long k) {
+  return __byte_perm((uint32_t)(k >> 32), 0u, 0x1111u) | 0x80808080u;
 }
-
-// 0x80 in exactly the bytes of x that are zero (no false positives, unlike the borrow trick).  Per
-// 32-bit half: (x & 0x7F..) + 0x7F.. never carries across a byte, so the halves are independent.
+// 0x80 in exactly the bytes of x that are zero (exact per byte; the halves are independent).
 __device__ __forceinline__ uint32_t zero_byte_mask32(uint32_t x) {
   return ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);
 }
-__device__ __forceinline__ unsigned long long zero_byte_mask(unsigned long long x) {
-  return ((unsigned long long)zero_byte_mask32((uint32_t)(x >> 32)) << 32) | zero_byte_mask32((uint32_t)x);
-}
-// Bucket full: slots are claimed in order 0..7 (one atomic count per bucket) and every claim below 8
-// writes its fingerprint before the build/probe barrier, so the bucket is full iff slot 7 is set.
-__device__ __forceinline__ bool bucket_full(unsigned long long w) { return (uint32_t)(w >> 56) != 0u; }
-__device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
-  const JoinHash h = join_hash(k);
-  uint32_t b = h.b1, s = atomicAdd(&T.cnt[b], 1u);
-  if (s >= (uint32_t)kJWays) { b = h.b2; s = atomicAdd(&T.cnt[b], 1u); }
+// Some byte of x is zero (exact for presence).
+__device__ __forceinline__ uint32_t has_zero_byte(uint32_t x) { return (x - 0x01010101u) & ~x & 0x80808080u; }
+
+__device__ __forceinline__ void join_insert_slow(JoinSmem &T, unsigned long long k, uint32_t t, uint32_t fpb) {
+  const uint32_t b = jb2(t), s = atomicAdd(&T.cnt[b], 1u);
   if (s < (uint32_t)kJWays) {
     T.key[b][s] = k;
-    reinterpret_cast<uint8_t *>(&T.fp[b])[s] = (uint8_t)h.fp;  // slot s is this thread's alone
+    reinterpret_cast<uint8_t *>(&T.fp[b])[s] = (uint8_t)fpb;
   } else {
     const uint32_t i = atomicAdd(&T.nstash, 1u);
     if (i < (uint32_t)kStash) T.stash[i] = k; else T.ovf = 1u;
   }
 }
 
-// Copies of k among the slots of bucket b whose fingerprint byte matches (one iteration per match:
-// usually none, so a warp rarely runs the key comparisons at all).
-__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, unsigned long long w,
-                                                unsigned long long pat, unsigned long long k, uint32_t &c,
-                                                uint32_t &first) {
-  unsigned long long m = zero_byte_mask(w ^ pat);
+__device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
+  const uint32_t t = jmix(k), b = jb1(t), fpb = jfp4(k) & 0xFFu;
+  const uint32_t s = atomicAdd(&T.cnt[b], 1u);
+  if (s < (uint32_t)kJWays) {
+    T.key[b][s] = k;
+    reinterpret_cast<uint8_t *>(&T.fp[b])[s] = (uint8_t)fpb;  // slot s is this thread's alone
+  } else {
+    join_insert_slow(T, k, t, fpb);
+  }
+}
+
+// Copies of k among the slots of bucket b whose fingerprint byte matches.
+__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, unsigned long long w, uint32_t pat,
+                                                unsigned long long k, uint32_t &c, uint32_t &first) {
+  unsigned long long m = ((unsigned long long)zero_byte_mask32((uint32_t)(w >> 32) ^ pat) << 32) |
+                         zero_byte_mask32((uint32_t)w ^ pat);
   while (m) {
     const uint32_t s = (uint32_t)(__ffsll((long long)m) - 1) >> 3;
     if (T.key[b][s] == k) {
@@ -618,27 +579,20 @@ __device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, u
   }
 }
 
-// Some byte of x is zero: the borrow trick, exact for presence (not for which bytes).
-__device__ __forceinline__ bool any_zero_byte(unsigned long long x) {
-  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-  return (((lo - 0x01010101u) & ~lo) | ((hi - 0x01010101u) & ~hi)) & 0x80808080u;
-}
-
-// Multiplicity of k in the table; `first` = slot id of its first copy (b1, then b2, then stash).
-// Fast path (almost every probe): no fingerprint byte of b1 matches and b1 is not full.
-__device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long long k, uint32_t nstash,
-                                               uint32_t &first) {
-  const JoinHash h = join_hash(k);
-  const unsigned long long pat = h.fp * 0x0101010101010101ull;
-  const unsigned long long w1 = T.fp[h.b1];
+// Multiplicity of k in the table (slow path: some fingerprint byte of b1 matches, or b1 is full);
+// `first` = slot id of its first copy (b1, then b2, then stash).
+__device__ __forceinline__ uint32_t join_count_slow(const JoinSmem &T, unsigned long long k, uint32_t nstash,
+                                                 uint32_t &first) {
+  const uint32_t t = jmix(k), b1 = jb1(t), pat = jfp4(k);
+  const unsigned long long w1 = T.fp[b1];
   first = 0xFFFFFFFFu;
-  if (!any_zero_byte(w1 ^ pat) && !bucket_full(w1)) return 0u;
   uint32_t c = 0;
-  count_in_bucket(T, h.b1, w1, pat, k, c, first);
-  if (bucket_full(w1)) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
-    const unsigned long long w2 = T.fp[h.b2];
-    count_in_bucket(T, h.b2, w2, pat, k, c, first);
-    if (bucket_full(w2))
+  count_in_bucket(T, b1, w1, pat, k, c, first);
+  if ((long long)w1 < 0) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
+    const uint32_t b2 = jb2(t);
+    const unsigned long long w2 = T.fp[b2];
+    count_in_bucket(T, b2, w2, pat, k, c, first);
+    if ((long long)w2 < 0)
       for (uint32_t i = 0; i < nstash; ++i)
         if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
   }
@@ -648,17 +602,18 @@ __device__ __forceinline__ uint32_t join_count(const JoinSmem &T, unsigned long 
 // Join of bucket b of a wave by one CTA of NT threads: clear the table, insert the build keys,
 // probe with the probe keys (fastval.py:75-107 semantics: every full-64-bit-hash-equal pair is a
 // hit), record each hit key once, reset the bucket's fill counters for the next use of the buffer.
-// Key 0 only pads runs (real zero keys are counted by the scatter) and is skipped, as are the
-// zero-filled loads past the bucket's end.  Ends with a barrier.
+// The regions hold exactly min(fill, cap) real keys (fill > cap flagged the batch).  Ends with a
+// barrier.
 template <int NT>
 __device__ __forceinline__ void join_bucket(JoinSmem &T, const PartArgs &S, uint32_t b) {
   const uint32_t tid = threadIdx.x;
   constexpr int U = MSP_JOIN_U;  // keys loaded per thread before the table operations
   long long tp0 = 0, tp1 = 0, tp2 = 0;
   if (S.dbg && tid == 0) tp0 = clock64();
-  for (uint32_t i = tid; i < (uint32_t)kJBuckets; i += NT) { T.cnt[i] = 0u; T.fp[i] = 0ull; }
+  for (uint32_t i = tid; i < (uint32_t)kJBuckets / 4; i += NT) reinterpret_cast<uint4 *>(T.cnt)[i] = make_uint4(0, 0, 0, 0);
+  for (uint32_t i = tid; i < (uint32_t)kJBuckets / 2; i += NT) reinterpret_cast<uint4 *>(T.fp)[i] = make_uint4(0, 0, 0, 0);
   for (uint32_t i = tid; i < (uint32_t)kHitWords; i += NT) T.hitbits[i] = 0u;
-  if (tid == 0) { T.nstash = 0; T.ovf = 0; }
+  if (tid == 0) { T.nstash = 0; T.ovf = 0; T.nq = 0; }
   const uint32_t gid = __ldg(S.gid + b);
   const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
   const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
@@ -673,15 +628,14 @@ __device__ __forceinline__ void join_bucket(JoinSmem &T, const PartArgs &S, uint
   __syncthreads();
   for (uint32_t base = 0; base < nbuild; base += NT * U) {
     unsigned long long nx[U];  // next keys in flight while this batch is inserted
-    const uint32_t nb2 = base + NT * U;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint32_t i = nb2 + u * NT + tid;
+      const uint32_t i = base + NT * U + u * NT + tid;
       nx[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (kv[u]) join_insert(T, kv[u]);
+      if (base + u * NT + tid < nbuild) join_insert(T, kv[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) kv[u] = nx[u];
   }
@@ -694,34 +648,55 @@ __device__ __forceinline__ void join_bucket(JoinSmem &T, const PartArgs &S, uint
   if (S.dbg && tid == 0) tp1 = clock64();
   const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
   if (T.ovf && tid == 0) { atomicOr(S.batch_ovf + gid, 1u); if (S.dbg) atomicAdd(S.dbg + 14, 1ull); }
-  unsigned long long hits = 0;
+  uint32_t hits = 0;
+  // a probe hit: count it, record the key once (first copy's slot) for the exact confirmation
+  auto probe_slow = [&](unsigned long long k) {
+    uint32_t first;
+    const uint32_t c = join_count_slow(T, k, nstash, first);
+    if (c) {
+      hits += c;
+      if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
+        const unsigned long long h = atomicAdd(S.nhits, 1ull);
+        if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
+      }
+    }
+  };
+  const uint32_t lane = tid & 31;
   for (uint32_t base = 0; base < nprobe; base += NT * U) {
     unsigned long long nx[U];  // next keys in flight while this batch is probed
-    const uint32_t nb2 = base + NT * U;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint32_t i = nb2 + u * NT + tid;
+      const uint32_t i = base + NT * U + u * NT + tid;
       nx[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+      // fast test, branch-free: no fingerprint byte of b1 matches and b1 is not full -> no copy of k
       const unsigned long long k = kv[u];
-      if (!k) continue;
-      uint32_t first;
-      const uint32_t c = join_count(T, k, nstash, first);
-      if (c) {
-        hits += c;
-        if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
-          const unsigned long long h = atomicAdd(S.nhits, 1ull);
-          if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
+      const uint32_t pat = jfp4(k);
+      const unsigned long long w = T.fp[jb1(jmix(k))];
+      const bool maybe = ((has_zero_byte((uint32_t)w ^ pat) | has_zero_byte((uint32_t)(w >> 32) ^ pat)) != 0u ||
+                          (long long)w < 0) && base + u * NT + tid < nprobe;
+      const uint32_t mm = __ballot_sync(0xffffffffu, maybe);
+      if (mm) {  // defer the exact count (warp-aggregated append): no divergent slow path here
+        uint32_t q0 = 0;
+        if (lane == (uint32_t)(__ffs(mm) - 1)) q0 = atomicAdd(&T.nq, (uint32_t)__popc(mm));
+        q0 = __shfl_sync(0xffffffffu, q0, __ffs(mm) - 1);
+        if (maybe) {
+          const uint32_t qi = q0 + __popc(mm & ((1u << lane) - 1u));
+          if (qi < (uint32_t)kJQueue) T.queue[qi] = k;
+          else probe_slow(k);  // queue full (duplicate-heavy bucket)
         }
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) kv[u] = nx[u];
   }
-  hits = warp_sum(hits);
-  if ((tid & 31) == 0) T.bhits[tid >> 5] = hits;
+  __syncthreads();
+  const uint32_t nq = min(T.nq, (uint32_t)kJQueue);
+  for (uint32_t i = tid; i < nq; i += NT) probe_slow(T.queue[i]);
+  const unsigned long long wh = warp_sum((unsigned long long)hits);
+  if ((tid & 31) == 0) T.bhits[tid >> 5] = wh;
   __syncthreads();
   if (S.dbg && tid == 0) {
     tp2 = clock64();
@@ -822,9 +797,10 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
     const uint32_t w = (uint32_t)(tk >> 32) & 0x7FFFFFFFu, idx = (uint32_t)tk;
     const WaveDesc wd = s_wd;
     PartArgs S = W.pa;
-    S.scratch = W.scratch[w % kWaveBuffers];
-    S.fill[0] = W.fill[w % kWaveBuffers];
-    S.fill[1] = W.fill[w % kWaveBuffers] + kMaxWaveBuckets;
+    const uint32_t buf = w % kWaveBuffers;
+    S.scratch = W.scratch + buf * W.scratch_stride;
+    S.fill[0] = W.fill + buf * (2 * kMaxWaveBuckets);
+    S.fill[1] = S.fill[0] + kMaxWaveBuckets;
     S.start[0] = W.bstart0 + wd.b0;
     S.start[1] = W.bstart1 + wd.b0;
     S.cap[0] = W.bcap0 + wd.b0;

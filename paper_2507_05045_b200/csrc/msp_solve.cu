@@ -81,13 +81,13 @@ struct Device {
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
   DBuf rkeys, runits, rfilt, rhits;
-  DBuf bfilt, bhits, bovf, scratch, bk, bruns, fill, zkeys, dbg;
+  DBuf bfilt, bhits, bovf, scratch, bk, bruns, fill, dbg;
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   uint64_t hit_cap = 0;  // distinct hit keys the hit list holds (grown on overflow, fastval.py:126-139)
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
-  DBuf scratch2, fill2, scratch3, fill3, scratch4, fill4;
+  uint64_t wstride = 0;  // keys per wave scratch buffer (D.scratch holds kWaveBuffers of them)
   DBuf tdesc, gstb, gsu, uinfo, chunks, cchunks, l2chunks, cctr, cfirst, ccfirst, tchunks, wdesc, wctr, tasks;
   uint32_t cctr_next = 0;  // next unused chunk counter in cctr (zeroed per solve)
   // pinned staging ring for the per-launch metadata uploads: a cudaMemcpyAsync from pageable memory
@@ -103,8 +103,8 @@ struct Device {
     DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
-                   &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &bruns, &fill, &cscratch[0], &cscratch[1],
-                   &cfill, &cbk, &hunits, &l2bk, &l2src, &scratch2, &fill2, &scratch3, &fill3, &scratch4, &fill4, &tdesc, &gstb, &gsu, &uinfo,
+                   &bfilt, &bhits, &bovf, &scratch, &bk, &bruns, &fill, &cscratch[0], &cscratch[1],
+                   &cfill, &cbk, &hunits, &l2bk, &l2src, &tdesc, &gstb, &gsu, &uinfo,
                    &chunks, &cchunks, &l2chunks, &cctr, &cfirst, &ccfirst, &tchunks, &wdesc, &wctr, &tasks};
     for (DBuf *b : all) b->release();
     for (int i = 0; i < 4; ++i) { tw[i].release(); tm[i].release(); tw2[i].release(); tm2[i].release();
@@ -647,8 +647,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   CK(cudaMemsetAsync(D.bfilt.p, 0, 8 * G1, st));
   CK(cudaMemsetAsync(D.bhits.p, 0, 8 * G1, st));
   CK(cudaMemsetAsync(D.bovf.p, 0, 4 * G1, st));
-  CK(D.zkeys.ensure(16 * G1));
-  CK(cudaMemsetAsync(D.zkeys.p, 0, 16 * G1, st));
   if (!D.hit_cap) {
     D.hit_cap = 1 << 20;
     if (const char *ev = getenv("MSP_HIT_CAP")) D.hit_cap = std::max<uint64_t>(16, strtoull(ev, nullptr, 10));  // (tests)
@@ -685,8 +683,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   };
   auto launch_pair = [&](size_t wi, auto &&scatter_fn, PartArgs &pa) -> int {
     const int buf = (int)(wi & 1);
-    pa.scratch = (buf ? D.scratch2 : D.scratch).as<unsigned long long>();
-    pa.fill[0] = (buf ? D.fill2 : D.fill).as<uint32_t>();
+    pa.scratch = D.scratch.as<unsigned long long>() + buf * D.wstride;
+    pa.fill[0] = D.fill.as<uint32_t>() + buf * (2 * kMaxWaveBuckets);
     pa.fill[1] = pa.fill[0] + kMaxWaveBuckets;
     if (!overlap) {
       CK(scatter_fn(pa, st));
@@ -701,15 +699,18 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(cudaEventRecord(D.ev_j[buf], D.stream2));
     return MSP_OK;
   };
+  // kWaveBuffers scratch buffers of >= scratch_keys keys each, and their fill counters (zeroed per
+  // solve and after a reallocation; the joins reset them after every bucket)
   auto ensure_wave_buffers = [&](uint64_t scratch_keys) -> int {
-    CK(D.scratch.ensure(8 * (scratch_keys + kSinkSlots)));
-    CK(D.scratch2.ensure(8 * (scratch_keys + kSinkSlots)));
-    void *f1 = D.fill.p, *f2 = D.fill2.p;
-    CK(D.fill.ensure(4 * 2 * kMaxWaveBuckets));
-    CK(D.fill2.ensure(4 * 2 * kMaxWaveBuckets));
-    if (f1 != D.fill.p || f2 != D.fill2.p || !fill_zeroed) {
-      CK(cudaMemsetAsync(D.fill.p, 0, 4 * 2 * kMaxWaveBuckets, st));
-      CK(cudaMemsetAsync(D.fill2.p, 0, 4 * 2 * kMaxWaveBuckets, st));
+    const uint64_t stride = (scratch_keys + kSinkSlots + 31) & ~31ull;
+    if (stride > D.wstride || !D.scratch.p) {
+      CK(D.scratch.ensure(8 * kWaveBuffers * stride));
+      D.wstride = D.scratch.cap / (8 * kWaveBuffers) & ~31ull;
+    }
+    void *f0 = D.fill.p;
+    CK(D.fill.ensure(4 * kWaveBuffers * 2 * kMaxWaveBuckets));
+    if (f0 != D.fill.p || !fill_zeroed) {
+      CK(cudaMemsetAsync(D.fill.p, 0, 4 * kWaveBuffers * 2 * kMaxWaveBuckets, st));
       fill_zeroed = true;
     }
     return MSP_OK;
@@ -846,8 +847,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   // buckets per role of one partitioned wave (scatter entries = 2x): fewer entries give longer
   // runs per round; MSP_WAVE_BUCKETS overrides for tuning
   uint32_t wave_buckets = kMaxWaveBuckets;
-  uint32_t ovf_trigger = 0;
-  if (const char *ev = getenv("MSP_OVF_TRIGGER")) ovf_trigger = (uint32_t)std::max(1, std::min(1024, atoi(ev)));
   unsigned long long *dbg_stats = nullptr;
   CK(D.cctr.ensure(4 * kChunkCounters));
   CK(cudaMemsetAsync(D.cctr.p, 0, 4 * kChunkCounters, st));
@@ -921,31 +920,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
     return MSP_OK;
   };
-  // kWaveBuffers scratch buffers (+ fill counters, zeroed per solve) for the pipeline
-  bool fill3_zeroed = false;
-  auto ensure_pipeline_buffers = [&](uint64_t scratch_keys) -> int {
-    if (int r1 = ensure_wave_buffers(scratch_keys)) return r1;
-    void *f3 = D.fill3.p, *f4 = D.fill4.p;
-    CK(D.scratch3.ensure(8 * (scratch_keys + kSinkSlots)));
-    CK(D.scratch4.ensure(8 * (scratch_keys + kSinkSlots)));
-    CK(D.fill3.ensure(4 * 2 * kMaxWaveBuckets));
-    CK(D.fill4.ensure(4 * 2 * kMaxWaveBuckets));
-    if (f3 != D.fill3.p || f4 != D.fill4.p || !fill3_zeroed) {
-      CK(cudaMemsetAsync(D.fill3.p, 0, 4 * 2 * kMaxWaveBuckets, st));
-      CK(cudaMemsetAsync(D.fill4.p, 0, 4 * 2 * kMaxWaveBuckets, st));
-      fill3_zeroed = true;
-    }
-    return MSP_OK;
-  };
   auto pipeline_base = [&](WavesArgs &W) {
-    W.scratch[0] = D.scratch.as<unsigned long long>();
-    W.scratch[1] = D.scratch2.as<unsigned long long>();
-    W.scratch[2] = D.scratch3.as<unsigned long long>();
-    W.scratch[3] = D.scratch4.as<unsigned long long>();
-    W.fill[0] = D.fill.as<uint32_t>();
-    W.fill[1] = D.fill2.as<uint32_t>();
-    W.fill[2] = D.fill3.as<uint32_t>();
-    W.fill[3] = D.fill4.as<uint32_t>();
+    W.scratch = D.scratch.as<unsigned long long>();
+    W.scratch_stride = D.wstride;
+    W.fill = D.fill.as<uint32_t>();
   };
 
   // ---- classify batches: partitioned shared-memory join (default) or global-table join
@@ -1087,9 +1065,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.fill[0] = D.fill.as<uint32_t>();
       pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
       pa.batch_ovf = D.bovf.as<unsigned int>();
-      pa.zero_keys = D.zkeys.as<unsigned long long>();
       pa.dbg = dbg_stats;
-      pa.ovf_trigger = ovf_trigger;
       pa.hits = D.hits.as<HitRec>();
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
@@ -1126,7 +1102,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         if (int ru_ = upload(D.tchunks.p, tch.data(), 8 * tch.size())) return ru_;
         CK(D.wdesc.ensure(sizeof(WaveDesc) * wds.size()));
         if (int ru_ = upload(D.wdesc.p, wds.data(), sizeof(WaveDesc) * wds.size())) return ru_;
-        rc = ensure_pipeline_buffers(max_scratch);
+        rc = ensure_wave_buffers(max_scratch);
         if (rc) return rc;
         WavesArgs W{};
         W.sc = sa;
@@ -1212,7 +1188,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(D.cscratch[0].ensure(8 * (mcb + kSinkSlots)));
       CK(D.cscratch[1].ensure(8 * (mcp + kSinkSlots)));
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, mt)));
-      rc = ensure_pipeline_buffers(2 * key_budget + 4 * kMaxWaveBuckets * 64ull);
+      rc = ensure_wave_buffers(2 * key_budget + 4 * kMaxWaveBuckets * 64ull);
       if (rc) return rc;
     }
     for (size_t hi_ = 0; hi_ < huge_b.size() && !stopped; ++hi_) {
@@ -1280,8 +1256,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       if (int ru_ = upload(D.ccfirst.p, ccf.data(), 4 * ccf.size())) return ru_;
       c1.batch_ovf = D.bovf.as<unsigned int>();
       c1.dbg = dbg_stats ? dbg_stats + 16 : nullptr;
-      c1.ovf_trigger = ovf_trigger;
-      c1.zero_keys = D.zkeys.as<unsigned long long>();
       if (profile) CK(cudaEventRecord(D.pev[0], st));
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, std::max(ltiles[0], ltiles[1]))));
       for (int role = 0; role < 2; ++role) {
@@ -1362,9 +1336,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.fill[0] = D.fill.as<uint32_t>();
       pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
       pa.batch_ovf = D.bovf.as<unsigned int>();
-      pa.zero_keys = D.zkeys.as<unsigned long long>();
       pa.dbg = dbg_stats ? dbg_stats + 32 : nullptr;
-      pa.ovf_trigger = ovf_trigger;
       pa.hits = D.hits.as<HitRec>();
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
@@ -1387,7 +1359,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       if (!(opt->flags & MSP_FLAG_WAVE_LAUNCHES)) {  // level-2 waves through the persistent pipeline
         rc = join_streams();  // (the previous batch's joins may still read the wave buffers)
         if (rc) return rc;
-        rc = ensure_pipeline_buffers(max_scr);
+        rc = ensure_wave_buffers(max_scr);
         if (rc) return rc;
         std::vector<WaveDesc> wds(lw.size());
         for (size_t wi = 0; wi < lw.size(); ++wi) {
@@ -1587,13 +1559,12 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
 
   // ---- totals
   CK(cudaEventRecord(D.ev[2], st));
-  std::vector<unsigned long long> bf(P.G), bh(P.G), zk(2 * (size_t)P.G);
+  std::vector<unsigned long long> bf(P.G), bh(P.G);
   unsigned long long nh = 0;
   int err = 0;
   if (P.G) {
     CK(cudaMemcpyAsync(bf.data(), D.bfilt.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(bh.data(), D.bhits.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(zk.data(), D.zkeys.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
@@ -1604,14 +1575,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   S.dev_ms_hot = hot_ms;
   S.hot_bytes = 8 * S.hot_pairs;  // algorithmic bytes: one 64-bit key written or read per candidate pair
   if (err) { set_err("join table region overflow (err=%d)", err); return MSP_INTERNAL; }
-  // real zero keys never reach the partitioned join (0 pads the scatter's runs): their hash hits
-  // are the per-batch product, and key 0 joins the recovery set (global-table batches count their
-  // own zeros and never touch zkeys)
-  std::vector<HitRec> zero_hits;
-  for (uint32_t g = 0; g < P.G; ++g) {
-    const unsigned long long zz = dropped[g] ? 0ull : zk[2 * (size_t)g] * zk[2 * (size_t)g + 1];
-    if (zz) { bh[g] += zz; zero_hits.push_back(HitRec{g, 0u, 0ull}); }
-  }
   for (uint32_t g = 0; g < P.G; ++g) { S.filtered_residuals += (int64_t)bf[g]; S.hash_hits += (int64_t)bh[g]; }
   if ((opt->flags & MSP_FLAG_BATCH_STATS) && P.G) {  // per-batch ValidationStats (validate.py:63-71)
     res->batch_stats = (int64_t *)malloc(sizeof(int64_t) * 5 * (size_t)P.G);
@@ -1637,7 +1600,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(cudaMemcpy(t2.data(), D.hits.as<HitRec>() + from, sizeof(HitRec) * t2.size(), cudaMemcpyDeviceToHost));
       hv.insert(hv.end(), t2.begin(), t2.end());
     }
-    hv.insert(hv.end(), zero_hits.begin(), zero_hits.end());
     mark("recovery start");
     rc = recover(hv);
     if (rc) return rc;

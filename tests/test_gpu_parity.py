@@ -488,8 +488,11 @@ def test_hit_list_regrowth_subprocess():
         "r = msb.solve(inst, msb.SolverConfig(mode='all'))\n"
         "print(json.dumps([len(r.solutions), r.stats.hash_hits, r.stats.batches]))\n"
     )
-    env = dict(__import__("os").environ, MSP_HIT_CAP="16")
-    here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
+    import os
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, MSP_HIT_CAP="16",
+               PYTHONPATH=os.pathsep.join([os.path.dirname(here), here, os.environ.get("PYTHONPATH", "")]))
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=here,
                          timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
