@@ -110,6 +110,7 @@ struct PartArgs {
   const uint32_t *gid;        // batch of each bucket
   uint32_t nb;                // buckets per role
   uint32_t roles;             // roles present in the launch's entries (0 means 2)
+  unsigned long long *zero_keys;  // per (batch, side): real keys equal to 0 (never staged: 0 pads runs)
   unsigned long long *dbg;    // diagnostics (MSP_DEBUG_STATS): rounds, staged, overflow, pads
   unsigned int *batch_ovf;    // per batch: a bucket overflowed -> re-join with the global table
   HitRec *hits; unsigned long long *nhits; uint64_t hit_cap;

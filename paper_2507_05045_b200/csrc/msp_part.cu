@@ -10,7 +10,7 @@
 //                  key's slot is its rank inside its bucket entry (no sort), flushing each round
 //                  as one coalesced run per bucket into the wave's scratch.  Right pairs that
 //                  overshoot d are counted, not written.
-//   join_bucket    one CTA per bucket: insert the build side's keys (the smaller side of the batch)
+//   join_group     one CTA per bucket: insert the build side's keys (the smaller side of the batch)
 //                  into a 16K-slot table in shared memory, stream the probe side's keys through
 //                  it, count hash hits, record each hit key once for recovery.
 //   k_waves        the persistent pipeline that runs both as tasks of one launch (one CTA per SM).
@@ -20,6 +20,7 @@
 // table path (msp_enum.cu), so results never depend on the partitioning.
 #include <cstdint>
 #include <algorithm>
+#include <cstddef>
 #include <mutex>
 #include <set>
 #include <type_traits>
@@ -56,16 +57,19 @@ constexpr int kUS = MSP_SCATTER_KEYS;                           // keys per lane
 // Shared memory of a scatter CTA (k_scatter / k_rescatter / scatter tasks of k_waves).  A CTA works
 // on one CHUNK at a time: consecutive tiles of ONE unit (one batch side), whose keys spread
 // uniformly over the unit's NB bucket entries.  A round's keys are bucketed in place: entry j owns
-// slots [j*C, j*C + C), C = kStageKeys / NB, and a key's slot is its rank within the entry (one
-// shared atomic), so the round needs no sort.  The round ends once a lane has staged its share of
-// MSP_STAGE_FILL_PCT % of the stage (no shared counter on the hot path); a key ranked past C -- rare at
-// that fill -- goes straight to its bucket region (one global atomic).  Bucket regions therefore
-// hold exactly `fill` real keys, densely: no padding, every key value (0 included) is a real key.
+// slots [j*C, j*C + C) (C even), C = kStageKeys / NB, and a key's slot is its rank within the
+// entry (one shared atomic), so the round needs no sort.  The round ends once a lane has staged its
+// share of MSP_STAGE_FILL_PCT % of the stage (no shared counter on the hot path); a key ranked past
+// C -- rare at that fill -- goes straight to its bucket region (one global atomic).  The flush
+// moves each entry's run to its bucket region with ONE bulk copy (cp.async.bulk, TMA): runs are
+// padded to an even length with key 0 so both ends stay 16-byte aligned; real keys equal to 0 are
+// never staged but counted per (batch, side) (zero_keys), and every reader skips key 0.
 // The producers' loop-vector buffers follow the struct (scatter only).
 struct __align__(16) Stage {
   unsigned long long key[kStageKeys];
-  uint32_t cnt[kMaxNB];              // keys ranked into each entry this round (> C: the rest spilled)
-  uint32_t round_end, chunk, tctr, pad;
+  uint32_t cnt[kMaxNB + 32];         // keys ranked into each entry this round (> C: the rest spilled);
+                                     // + one dummy counter per lane (never read)
+  uint32_t round_end, chunk, tctr, nstaged;
 };
 
 // Reservation of n slots at *p, result left in flight in r (predicated: no-op when n == 0, so no
@@ -81,7 +85,7 @@ size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps
 
 __device__ __forceinline__ void stage_init(Stage &g) {
   for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
-  if (threadIdx.x == 0) g.round_end = 0;
+  if (threadIdx.x == 0) { g.round_end = 0; g.nstaged = 0; }
 }
 
 // The CTA's next work chunk (dynamic: one global atomic per chunk), broadcast through shared memory.
@@ -98,43 +102,43 @@ __device__ __forceinline__ uint32_t next_chunk(Stage &g, unsigned int *ctr) {
 template <class T>
 __device__ __forceinline__ T sel(T const (&a)[2], uint32_t role) { return role ? a[1] : a[0]; }
 
-// A key ranked past its entry's C slots: straight to its bucket region (one global atomic + store).
+// A key ranked past its entry's C slots: straight to its bucket region (one global atomic, the key
+// and a pad).
 __device__ __forceinline__ void stage_spill(const PartArgs &S, uint32_t e, unsigned long long key) {
   const uint32_t role = e >= S.nb, b = e - role * S.nb;
-  const uint32_t pos = atomicAdd(sel(S.fill, role) + b, 1u);
-  if (pos < __ldg(sel(S.cap, role) + b)) __stcg(S.scratch + __ldg(sel(S.start, role) + b) + pos, key);
-  else atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+  const uint32_t pos = atomicAdd(sel(S.fill, role) + b, 2u);  // (even: the regions stay 16-byte aligned)
+  if (pos + 2 <= __ldg(sel(S.cap, role) + b)) {
+    unsigned long long *p = S.scratch + __ldg(sel(S.start, role) + b) + pos;
+    __stcg(p, key);
+    __stcg(p + 1, 0ull);
+  } else {
+    atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+  }
   if (S.dbg) atomicAdd(S.dbg + 13, 1ull);
 }
 
-// r = atomicAdd(p, 1) on shared memory when `on` (predicated: no branch, no convergence barrier);
-// r = ~0 otherwise.
-__device__ __forceinline__ uint32_t atom_inc_shared_if(uint32_t *p, bool on) {
-  uint32_t r = 0xFFFFFFFFu;
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q atom.shared.add.u32 %0, [%1], 1;\n\t}"
-               : "+r"(r)
-               : "r"(a), "r"((uint32_t)on)
-               : "memory");
-  return r;
-}
 
 // Stage N keys per lane into their entries j (local to the chunk's unit): rank (shared atomics,
 // all issued before any dependent store), then store into the entry's slots; keys ranked past C
 // (rare) are spilled in a separate, warp-uniform pass so the common path stays branch-free.
-// `staged` counts this lane's keys of the round; at `budget` the lane ends the round for the CTA.
+// `staged` counts this lane's keys of the round; at `budget` the lane ends the round for the CTA
+// (lanes stage at similar rates, so the stage is then ~half full and keys ranked past C stay rare:
+// an exact CTA-wide count to a fuller stage measured slower, its spills cost more than its rounds).
 template <int N>
 __device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t C,
                                            uint32_t &staged, uint32_t budget,
                                            const unsigned long long (&key)[N], const uint32_t (&j)[N],
                                            const bool (&ok)[N]) {
+  // every lane ranks every key (no predicated atomic, which would become a branch): a key that is
+  // not staged ranks itself in the lane's own dummy counter past the entries instead
+  const uint32_t dummy = kMaxNB + (threadIdx.x & 31);
   uint32_t r[N];
 #pragma unroll
-  for (int u = 0; u < N; ++u) r[u] = atom_inc_shared_if(&g.cnt[j[u]], ok[u]);
+  for (int u = 0; u < N; ++u) r[u] = atomicAdd(&g.cnt[ok[u] ? j[u] : dummy], 1u);
   bool spill = false;
 #pragma unroll
   for (int u = 0; u < N; ++u) {
-    if (r[u] < C) g.key[j[u] * C + r[u]] = key[u];  // (r == ~0 when !ok)
+    if (ok[u] && r[u] < C) g.key[j[u] * C + r[u]] = key[u];
     spill |= ok[u] && r[u] >= C;
     staged += ok[u] ? 1u : 0u;
   }
@@ -146,60 +150,57 @@ __device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t
   if (staged >= budget) *(volatile uint32_t *)&g.round_end = 1u;
 }
 
-// Called by every thread after a barrier that ends the round: warp w owns entries w, w + W, ...
-// (W = warps); its lanes reserve one scratch range per nonempty entry (global atomics, all in
-// flight at once), then the warp writes each entry's run (consecutive lanes store consecutive
-// keys, two per lane per step) and clears the entry's count.  Ends with a barrier.
+// Generic-proxy shared-memory writes (the staged keys) made visible to the async proxy (TMA).
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Bulk copy (TMA) of `bytes` (multiple of 16) from shared memory to global memory, 16-byte aligned
+// ends; the issuing thread waits for it with bulk_wait_read() before the source is rewritten.
+__device__ __forceinline__ void bulk_store(unsigned long long *dst, const unsigned long long *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               :: "l"(dst), "r"((uint32_t)__cvta_generic_to_shared(src)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// Called by every thread after a barrier that ends the round (every thread fenced its staged
+// writes for the async proxy before it): one lane per nonempty entry reserves the entry's run,
+// padded to even length with key 0, in its bucket region (global atomics, all in flight at once)
+// and moves it with one bulk copy; the issuing lanes wait until the copies have read the stage,
+// then the stage is free again.  Ends with a barrier.
 __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_t ebase, uint32_t NB, uint32_t C) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t tid = threadIdx.x;
   const uint32_t nb = S.nb;
-  constexpr uint32_t kW = kScatterThreads / 32;
-  for (uint32_t j0 = warp; j0 < NB; j0 += 32 * kW) {
-    const uint32_t j = j0 + lane * kW;
-    uint32_t n = 0, dst = 0, pos = 0;
-    uint32_t *fp = nullptr;
-    if (j < NB) {
-      n = min(g.cnt[j], C);
-      g.cnt[j] = 0u;
-      const uint32_t e = ebase + j, role = e >= nb;
-      fp = sel(S.fill, role) + (e - role * nb);
+  bool issued = false;
+  for (uint32_t j = tid; j < NB; j += kScatterThreads) {
+    uint32_t n = min(g.cnt[j], C);
+    g.cnt[j] = 0u;
+    if (!n) continue;
+    const uint32_t e = ebase + j, role = e >= nb, b = e - role * nb;
+    const uint32_t ne = (n + 1u) & ~1u;
+    const uint32_t pos = atomicAdd(sel(S.fill, role) + b, ne);
+    if (pos + ne <= __ldg(sel(S.cap, role) + b)) {
+      unsigned long long *src = g.key + j * C;
+      if (ne != n) { src[n] = 0ull; fence_proxy_async_smem(); }  // the pad (n odd => n < C)
+      bulk_store(S.scratch + __ldg(sel(S.start, role) + b) + pos, src, ne * 8u);
+      issued = true;
+    } else {
+      atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
+      if (S.dbg) atomicAdd(S.dbg + 12, 1ull);
     }
-    reserve_async(pos, fp, n);
-    if (n) {
-      const uint32_t e = ebase + j, role = e >= nb, b = e - role * nb;
-      if (pos + n <= __ldg(sel(S.cap, role) + b)) {
-        dst = __ldg(sel(S.start, role) + b) + pos;
-      } else {
-        atomicOr(S.batch_ovf + __ldg(S.gid + b), 1u);
-        if (S.dbg) atomicAdd(S.dbg + 12, 1ull);
-        n = 0;
-      }
-      if (S.dbg) atomicAdd(S.dbg + 1, (unsigned long long)n);
-    }
-    uint32_t todo = __ballot_sync(0xffffffffu, n != 0u);
-    while (todo) {
-      const uint32_t src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t nn = __shfl_sync(0xffffffffu, n, src);
-      unsigned long long *to = S.scratch + __shfl_sync(0xffffffffu, dst, src);
-      const unsigned long long *from = g.key + (j0 + src * kW) * C;
-      for (uint32_t i = lane; i < nn; i += 64) {
-        const unsigned long long k0 = from[i];
-        const bool two = i + 32 < nn;
-        const unsigned long long k1 = two ? from[i + 32] : 0ull;
-        __stcg(to + i, k0);
-        if (two) __stcg(to + i + 32, k1);
-      }
-    }
+    if (S.dbg) atomicAdd(S.dbg + 1, (unsigned long long)n);
+  }
+  if (issued) {
+    bulk_commit();
+    bulk_wait_read();
   }
   if (S.dbg && tid == 0) atomicAdd(S.dbg + 0, 1ull);
-  if (tid == 0) g.round_end = 0u;
+  if (tid == 0) { g.round_end = 0u; g.nstaged = 0u; }
   __syncthreads();
 }
 
 // Stage slots per entry of a unit with NB buckets, and each lane's share of a round.
 __device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_t &budget) {
-  C = kStageKeys / NB;
+  C = (kStageKeys / NB) & ~1u;  // even: every entry's run starts 16-byte aligned
   budget = max(1u, NB * C * MSP_STAGE_FILL_PCT / (100u * kScatterThreads));
 }
 
@@ -263,10 +264,28 @@ __device__ __forceinline__ uint4 ld_tile(const TileDesc *t, uint32_t i, uint32_t
 }
 
 // FNV fold step (validate.py:40-42) on (lo, hi) for v < 2^32: (h ^ v) * (2^40 + 435) mod 2^64.
+// Written so that each state word has a two-instruction dependency chain per step: lo' = low(x *
+// 435) after x = lo ^ v; hi' = hi * 435 + high(x * 435) + (x << 8), where hi * 435 does not wait
+// for x and the shift is a byte permute (ALU pipe, not an IMAD the FMA pipe would also carry).
+#ifndef MSP_FOLD_PTX
+#define MSP_FOLD_PTX 0
+#endif
 __device__ __forceinline__ void fold(uint32_t &lo, uint32_t &hi, uint32_t v) {
+#if MSP_FOLD_PTX
+  asm("{\n\t.reg .u32 x, t1, t3, c;\n\t.reg .u64 p;\n\t"
+      "xor.b32 x, %0, %2;\n\t"
+      "mul.lo.u32 t1, %1, 435;\n\t"
+      "mul.wide.u32 p, x, 435;\n\t"
+      "prmt.b32 t3, x, 0, 0x2104;\n\t"
+      "mov.b64 {%0, c}, p;\n\t"
+      "add.u32 t1, t1, c;\n\t"
+      "add.u32 %1, t1, t3;\n\t}"
+      : "+r"(lo), "+r"(hi) : "r"(v));
+#else
   const uint32_t x = lo ^ v;
   hi = hi * 435u + __umulhi(x, 435u) + (x << 8);
   lo = x * 435u;
+#endif
 }
 
 // Companion-vector loads of one tile for this lane: its lane entry and its (lane-th) loop entry.
@@ -294,6 +313,7 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
   unsigned long long key[kUS];
   uint32_t j[kUS];
   bool ok[kUS];
+  uint32_t nzero = 0;
 #pragma unroll
   for (int u = 0; u < kUS; ++u) {
     uint32_t yv[SW];
@@ -317,9 +337,13 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
       fold(lo, hi, (c & 1) ? (w >> 16) & (RIGHT ? 0x7FFFu : 0xFFFFu) : w & (RIGHT ? 0x7FFFu : 0xFFFFu));
     }
     key[u] = ((unsigned long long)hi << 32) | lo;
-    ok[u] = in;
+    const bool z = in && (hi | lo) == 0u;  // a real key 0: counted per (batch, side), never staged
+    nzero += z ? 1u : 0u;
+    ok[u] = in && !z;
     j[u] = __umulhi(hi, nbk);  // bucket within the unit = floor(hi * NB / 2^32)
   }
+  if (__any_sync(0xffffffffu, nzero != 0u) && nzero)
+    atomicAdd(S.zero_keys + 2 * ui.gid + (RIGHT ? 1u : 0u), (unsigned long long)nzero);
   if (diag) {
 #pragma unroll
     for (int u = 0; u < kUS; ++u) dacc ^= ok[u] ? key[u] : 0ull;
@@ -397,6 +421,7 @@ __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const Sc
         }
       }
     }
+    fence_proxy_async_smem();  // the round's staged keys -> the flush's bulk copies
     const bool more = __syncthreads_or(have);
     flush_round(g, S, ebase, nbk, C);
     staged = 0;
@@ -463,7 +488,7 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
 #pragma unroll
       for (int u = 0; u < N; ++u) {
         key[u] = nxt[u];
-        ok[u] = idx + u * stride < s1;
+        ok[u] = idx + u * stride < s1 && key[u] != 0ull;  // (0: a run pad)
         const uint32_t x = idx + (N + u) * stride;
         nxt[u] = x < s1 ? __ldcs(src.keys + x) : 0ull;
       }
@@ -472,6 +497,7 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
       stage_keys<N>(g, S, ebase, C, staged, budget, key, j, ok);
       idx += N * stride;
     }
+    fence_proxy_async_smem();
     const bool more = __syncthreads_or(idx - lane < s1);
     flush_round(g, S, ebase, NB, C);
     staged = 0;
@@ -495,38 +521,71 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_rescatter(con
   }
 }
 
-#ifndef MSP_JOIN_U
-#define MSP_JOIN_U 4
-#endif
 constexpr int kJoinThreads = 1024;
-constexpr int kJoinSlots = 1 << kJoinSlotsLog2;        // 16K key slots
+constexpr int kJoinSlots = 1 << kJoinSlotsLog2;        // 16K table slots
 constexpr int kJWays = 8;                               // slots per table bucket
 constexpr int kJBuckets = kJoinSlots / kJWays;          // 2K buckets of 8 slots
 constexpr int kStash = 256;                             // keys whose two buckets were both full
 constexpr int kHitWords = (kJoinSlots + kStash) / 32;
 constexpr int kJQueue = 1024;                           // deferred probes per bucket (then inline)
+constexpr int kBuildBuf = 9728;                         // build keys of one bucket in shared memory
+constexpr int kProbeChunk = 4096;                       // probe keys per streamed chunk (2 buffers)
 
-// Shared-memory join table of one bucket: 8-slot buckets, first fit in bucket b1, then b2, then a
-// small stash.  Each slot keeps the full 64-bit key and a fingerprint byte 0x80 | 7 key bits (0 =
-// empty); the eight fingerprints of a bucket are one 64-bit word.  An insert is one shared atomic
-// + two stores; a probe reads ONE fingerprint word and tests all eight bytes at once, reading full
-// keys only on a fingerprint match (~2% of probes plus the true hits).  A key sits in b2 only if b1
-// was full (slot 7's marker bit, the word's sign bit), so b2 is read only by probes whose b1 is
-// full.  b1/b2 come from a multiplicative mix of the key's low word, the fingerprint from its high
-// word (whose top bits chose the partition bucket).  Only counts and fingerprints are cleared per
-// bucket.
+// Shared-memory join of one partition bucket.  The table has 8-slot buckets, first fit in bucket
+// b1, then b2, then a small stash; a slot holds a fingerprint byte 0x80 | 7 key bits (0 = empty;
+// the eight of a bucket are one 64-bit word) and the 16-bit index of its key in the bucket's build
+// region.  An insert is one shared atomic + two small stores; a probe reads ONE fingerprint word and
+// tests all eight bytes at once (branch-free); the ~2% of probes whose test does not rule a match
+// out are queued and counted exactly at the end of the bucket, comparing full keys read back from
+// the build region in global memory.  A key sits in b2 only if b1 was full (slot 7's marker bit,
+// the word's sign bit).  b1/b2 come from a multiplicative mix of the key's low word, the
+// fingerprint from its high word (whose top bits chose the partition bucket).
+// Keys move by TMA bulk copies (cp.async.bulk + mbarrier): a bucket's build keys land in `bkeys`
+// while the previous bucket is still probing, its probe keys stream through two `pkeys` chunks.
 struct JoinSmem {
-  unsigned long long key[kJBuckets][kJWays];
   unsigned long long fp[kJBuckets];     // eight fingerprint bytes
   uint32_t cnt[kJBuckets];              // claims (may exceed 8: failed claims move on)
-  unsigned long long stash[kStash];
+  uint16_t idx[kJBuckets][kJWays];      // build-region index of each slot's key
+  uint16_t stash[kStash];               // build-region indices of stashed keys
   uint32_t hitbits[kHitWords];
+  unsigned long long queue[kJQueue];    // per-warp segments: probe keys whose fast test did not rule
+                                        // out a match
   unsigned long long bhits[kJoinThreads / 32];
-  unsigned long long queue[kJQueue];    // probe keys whose fast test did not rule out a match
-  uint32_t nstash, ovf, nq, pad;
+  unsigned long long mbar[3];           // build keys, probe chunk buffers 0 / 1
+  uint32_t nstash, ovf, pad[2];
+  alignas(16) unsigned long long bkeys[kBuildBuf];       // (bulk-copy destinations: 16-byte aligned)
+  alignas(16) unsigned long long pkeys[2][kProbeChunk];
 };
+static_assert(offsetof(JoinSmem, bkeys) % 16 == 0 && offsetof(JoinSmem, pkeys) % 16 == 0, "bulk copy alignment");
 
 size_t join_smem_bytes() { return sizeof(JoinSmem); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_inval(unsigned long long *b) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" :: "r"(smem_u32(b)) : "memory");
+}
+// Thread 0: expect `bytes` on barrier b and copy them from global src to shared dst (bulk copies of
+// <= 32 KB, 16-byte aligned ends).
+__device__ __forceinline__ void bulk_load(unsigned long long *dst, const unsigned long long *src, uint32_t bytes,
+                                          unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+  for (uint32_t o = 0; o < bytes; o += 32768u) {
+    const uint32_t n = min(32768u, bytes - o);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst) + o), "l"(reinterpret_cast<const char *>(src) + o), "r"(n), "r"(smem_u32(bar))
+                 : "memory");
+  }
+}
+// Every thread: wait for the completion of phase `parity` of barrier b.
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
+}
 
 __device__ __forceinline__ uint32_t jmix(unsigned long long k) { return (uint32_t)k * 0x9E3779B1u; }
 __device__ __forceinline__ uint32_t jb1(uint32_t t) { return t >> 21; }
@@ -542,36 +601,29 @@ __device__ __forceinline__ uint32_t zero_byte_mask32(uint32_t x) {
 // Some byte of x is zero (exact for presence).
 __device__ __forceinline__ uint32_t has_zero_byte(uint32_t x) { return (x - 0x01010101u) & ~x & 0x80808080u; }
 
-__device__ __forceinline__ void join_insert_slow(JoinSmem &T, unsigned long long k, uint32_t t, uint32_t fpb) {
-  const uint32_t b = jb2(t), s = atomicAdd(&T.cnt[b], 1u);
+// Insert the key k found at build-region index i.
+__device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k, uint32_t i) {
+  const uint32_t t = jmix(k), fpb = jfp4(k) & 0xFFu;
+  uint32_t b = jb1(t), s = atomicAdd(&T.cnt[b], 1u);
+  if (s >= (uint32_t)kJWays) { b = jb2(t); s = atomicAdd(&T.cnt[b], 1u); }
   if (s < (uint32_t)kJWays) {
-    T.key[b][s] = k;
-    reinterpret_cast<uint8_t *>(&T.fp[b])[s] = (uint8_t)fpb;
-  } else {
-    const uint32_t i = atomicAdd(&T.nstash, 1u);
-    if (i < (uint32_t)kStash) T.stash[i] = k; else T.ovf = 1u;
-  }
-}
-
-__device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
-  const uint32_t t = jmix(k), b = jb1(t), fpb = jfp4(k) & 0xFFu;
-  const uint32_t s = atomicAdd(&T.cnt[b], 1u);
-  if (s < (uint32_t)kJWays) {
-    T.key[b][s] = k;
+    T.idx[b][s] = (uint16_t)i;
     reinterpret_cast<uint8_t *>(&T.fp[b])[s] = (uint8_t)fpb;  // slot s is this thread's alone
   } else {
-    join_insert_slow(T, k, t, fpb);
+    const uint32_t q = atomicAdd(&T.nstash, 1u);
+    if (q < (uint32_t)kStash) T.stash[q] = (uint16_t)i; else T.ovf = 1u;
   }
 }
 
-// Copies of k among the slots of bucket b whose fingerprint byte matches.
-__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, unsigned long long w, uint32_t pat,
-                                                unsigned long long k, uint32_t &c, uint32_t &first) {
+// Copies of k among the slots of bucket b whose fingerprint byte matches (full keys from global).
+__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, const unsigned long long *bk, uint32_t b,
+                                                unsigned long long w, uint32_t pat, unsigned long long k,
+                                                uint32_t &c, uint32_t &first) {
   unsigned long long m = ((unsigned long long)zero_byte_mask32((uint32_t)(w >> 32) ^ pat) << 32) |
                          zero_byte_mask32((uint32_t)w ^ pat);
   while (m) {
     const uint32_t s = (uint32_t)(__ffsll((long long)m) - 1) >> 3;
-    if (T.key[b][s] == k) {
+    if (__ldg(bk + T.idx[b][s]) == k) {
       if (!c) first = b * kJWays + s;
       ++c;
     }
@@ -579,146 +631,179 @@ __device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, u
   }
 }
 
-// Multiplicity of k in the table (slow path: some fingerprint byte of b1 matches, or b1 is full);
-// `first` = slot id of its first copy (b1, then b2, then stash).
-__device__ __forceinline__ uint32_t join_count_slow(const JoinSmem &T, unsigned long long k, uint32_t nstash,
-                                                 uint32_t &first) {
+// Multiplicity of k among the build keys (b1, b2 if b1 is full, the stash if b2 is full too);
+// `first` = slot id of its first copy.
+__device__ __forceinline__ uint32_t join_count_slow(const JoinSmem &T, const unsigned long long *bk,
+                                                    unsigned long long k, uint32_t nstash, uint32_t &first) {
   const uint32_t t = jmix(k), b1 = jb1(t), pat = jfp4(k);
   const unsigned long long w1 = T.fp[b1];
   first = 0xFFFFFFFFu;
   uint32_t c = 0;
-  count_in_bucket(T, b1, w1, pat, k, c, first);
+  count_in_bucket(T, bk, b1, w1, pat, k, c, first);
   if ((long long)w1 < 0) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
     const uint32_t b2 = jb2(t);
     const unsigned long long w2 = T.fp[b2];
-    count_in_bucket(T, b2, w2, pat, k, c, first);
+    count_in_bucket(T, bk, b2, w2, pat, k, c, first);
     if ((long long)w2 < 0)
       for (uint32_t i = 0; i < nstash; ++i)
-        if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
+        if (__ldg(bk + T.stash[i]) == k) { if (!c) first = kJoinSlots + i; ++c; }
   }
   return c;
 }
 
-// Join of bucket b of a wave by one CTA of NT threads: clear the table, insert the build keys,
-// probe with the probe keys (fastval.py:75-107 semantics: every full-64-bit-hash-equal pair is a
-// hit), record each hit key once, reset the bucket's fill counters for the next use of the buffer.
-// The regions hold exactly min(fill, cap) real keys (fill > cap flagged the batch).  Ends with a
-// barrier.
+// Join of buckets [b0, b1) of a wave by one CTA of NT threads (fastval.py:75-107 semantics: every
+// full-64-bit-hash-equal (build, probe) pair is a hit; each hit key is recorded once for the exact
+// confirmation), resetting each bucket's fill counters for the next use of the scratch buffer.  The
+// regions hold min(fill, cap) keys, run pads (key 0) among them (fill > cap flagged the batch).
+// Per bucket: its build keys are already landing in bkeys (prefetched during the previous bucket's
+// probe, or issued here), its first two probe chunks are issued at the start; clear the table;
+// insert; prefetch the next bucket's build keys; stream the probe chunks; count the queued probes
+// exactly.  Ends with a barrier.
+// (MSP_JOIN_INLINE=__noinline__ gives the join its own register allocation: measured slower)
+#ifndef MSP_JOIN_INLINE
+#define MSP_JOIN_INLINE __forceinline__
+#endif
 template <int NT>
-__device__ __forceinline__ void join_bucket(JoinSmem &T, const PartArgs &S, uint32_t b) {
-  const uint32_t tid = threadIdx.x;
-  constexpr int U = MSP_JOIN_U;  // keys loaded per thread before the table operations
-  long long tp0 = 0, tp1 = 0, tp2 = 0;
-  if (S.dbg && tid == 0) tp0 = clock64();
-  for (uint32_t i = tid; i < (uint32_t)kJBuckets / 4; i += NT) reinterpret_cast<uint4 *>(T.cnt)[i] = make_uint4(0, 0, 0, 0);
-  for (uint32_t i = tid; i < (uint32_t)kJBuckets / 2; i += NT) reinterpret_cast<uint4 *>(T.fp)[i] = make_uint4(0, 0, 0, 0);
-  for (uint32_t i = tid; i < (uint32_t)kHitWords; i += NT) T.hitbits[i] = 0u;
-  if (tid == 0) { T.nstash = 0; T.ovf = 0; T.nq = 0; }
-  const uint32_t gid = __ldg(S.gid + b);
-  const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
-  const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
-  const unsigned long long *bk = S.scratch + __ldg(S.start[0] + b);
-  const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
-  unsigned long long kv[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {  // first build keys in flight across the clear
-    const uint32_t i = u * NT + tid;
-    kv[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
-  }
+__device__ MSP_JOIN_INLINE void join_group(JoinSmem &T, const PartArgs &S, uint32_t b0, uint32_t b1) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) { mbar_init(&T.mbar[0]); mbar_init(&T.mbar[1]); mbar_init(&T.mbar[2]); }
   __syncthreads();
-  for (uint32_t base = 0; base < nbuild; base += NT * U) {
-    unsigned long long nx[U];  // next keys in flight while this batch is inserted
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = base + NT * U + u * NT + tid;
-      nx[u] = i < nbuild ? __ldcs(bk + i) : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (base + u * NT + tid < nbuild) join_insert(T, kv[u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) kv[u] = nx[u];
-  }
-#pragma unroll
-  for (int u = 0; u < U; ++u) {  // first probe keys in flight across the barrier
-    const uint32_t i = u * NT + tid;
-    kv[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
-  }
-  __syncthreads();
-  if (S.dbg && tid == 0) tp1 = clock64();
-  const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
-  if (T.ovf && tid == 0) { atomicOr(S.batch_ovf + gid, 1u); if (S.dbg) atomicAdd(S.dbg + 14, 1ull); }
-  uint32_t hits = 0;
-  // a probe hit: count it, record the key once (first copy's slot) for the exact confirmation
-  auto probe_slow = [&](unsigned long long k) {
-    uint32_t first;
-    const uint32_t c = join_count_slow(T, k, nstash, first);
-    if (c) {
-      hits += c;
-      if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
-        const unsigned long long h = atomicAdd(S.nhits, 1ull);
-        if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
+  uint32_t ph_b = 0, ph_p0 = 0, ph_p1 = 0;  // barrier phases (every thread tracks them alike)
+  bool build_ready = false;                 // this bucket's build keys were prefetched
+  for (uint32_t b = b0; b < b1; ++b) {
+    long long tp0 = 0, tp1 = 0, tp2 = 0;
+    if (S.dbg && tid == 0) tp0 = clock64();
+    const uint32_t gid = __ldg(S.gid + b);
+    const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
+    const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
+    const unsigned long long *bk = S.scratch + __ldg(S.start[0] + b);
+    const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
+    const uint32_t npc = (nprobe + kProbeChunk - 1) / kProbeChunk;  // probe chunks
+    const bool oversized = nbuild > 65535u;  // 16-bit slot indices: the batch goes to the global table
+    if (tid == 0) {
+      fence_proxy_async_smem();  // (generic accesses of the buffers before -> async writes)
+      if (!build_ready && nbuild && !oversized)
+        bulk_load(T.bkeys, bk, 8u * min((nbuild + 1u) & ~1u, (uint32_t)kBuildBuf), &T.mbar[0]);
+      for (uint32_t c = 0; c < 2 && c < npc; ++c) {
+        const uint32_t n = min(nprobe - c * kProbeChunk, (uint32_t)kProbeChunk);
+        bulk_load(T.pkeys[c], pk + c * kProbeChunk, 8u * ((n + 1u) & ~1u), &T.mbar[1 + c]);
       }
     }
-  };
-  const uint32_t lane = tid & 31;
-  for (uint32_t base = 0; base < nprobe; base += NT * U) {
-    unsigned long long nx[U];  // next keys in flight while this batch is probed
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = base + NT * U + u * NT + tid;
-      nx[u] = i < nprobe ? __ldcs(pk + i) : 0ull;
+    for (uint32_t i = tid; i < (uint32_t)kJBuckets / 4; i += NT) reinterpret_cast<uint4 *>(T.cnt)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = tid; i < (uint32_t)kJBuckets / 2; i += NT) reinterpret_cast<uint4 *>(T.fp)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = tid; i < (uint32_t)kHitWords; i += NT) T.hitbits[i] = 0u;
+    if (tid == 0) { T.nstash = 0; T.ovf = 0; }
+    __syncthreads();
+    // ---- build: pieces of <= kBuildBuf keys through bkeys (one piece unless the bucket is oversized)
+    if (oversized) {
+      if (tid == 0) atomicOr(S.batch_ovf + gid, 1u);
+    } else {
+      for (uint32_t p0 = 0; p0 < nbuild; p0 += kBuildBuf) {
+        if (p0) {  // a later piece (oversized bucket): load it now
+          if (tid == 0) {
+            fence_proxy_async_smem();
+            bulk_load(T.bkeys, bk + p0, 8u * ((min(nbuild - p0, (uint32_t)kBuildBuf) + 1u) & ~1u), &T.mbar[0]);
+          }
+        }
+        mbar_wait(&T.mbar[0], ph_b);
+        ph_b ^= 1u;
+        const uint32_t pn = min(nbuild - p0, (uint32_t)kBuildBuf);
+        for (uint32_t i = tid; i < pn; i += NT) {
+          const unsigned long long k = T.bkeys[i];
+          if (k != 0ull) join_insert(T, k, p0 + i);  // (0: a run pad)
+        }
+        __syncthreads();
+      }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      // fast test, branch-free: no fingerprint byte of b1 matches and b1 is not full -> no copy of k
-      const unsigned long long k = kv[u];
-      const uint32_t pat = jfp4(k);
-      const unsigned long long w = T.fp[jb1(jmix(k))];
-      const bool maybe = ((has_zero_byte((uint32_t)w ^ pat) | has_zero_byte((uint32_t)(w >> 32) ^ pat)) != 0u ||
-                          (long long)w < 0) && base + u * NT + tid < nprobe;
-      const uint32_t mm = __ballot_sync(0xffffffffu, maybe);
-      if (mm) {  // defer the exact count (warp-aggregated append): no divergent slow path here
-        uint32_t q0 = 0;
-        if (lane == (uint32_t)(__ffs(mm) - 1)) q0 = atomicAdd(&T.nq, (uint32_t)__popc(mm));
-        q0 = __shfl_sync(0xffffffffu, q0, __ffs(mm) - 1);
-        if (maybe) {
-          const uint32_t qi = q0 + __popc(mm & ((1u << lane) - 1u));
-          if (qi < (uint32_t)kJQueue) T.queue[qi] = k;
-          else probe_slow(k);  // queue full (duplicate-heavy bucket)
+    build_ready = false;
+    if (b + 1 < b1 && tid == 0) {  // prefetch the next bucket's build keys while this one probes
+      const uint32_t nb2 = min(S.fill[0][b + 1], __ldg(S.cap[0] + b + 1));
+      if (nb2 && nb2 <= (uint32_t)kBuildBuf) {
+        fence_proxy_async_smem();
+        bulk_load(T.bkeys, S.scratch + __ldg(S.start[0] + b + 1), 8u * ((nb2 + 1u) & ~1u), &T.mbar[0]);
+      }
+    }
+    if (b + 1 < b1) {
+      const uint32_t nb2 = min(S.fill[0][b + 1], __ldg(S.cap[0] + b + 1));
+      build_ready = nb2 && nb2 <= (uint32_t)kBuildBuf;
+    }
+    if (S.dbg && tid == 0) tp1 = clock64();
+    const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
+    if (T.ovf && tid == 0) { atomicOr(S.batch_ovf + gid, 1u); if (S.dbg) atomicAdd(S.dbg + 14, 1ull); }
+    uint32_t hits = 0;
+    auto probe_slow = [&](unsigned long long k) {  // a possible hit: count it, record the key once
+      uint32_t first;
+      const uint32_t c = join_count_slow(T, bk, k, nstash, first);
+      if (c) {
+        hits += c;
+        if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
+          const unsigned long long h = atomicAdd(S.nhits, 1ull);
+          if (h < S.hit_cap) S.hits[h] = HitRec{gid, 0u, k};
+        }
+      }
+    };
+    // ---- probe: chunks c through pkeys[c & 1]; possible hits go to the warp's own queue segment
+    constexpr uint32_t kQW = kJQueue / (NT / 32);
+    unsigned long long *qw = T.queue + (tid >> 5) * kQW;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t nqw = 0;  // (warp-uniform)
+    for (uint32_t c = 0; c < npc; ++c) {
+      const uint32_t pb = c & 1u;
+      mbar_wait(&T.mbar[1 + pb], pb ? ph_p1 : ph_p0);
+      if (pb) ph_p1 ^= 1u; else ph_p0 ^= 1u;
+      const uint32_t n = min(nprobe - c * kProbeChunk, (uint32_t)kProbeChunk);
+      const unsigned long long *pc = T.pkeys[pb];
+      for (uint32_t i = tid; i - lane < n; i += NT) {  // (whole warps iterate: the exit is warp-uniform)
+        // fast test, branch-free: no fingerprint byte of b1 matches and b1 is not full -> no copy
+        const unsigned long long k = pc[min(i, n - 1)];
+        const uint32_t pat = jfp4(k);
+        const unsigned long long w = T.fp[jb1(jmix(k))];
+        const bool maybe = ((has_zero_byte((uint32_t)w ^ pat) | has_zero_byte((uint32_t)(w >> 32) ^ pat)) != 0u ||
+                            (long long)w < 0) && i < n && k != 0ull;
+        const uint32_t mm = __ballot_sync(0xffffffffu, maybe);
+        const uint32_t qi = nqw + __popc(mm & lt);
+        if (maybe && qi < kQW) qw[qi] = k;  // deferred exact count: no divergent slow path here
+        nqw += __popc(mm);
+        if (nqw > kQW && __any_sync(0xffffffffu, maybe && qi >= kQW))
+          if (maybe && qi >= kQW) probe_slow(k);  // the warp's segment is full (duplicate-heavy bucket)
+      }
+      if (c + 2 < npc) {  // refill this buffer with chunk c + 2 once every thread is done with it
+        __syncthreads();
+        if (tid == 0) {
+          fence_proxy_async_smem();
+          const uint32_t n2 = min(nprobe - (c + 2) * kProbeChunk, (uint32_t)kProbeChunk);
+          bulk_load(T.pkeys[pb], pk + (c + 2) * kProbeChunk, 8u * ((n2 + 1u) & ~1u), &T.mbar[1 + pb]);
         }
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) kv[u] = nx[u];
+    for (uint32_t i = lane; i < min(nqw, kQW); i += 32) probe_slow(qw[i]);
+    const unsigned long long wh = warp_sum((unsigned long long)hits);
+    if (lane == 0) T.bhits[tid >> 5] = wh;
+    __syncthreads();
+    if (S.dbg && tid == 0) {
+      tp2 = clock64();
+      atomicAdd(S.dbg + 8, (unsigned long long)(tp1 - tp0));
+      atomicAdd(S.dbg + 9, (unsigned long long)(tp2 - tp1));
+      atomicAdd(S.dbg + 10, (unsigned long long)nstash);
+      atomicAdd(S.dbg + 11, 1ull);
+    }
+    if (tid == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < NT / 32; ++w) t += T.bhits[w];
+      if (t) atomicAdd(S.batch_hits + gid, t);
+      S.fill[0][b] = 0;
+      S.fill[1][b] = 0;
+    }
   }
   __syncthreads();
-  const uint32_t nq = min(T.nq, (uint32_t)kJQueue);
-  for (uint32_t i = tid; i < nq; i += NT) probe_slow(T.queue[i]);
-  const unsigned long long wh = warp_sum((unsigned long long)hits);
-  if ((tid & 31) == 0) T.bhits[tid >> 5] = wh;
-  __syncthreads();
-  if (S.dbg && tid == 0) {
-    tp2 = clock64();
-    atomicAdd(S.dbg + 8, (unsigned long long)(tp1 - tp0));
-    atomicAdd(S.dbg + 9, (unsigned long long)(tp2 - tp1));
-    atomicAdd(S.dbg + 10, (unsigned long long)nstash);
-    atomicAdd(S.dbg + 11, 1ull);
-  }
-  if (tid == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < NT / 32; ++w) t += T.bhits[w];
-    if (t) atomicAdd(S.batch_hits + gid, t);
-    S.fill[0][b] = 0;
-    S.fill[1][b] = 0;
-  }
+  if (tid == 0) { mbar_inval(&T.mbar[0]); mbar_inval(&T.mbar[1]); mbar_inval(&T.mbar[2]); }
   __syncthreads();
 }
 
 __global__ void __launch_bounds__(kJoinThreads, 1) k_join(const PartArgs S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   JoinSmem &T = *reinterpret_cast<JoinSmem *>(smem_raw);
-  for (uint32_t b = blockIdx.x; b < S.nb; b += gridDim.x) join_bucket<kJoinThreads>(T, S, b);
+  for (uint32_t b = blockIdx.x; b < S.nb; b += gridDim.x) join_group<kJoinThreads>(T, S, b, b + 1);
 }
 
 // ---------------------------------------------------------------- persistent wave pipeline
@@ -810,8 +895,7 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
     S.roles = 2;
     if (tk >> 63) {  // join: buckets [idx, idx + kJoinGroup) of the wave
       const uint32_t b1 = min(idx + (uint32_t)kJoinGroup, wd.nb);
-      for (uint32_t b = idx; b < b1; ++b) join_bucket<kScatterThreads>(T, S, b);
-      __syncthreads();  // (join_bucket ended with one; the CTA's writes are ordered before the release)
+      join_group<kScatterThreads>(T, S, idx, b1);  // (ends with a barrier: the CTA's writes are ordered before the release)
       if (tid == 0) { __threadfence(); atomicAdd(W.join_done + w, 1u); }
       if (tid == 0 && W.pa.dbg) { const long long now = clock64(); atomicAdd(W.pa.dbg + 5, (unsigned long long)(now - t_prev)); t_prev = now; }
     } else {  // scatter chunk idx of the wave (tiles, or a level-2 slot range of a coarse region)

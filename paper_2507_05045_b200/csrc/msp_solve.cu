@@ -81,7 +81,7 @@ struct Device {
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
   DBuf rkeys, runits, rfilt, rhits;
-  DBuf bfilt, bhits, bovf, scratch, bk, bruns, fill, dbg;
+  DBuf bfilt, bhits, bovf, scratch, bk, bruns, fill, zkeys, dbg;
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   uint64_t hit_cap = 0;  // distinct hit keys the hit list holds (grown on overflow, fastval.py:126-139)
@@ -103,7 +103,7 @@ struct Device {
     DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
-                   &bfilt, &bhits, &bovf, &scratch, &bk, &bruns, &fill, &cscratch[0], &cscratch[1],
+                   &bfilt, &bhits, &bovf, &zkeys, &scratch, &bk, &bruns, &fill, &cscratch[0], &cscratch[1],
                    &cfill, &cbk, &hunits, &l2bk, &l2src, &tdesc, &gstb, &gsu, &uinfo,
                    &chunks, &cchunks, &l2chunks, &cctr, &cfirst, &ccfirst, &tchunks, &wdesc, &wctr, &tasks};
     for (DBuf *b : all) b->release();
@@ -521,6 +521,15 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 
 uint32_t even_up(double x) { const uint32_t v = (uint32_t)x; return v + (v & 1u); }
 
+// Capacity of a bucket region holding `mean` keys on average (multinomial spread: mean + 7 sigma)
+// plus the key-0 pads of the scatter's even-length bulk-copy runs: every round of every chunk of
+// the side pads each bucket at most once, about half of the time.  `side_keys` / `chunks`: the
+// partitioned side's keys and work chunks (rounds hold >= ~1/3 of a stage).
+uint32_t region_cap(double mean, double side_keys, double chunks) {
+  const double rounds = side_keys / (kScatterStageKeys / 3.0) + chunks;
+  return even_up(mean + 7.0 * std::sqrt(mean) + 16 + 0.5 * rounds + 4.0 * std::sqrt(rounds) + 16);
+}
+
 constexpr uint32_t kChunkCounters = 1u << 16;
 // Internal status: the hit list overflowed; msp_solve re-runs the (deterministic) solve with the
 // grown list, as fastval.join_pairs regrows its output buffer (fastval.py:126-139).
@@ -647,6 +656,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   CK(cudaMemsetAsync(D.bfilt.p, 0, 8 * G1, st));
   CK(cudaMemsetAsync(D.bhits.p, 0, 8 * G1, st));
   CK(cudaMemsetAsync(D.bovf.p, 0, 4 * G1, st));
+  CK(D.zkeys.ensure(16 * G1));
+  CK(cudaMemsetAsync(D.zkeys.p, 0, 16 * G1, st));
   if (!D.hit_cap) {
     D.hit_cap = 1 << 20;
     if (const char *ev = getenv("MSP_HIT_CAP")) D.hit_cap = std::max<uint64_t>(16, strtoull(ev, nullptr, 10));  // (tests)
@@ -972,7 +983,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       if (cur.nb == 0) { cur.g0 = g; cur.t0 = all_tiles; }
       const double mb = (double)nb / NB, mp = (double)np / NB;
       // capacities even: bucket regions start 16-byte aligned for the scatter's bulk copies
-      const uint32_t cb = even_up(mb + 7.0 * std::sqrt(mb) + 16), cp = even_up(mp + 7.0 * std::sqrt(mp) + 16);
+      const double chb = (double)P.tiles[2 * (size_t)g + bside] / kTaskTilesMin + 2.0 * D.num_sms;
+      const double chp = (double)P.tiles[2 * (size_t)g + 1 - bside] / kTaskTilesMin + 2.0 * D.num_sms;
+      const uint32_t cb = region_cap(mb, (double)nb, chb), cp = region_cap(mp, (double)np, chp);
       // bucket k of the batch: build region at base + k(cb + cp), probe region right after it
       bruns.push_back(BucketRun{nbt_all, NB, (uint32_t)cur.scratch, cb, cp, g});
       cur.scratch += (uint64_t)NB * (cb + cp);
@@ -1065,6 +1078,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.fill[0] = D.fill.as<uint32_t>();
       pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
       pa.batch_ovf = D.bovf.as<unsigned int>();
+      pa.zero_keys = D.zkeys.as<unsigned long long>();
       pa.dbg = dbg_stats;
       pa.hits = D.hits.as<HitRec>();
       pa.nhits = D.nhits.as<unsigned long long>();
@@ -1172,8 +1186,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         uint32_t cbits = pow2ceil((nb + kCoarseTarget - 1) / kCoarseTarget);
         cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, 10));
         const double mb = (double)nb / (1u << cbits), mp = (double)np / (1u << cbits);
-        mcb = std::max<uint64_t>(mcb, (uint64_t)even_up(mb + 7.0 * std::sqrt(mb) + 16) << cbits);
-        mcp = std::max<uint64_t>(mcp, (uint64_t)even_up(mp + 7.0 * std::sqrt(mp) + 16) << cbits);
+        mcb = std::max<uint64_t>(mcb, (uint64_t)region_cap(mb, (double)nb, 4.0 * D.num_sms) << cbits);
+        mcp = std::max<uint64_t>(mcp, (uint64_t)region_cap(mp, (double)np, 4.0 * D.num_sms) << cbits);
         mt = std::max<uint64_t>(mt, std::max(P.tiles[2 * (size_t)g], P.tiles[2 * (size_t)g + 1]));
       }
       {  // the coarse regions of the largest batch must fit next to everything else
@@ -1201,7 +1215,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, 10));
       const uint32_t NC = 1u << cbits;
       const double mb = (double)nb / NC, mp = (double)np / NC;
-      const uint64_t cb = even_up(mb + 7.0 * std::sqrt(mb) + 16), cp = even_up(mp + 7.0 * std::sqrt(mp) + 16);
+      const uint64_t cb = region_cap(mb, (double)nb, 4.0 * D.num_sms), cp = region_cap(mp, (double)np, 4.0 * D.num_sms);
       if (cb * NC > 0xFFFFFFF0ull || cp * NC > 0xFFFFFFF0ull) {
         set_err("batch side too large for 32-bit coarse regions");
         return MSP_UNSUPPORTED;
@@ -1255,6 +1269,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(D.ccfirst.ensure(4 * ccf.size()));
       if (int ru_ = upload(D.ccfirst.p, ccf.data(), 4 * ccf.size())) return ru_;
       c1.batch_ovf = D.bovf.as<unsigned int>();
+      c1.zero_keys = D.zkeys.as<unsigned long long>();
       c1.dbg = dbg_stats ? dbg_stats + 16 : nullptr;
       if (profile) CK(cudaEventRecord(D.pev[0], st));
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, std::max(ltiles[0], ltiles[1]))));
@@ -1285,7 +1300,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       const uint32_t NF = (uint32_t)std::max<uint64_t>(1, (uint64_t)std::ceil(mb / kBucketTargetMax));
       if (NF > (uint32_t)kMaxUnitBuckets) { set_err("coarse bucket too large for one level-2 wave"); return MSP_UNSUPPORTED; }
       const double fmb = mb / NF, fmp = mp / NF;
-      const uint32_t fcb = even_up(fmb + 7.0 * std::sqrt(fmb) + 16), fcp = even_up(fmp + 7.0 * std::sqrt(fmp) + 16);
+      // level-2 sources: one coarse region per role, read in 16K-slot chunks
+      const uint32_t fcb = region_cap(fmb, (double)cb, (double)cb / 16384 + 2), fcp = region_cap(fmp, (double)cp, (double)cp / 16384 + 2);
       struct L2Wave { size_t s0, ns, b0, nb; uint64_t total, scratch; };
       std::vector<L2Wave> lw;
       std::vector<RescatterSrc> srcs;
@@ -1336,6 +1352,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.fill[0] = D.fill.as<uint32_t>();
       pa.fill[1] = D.fill.as<uint32_t>() + kMaxWaveBuckets;
       pa.batch_ovf = D.bovf.as<unsigned int>();
+      pa.zero_keys = D.zkeys.as<unsigned long long>();
       pa.dbg = dbg_stats ? dbg_stats + 32 : nullptr;
       pa.hits = D.hits.as<HitRec>();
       pa.nhits = D.nhits.as<unsigned long long>();
@@ -1559,12 +1576,13 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
 
   // ---- totals
   CK(cudaEventRecord(D.ev[2], st));
-  std::vector<unsigned long long> bf(P.G), bh(P.G);
+  std::vector<unsigned long long> bf(P.G), bh(P.G), zk(2 * (size_t)P.G);
   unsigned long long nh = 0;
   int err = 0;
   if (P.G) {
     CK(cudaMemcpyAsync(bf.data(), D.bfilt.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(bh.data(), D.bhits.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(zk.data(), D.zkeys.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
@@ -1575,6 +1593,14 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   S.dev_ms_hot = hot_ms;
   S.hot_bytes = 8 * S.hot_pairs;  // algorithmic bytes: one 64-bit key written or read per candidate pair
   if (err) { set_err("join table region overflow (err=%d)", err); return MSP_INTERNAL; }
+  // real zero keys never reach the partitioned join (0 pads the runs): their hash hits are the
+  // per-batch product, and key 0 joins the recovery set (global-table batches count their own
+  // zeros and never touch zkeys)
+  std::vector<HitRec> zero_hits;
+  for (uint32_t g = 0; g < P.G; ++g) {
+    const unsigned long long zz = dropped[g] ? 0ull : zk[2 * (size_t)g] * zk[2 * (size_t)g + 1];
+    if (zz) { bh[g] += zz; zero_hits.push_back(HitRec{g, 0u, 0ull}); }
+  }
   for (uint32_t g = 0; g < P.G; ++g) { S.filtered_residuals += (int64_t)bf[g]; S.hash_hits += (int64_t)bh[g]; }
   if ((opt->flags & MSP_FLAG_BATCH_STATS) && P.G) {  // per-batch ValidationStats (validate.py:63-71)
     res->batch_stats = (int64_t *)malloc(sizeof(int64_t) * 5 * (size_t)P.G);
@@ -1600,6 +1626,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       CK(cudaMemcpy(t2.data(), D.hits.as<HitRec>() + from, sizeof(HitRec) * t2.size(), cudaMemcpyDeviceToHost));
       hv.insert(hv.end(), t2.begin(), t2.end());
     }
+    hv.insert(hv.end(), zero_hits.begin(), zero_hits.end());
     mark("recovery start");
     rc = recover(hv);
     if (rc) return rc;

@@ -10,3 +10,7 @@ if [ -n "$PROF" ]; then
 python tools/rep_solve.py 7 2 > gpurun_out/${T}_plain.log 2>&1 && \
 ncu --set full --import-source on --clock-control none -k regex:k_waves -s 1 -c 1 -o gpurun_out/${T}_prof -f python tools/rep_solve.py 7 2 > gpurun_out/${T}_ncu.log 2>&1; echo "ncu rc=$?"
 fi
+if [ -n "$BIG" ]; then
+MSP_DEBUG_STATS=1 timeout 600 python tools/run_solve.py --m 8 --seed 1 > gpurun_out/${T}_solve_8_70.json 2> gpurun_out/${T}_solve_8_70.err; tail -c 250 gpurun_out/${T}_solve_8_70.json; echo; tail -5 gpurun_out/${T}_solve_8_70.err
+timeout 900 python tools/run_solve.py --m 9 --seed 1 > gpurun_out/${T}_solve_9_80.json 2>&1; tail -c 300 gpurun_out/${T}_solve_9_80.json; echo
+fi
