@@ -161,6 +161,12 @@ __device__ __forceinline__ void bulk_store(unsigned long long *dst, const unsign
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// Every thread, before the CTA publishes a chunk's keys (task counter / kernel end): its bulk copies
+// have fully completed (not just read the stage) and are ordered before its later generic accesses.
+__device__ __forceinline__ void bulk_complete() {
+  asm volatile("cp.async.bulk.wait_group 0;\n\tfence.proxy.async.global;" ::: "memory");
+  __threadfence();
+}
 
 // Called by every thread after a barrier that ends the round (every thread fenced its staged
 // writes for the async proxy before it): one lane per nonempty entry reserves the entry's run,
@@ -427,6 +433,7 @@ __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const Sc
     staged = 0;
     if (!more) break;
   }
+  bulk_complete();
   if (right) {
     const unsigned long long f = warp_sum(filt);
     if (lane == 0 && f) atomicAdd(A.batch_filtered + ui.gid, f);
@@ -503,6 +510,7 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
     staged = 0;
     if (!more) break;
   }
+  bulk_complete();
 }
 
 // Level 2 of the huge-batch path as its own launch (MSP_FLAG_WAVE_LAUNCHES): stream already-hashed
@@ -527,36 +535,37 @@ constexpr int kJWays = 8;                               // slots per table bucke
 constexpr int kJBuckets = kJoinSlots / kJWays;          // 2K buckets of 8 slots
 constexpr int kStash = 256;                             // keys whose two buckets were both full
 constexpr int kHitWords = (kJoinSlots + kStash) / 32;
-constexpr int kJQueue = 1024;                           // deferred probes per bucket (then inline)
-constexpr int kBuildBuf = 9728;                         // build keys of one bucket in shared memory
-constexpr int kProbeChunk = 4096;                       // probe keys per streamed chunk (2 buffers)
+constexpr int kJQueue = 512;                            // deferred probes (per-warp segments)
+#ifndef MSP_JOIN_CHUNK
+#define MSP_JOIN_CHUNK 4000
+#endif
+constexpr int kJChunk = MSP_JOIN_CHUNK;                 // keys per streamed chunk (two buffers)
+static_assert(kJChunk % 2 == 0, "chunks start 16-byte aligned");
 
 // Shared-memory join of one partition bucket.  The table has 8-slot buckets, first fit in bucket
-// b1, then b2, then a small stash; a slot holds a fingerprint byte 0x80 | 7 key bits (0 = empty;
-// the eight of a bucket are one 64-bit word) and the 16-bit index of its key in the bucket's build
-// region.  An insert is one shared atomic + two small stores; a probe reads ONE fingerprint word and
-// tests all eight bytes at once (branch-free); the ~2% of probes whose test does not rule a match
-// out are queued and counted exactly at the end of the bucket, comparing full keys read back from
-// the build region in global memory.  A key sits in b2 only if b1 was full (slot 7's marker bit,
-// the word's sign bit).  b1/b2 come from a multiplicative mix of the key's low word, the
+// b1, then b2, then a small stash; a slot holds the full 64-bit key and a fingerprint byte 0x80 | 7
+// key bits (0 = empty; the eight of a bucket are one 64-bit word).  An insert is one shared atomic
+// + two stores; a probe reads ONE fingerprint word and tests all eight bytes at once (branch-free);
+// the few probes whose test does not rule a match out are queued in the warp's segment and counted
+// exactly later (full keys, in shared memory).  A key sits in b2 only if b1 was full (slot 7's
+// marker bit, the word's sign bit).  b1/b2 come from a multiplicative mix of the key's low word, the
 // fingerprint from its high word (whose top bits chose the partition bucket).
-// Keys move by TMA bulk copies (cp.async.bulk + mbarrier): a bucket's build keys land in `bkeys`
-// while the previous bucket is still probing, its probe keys stream through two `pkeys` chunks.
+// Keys arrive by TMA bulk copies (cp.async.bulk + mbarrier) as ONE stream of chunks through two
+// buffers: each bucket's build chunks then its probe chunks, the next chunk always in flight while
+// the current one is processed -- across bucket boundaries too.
 struct JoinSmem {
+  unsigned long long key[kJBuckets][kJWays];
   unsigned long long fp[kJBuckets];     // eight fingerprint bytes
   uint32_t cnt[kJBuckets];              // claims (may exceed 8: failed claims move on)
-  uint16_t idx[kJBuckets][kJWays];      // build-region index of each slot's key
-  uint16_t stash[kStash];               // build-region indices of stashed keys
+  unsigned long long stash[kStash];
   uint32_t hitbits[kHitWords];
-  unsigned long long queue[kJQueue];    // per-warp segments: probe keys whose fast test did not rule
-                                        // out a match
+  unsigned long long queue[kJQueue];    // per-warp segments of deferred probes
   unsigned long long bhits[kJoinThreads / 32];
-  unsigned long long mbar[3];           // build keys, probe chunk buffers 0 / 1
+  unsigned long long mbar[2];           // one per chunk buffer
   uint32_t nstash, ovf, pad[2];
-  alignas(16) unsigned long long bkeys[kBuildBuf];       // (bulk-copy destinations: 16-byte aligned)
-  alignas(16) unsigned long long pkeys[2][kProbeChunk];
+  alignas(16) unsigned long long buf[2][kJChunk];  // (bulk-copy destinations: 16-byte aligned)
 };
-static_assert(offsetof(JoinSmem, bkeys) % 16 == 0 && offsetof(JoinSmem, pkeys) % 16 == 0, "bulk copy alignment");
+static_assert(offsetof(JoinSmem, buf) % 16 == 0, "bulk copy alignment");
 
 size_t join_smem_bytes() { return sizeof(JoinSmem); }
 
@@ -567,17 +576,13 @@ __device__ __forceinline__ void mbar_init(unsigned long long *b) {
 __device__ __forceinline__ void mbar_inval(unsigned long long *b) {
   asm volatile("mbarrier.inval.shared::cta.b64 [%0];" :: "r"(smem_u32(b)) : "memory");
 }
-// Thread 0: expect `bytes` on barrier b and copy them from global src to shared dst (bulk copies of
-// <= 32 KB, 16-byte aligned ends).
+// Thread 0: expect `bytes` on barrier b and copy them from global src to shared dst (one bulk copy,
+// 16-byte aligned ends).
 __device__ __forceinline__ void bulk_load(unsigned long long *dst, const unsigned long long *src, uint32_t bytes,
                                           unsigned long long *bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-  for (uint32_t o = 0; o < bytes; o += 32768u) {
-    const uint32_t n = min(32768u, bytes - o);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(smem_u32(dst) + o), "l"(reinterpret_cast<const char *>(src) + o), "r"(n), "r"(smem_u32(bar))
-                 : "memory");
-  }
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 // Every thread: wait for the completion of phase `parity` of barrier b.
 __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
@@ -601,29 +606,27 @@ __device__ __forceinline__ uint32_t zero_byte_mask32(uint32_t x) {
 // Some byte of x is zero (exact for presence).
 __device__ __forceinline__ uint32_t has_zero_byte(uint32_t x) { return (x - 0x01010101u) & ~x & 0x80808080u; }
 
-// Insert the key k found at build-region index i.
-__device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k, uint32_t i) {
+__device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   const uint32_t t = jmix(k), fpb = jfp4(k) & 0xFFu;
   uint32_t b = jb1(t), s = atomicAdd(&T.cnt[b], 1u);
   if (s >= (uint32_t)kJWays) { b = jb2(t); s = atomicAdd(&T.cnt[b], 1u); }
   if (s < (uint32_t)kJWays) {
-    T.idx[b][s] = (uint16_t)i;
+    T.key[b][s] = k;
     reinterpret_cast<uint8_t *>(&T.fp[b])[s] = (uint8_t)fpb;  // slot s is this thread's alone
   } else {
     const uint32_t q = atomicAdd(&T.nstash, 1u);
-    if (q < (uint32_t)kStash) T.stash[q] = (uint16_t)i; else T.ovf = 1u;
+    if (q < (uint32_t)kStash) T.stash[q] = k; else T.ovf = 1u;
   }
 }
 
-// Copies of k among the slots of bucket b whose fingerprint byte matches (full keys from global).
-__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, const unsigned long long *bk, uint32_t b,
-                                                unsigned long long w, uint32_t pat, unsigned long long k,
-                                                uint32_t &c, uint32_t &first) {
+// Copies of k among the slots of bucket b whose fingerprint byte matches.
+__device__ __forceinline__ void count_in_bucket(const JoinSmem &T, uint32_t b, unsigned long long w, uint32_t pat,
+                                                unsigned long long k, uint32_t &c, uint32_t &first) {
   unsigned long long m = ((unsigned long long)zero_byte_mask32((uint32_t)(w >> 32) ^ pat) << 32) |
                          zero_byte_mask32((uint32_t)w ^ pat);
   while (m) {
     const uint32_t s = (uint32_t)(__ffsll((long long)m) - 1) >> 3;
-    if (__ldg(bk + T.idx[b][s]) == k) {
+    if (T.key[b][s] == k) {
       if (!c) first = b * kJWays + s;
       ++c;
     }
@@ -633,107 +636,84 @@ __device__ __forceinline__ void count_in_bucket(const JoinSmem &T, const unsigne
 
 // Multiplicity of k among the build keys (b1, b2 if b1 is full, the stash if b2 is full too);
 // `first` = slot id of its first copy.
-__device__ __forceinline__ uint32_t join_count_slow(const JoinSmem &T, const unsigned long long *bk,
-                                                    unsigned long long k, uint32_t nstash, uint32_t &first) {
+__device__ __forceinline__ uint32_t join_count_slow(const JoinSmem &T, unsigned long long k, uint32_t nstash,
+                                                    uint32_t &first) {
   const uint32_t t = jmix(k), b1 = jb1(t), pat = jfp4(k);
   const unsigned long long w1 = T.fp[b1];
   first = 0xFFFFFFFFu;
   uint32_t c = 0;
-  count_in_bucket(T, bk, b1, w1, pat, k, c, first);
+  count_in_bucket(T, b1, w1, pat, k, c, first);
   if ((long long)w1 < 0) {  // b1 full: k may have moved on to b2 (and, if b2 is full too, the stash)
     const uint32_t b2 = jb2(t);
     const unsigned long long w2 = T.fp[b2];
-    count_in_bucket(T, bk, b2, w2, pat, k, c, first);
+    count_in_bucket(T, b2, w2, pat, k, c, first);
     if ((long long)w2 < 0)
       for (uint32_t i = 0; i < nstash; ++i)
-        if (__ldg(bk + T.stash[i]) == k) { if (!c) first = kJoinSlots + i; ++c; }
+        if (T.stash[i] == k) { if (!c) first = kJoinSlots + i; ++c; }
   }
   return c;
 }
+
+// The chunk stream of a join task: for each bucket, its build chunks then its probe chunks.
+struct ChunkCursor {
+  uint32_t b, c, nbc, npc;  // bucket, chunk within the bucket, build / probe chunks of the bucket
+};
 
 // Join of buckets [b0, b1) of a wave by one CTA of NT threads (fastval.py:75-107 semantics: every
 // full-64-bit-hash-equal (build, probe) pair is a hit; each hit key is recorded once for the exact
 // confirmation), resetting each bucket's fill counters for the next use of the scratch buffer.  The
 // regions hold min(fill, cap) keys, run pads (key 0) among them (fill > cap flagged the batch).
-// Per bucket: its build keys are already landing in bkeys (prefetched during the previous bucket's
-// probe, or issued here), its first two probe chunks are issued at the start; clear the table;
-// insert; prefetch the next bucket's build keys; stream the probe chunks; count the queued probes
-// exactly.  Ends with a barrier.
-// (MSP_JOIN_INLINE=__noinline__ gives the join its own register allocation: measured slower)
+// Ends with a barrier.
 #ifndef MSP_JOIN_INLINE
 #define MSP_JOIN_INLINE __forceinline__
 #endif
 template <int NT>
 __device__ MSP_JOIN_INLINE void join_group(JoinSmem &T, const PartArgs &S, uint32_t b0, uint32_t b1) {
   const uint32_t tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) { mbar_init(&T.mbar[0]); mbar_init(&T.mbar[1]); mbar_init(&T.mbar[2]); }
+  auto nbuild_of = [&](uint32_t b) { return min(S.fill[0][b], __ldg(S.cap[0] + b)); };
+  auto nprobe_of = [&](uint32_t b) { return min(S.fill[1][b], __ldg(S.cap[1] + b)); };
+  // thread 0: issue chunk `cur` of the stream into buffer `bf` (and advance the issue cursor)
+  auto issue = [&](ChunkCursor &ic, uint32_t bf) {
+    while (ic.b < b1 && ic.c >= ic.nbc + ic.npc) {
+      if (++ic.b >= b1) return;
+      ic.c = 0;
+      ic.nbc = (nbuild_of(ic.b) + kJChunk - 1) / kJChunk;
+      ic.npc = (nprobe_of(ic.b) + kJChunk - 1) / kJChunk;
+    }
+    if (ic.b >= b1) return;
+    const bool build = ic.c < ic.nbc;
+    const uint32_t n = build ? nbuild_of(ic.b) : nprobe_of(ic.b);
+    const uint32_t c0 = (build ? ic.c : ic.c - ic.nbc) * kJChunk;
+    const uint32_t len = min(n - c0, (uint32_t)kJChunk);
+    const unsigned long long *src = S.scratch + __ldg((build ? S.start[0] : S.start[1]) + ic.b) + c0;
+    fence_proxy_async_smem();  // (generic accesses of the buffer before -> async write)
+    bulk_load(T.buf[bf], src, 8u * ((len + 1u) & ~1u), &T.mbar[bf]);  // (odd: one slot past, < cap)
+    ++ic.c;
+  };
+  if (tid == 0) { mbar_init(&T.mbar[0]); mbar_init(&T.mbar[1]); }
   __syncthreads();
-  uint32_t ph_b = 0, ph_p0 = 0, ph_p1 = 0;  // barrier phases (every thread tracks them alike)
-  bool build_ready = false;                 // this bucket's build keys were prefetched
+  ChunkCursor ic{b0, 0, (nbuild_of(b0) + kJChunk - 1) / kJChunk, (nprobe_of(b0) + kJChunk - 1) / kJChunk};
+  if (tid == 0) { issue(ic, 0); issue(ic, 1); }
+  uint32_t k_chunk = 0;           // stream position of the next chunk to process (buffer k & 1)
+  uint32_t ph0 = 0, ph1 = 0;      // barrier phases (every thread tracks them alike)
+  constexpr uint32_t kQW = kJQueue / (NT / 32);
+  unsigned long long *qw = T.queue + (tid >> 5) * kQW;
+  const uint32_t lt = (1u << lane) - 1u;
   for (uint32_t b = b0; b < b1; ++b) {
     long long tp0 = 0, tp1 = 0, tp2 = 0;
     if (S.dbg && tid == 0) tp0 = clock64();
     const uint32_t gid = __ldg(S.gid + b);
-    const uint32_t nbuild = min(S.fill[0][b], __ldg(S.cap[0] + b));
-    const uint32_t nprobe = min(S.fill[1][b], __ldg(S.cap[1] + b));
-    const unsigned long long *bk = S.scratch + __ldg(S.start[0] + b);
-    const unsigned long long *pk = S.scratch + __ldg(S.start[1] + b);
-    const uint32_t npc = (nprobe + kProbeChunk - 1) / kProbeChunk;  // probe chunks
-    const bool oversized = nbuild > 65535u;  // 16-bit slot indices: the batch goes to the global table
-    if (tid == 0) {
-      fence_proxy_async_smem();  // (generic accesses of the buffers before -> async writes)
-      if (!build_ready && nbuild && !oversized)
-        bulk_load(T.bkeys, bk, 8u * min((nbuild + 1u) & ~1u, (uint32_t)kBuildBuf), &T.mbar[0]);
-      for (uint32_t c = 0; c < 2 && c < npc; ++c) {
-        const uint32_t n = min(nprobe - c * kProbeChunk, (uint32_t)kProbeChunk);
-        bulk_load(T.pkeys[c], pk + c * kProbeChunk, 8u * ((n + 1u) & ~1u), &T.mbar[1 + c]);
-      }
-    }
+    const uint32_t nbuild = nbuild_of(b), nprobe = nprobe_of(b);
+    const uint32_t nbc = (nbuild + kJChunk - 1) / kJChunk, npc = (nprobe + kJChunk - 1) / kJChunk;
     for (uint32_t i = tid; i < (uint32_t)kJBuckets / 4; i += NT) reinterpret_cast<uint4 *>(T.cnt)[i] = make_uint4(0, 0, 0, 0);
     for (uint32_t i = tid; i < (uint32_t)kJBuckets / 2; i += NT) reinterpret_cast<uint4 *>(T.fp)[i] = make_uint4(0, 0, 0, 0);
     for (uint32_t i = tid; i < (uint32_t)kHitWords; i += NT) T.hitbits[i] = 0u;
     if (tid == 0) { T.nstash = 0; T.ovf = 0; }
     __syncthreads();
-    // ---- build: pieces of <= kBuildBuf keys through bkeys (one piece unless the bucket is oversized)
-    if (oversized) {
-      if (tid == 0) atomicOr(S.batch_ovf + gid, 1u);
-    } else {
-      for (uint32_t p0 = 0; p0 < nbuild; p0 += kBuildBuf) {
-        if (p0) {  // a later piece (oversized bucket): load it now
-          if (tid == 0) {
-            fence_proxy_async_smem();
-            bulk_load(T.bkeys, bk + p0, 8u * ((min(nbuild - p0, (uint32_t)kBuildBuf) + 1u) & ~1u), &T.mbar[0]);
-          }
-        }
-        mbar_wait(&T.mbar[0], ph_b);
-        ph_b ^= 1u;
-        const uint32_t pn = min(nbuild - p0, (uint32_t)kBuildBuf);
-        for (uint32_t i = tid; i < pn; i += NT) {
-          const unsigned long long k = T.bkeys[i];
-          if (k != 0ull) join_insert(T, k, p0 + i);  // (0: a run pad)
-        }
-        __syncthreads();
-      }
-    }
-    build_ready = false;
-    if (b + 1 < b1 && tid == 0) {  // prefetch the next bucket's build keys while this one probes
-      const uint32_t nb2 = min(S.fill[0][b + 1], __ldg(S.cap[0] + b + 1));
-      if (nb2 && nb2 <= (uint32_t)kBuildBuf) {
-        fence_proxy_async_smem();
-        bulk_load(T.bkeys, S.scratch + __ldg(S.start[0] + b + 1), 8u * ((nb2 + 1u) & ~1u), &T.mbar[0]);
-      }
-    }
-    if (b + 1 < b1) {
-      const uint32_t nb2 = min(S.fill[0][b + 1], __ldg(S.cap[0] + b + 1));
-      build_ready = nb2 && nb2 <= (uint32_t)kBuildBuf;
-    }
-    if (S.dbg && tid == 0) tp1 = clock64();
-    const uint32_t nstash = min(T.nstash, (uint32_t)kStash);
-    if (T.ovf && tid == 0) { atomicOr(S.batch_ovf + gid, 1u); if (S.dbg) atomicAdd(S.dbg + 14, 1ull); }
-    uint32_t hits = 0;
+    uint32_t hits = 0, nqw = 0, nstash = 0;  // (nqw: warp-uniform)
     auto probe_slow = [&](unsigned long long k) {  // a possible hit: count it, record the key once
       uint32_t first;
-      const uint32_t c = join_count_slow(T, bk, k, nstash, first);
+      const uint32_t c = join_count_slow(T, k, nstash, first);
       if (c) {
         hits += c;
         if (!(atomicOr(T.hitbits + (first >> 5), 1u << (first & 31)) & (1u << (first & 31)))) {
@@ -742,41 +722,46 @@ __device__ MSP_JOIN_INLINE void join_group(JoinSmem &T, const PartArgs &S, uint3
         }
       }
     };
-    // ---- probe: chunks c through pkeys[c & 1]; possible hits go to the warp's own queue segment
-    constexpr uint32_t kQW = kJQueue / (NT / 32);
-    unsigned long long *qw = T.queue + (tid >> 5) * kQW;
-    const uint32_t lt = (1u << lane) - 1u;
-    uint32_t nqw = 0;  // (warp-uniform)
-    for (uint32_t c = 0; c < npc; ++c) {
-      const uint32_t pb = c & 1u;
-      mbar_wait(&T.mbar[1 + pb], pb ? ph_p1 : ph_p0);
-      if (pb) ph_p1 ^= 1u; else ph_p0 ^= 1u;
-      const uint32_t n = min(nprobe - c * kProbeChunk, (uint32_t)kProbeChunk);
-      const unsigned long long *pc = T.pkeys[pb];
-      for (uint32_t i = tid; i - lane < n; i += NT) {  // (whole warps iterate: the exit is warp-uniform)
-        // fast test, branch-free: no fingerprint byte of b1 matches and b1 is not full -> no copy
-        const unsigned long long k = pc[min(i, n - 1)];
-        const uint32_t pat = jfp4(k);
-        const unsigned long long w = T.fp[jb1(jmix(k))];
-        const bool maybe = ((has_zero_byte((uint32_t)w ^ pat) | has_zero_byte((uint32_t)(w >> 32) ^ pat)) != 0u ||
-                            (long long)w < 0) && i < n && k != 0ull;
-        const uint32_t mm = __ballot_sync(0xffffffffu, maybe);
-        const uint32_t qi = nqw + __popc(mm & lt);
-        if (maybe && qi < kQW) qw[qi] = k;  // deferred exact count: no divergent slow path here
-        nqw += __popc(mm);
-        if (nqw > kQW && __any_sync(0xffffffffu, maybe && qi >= kQW))
-          if (maybe && qi >= kQW) probe_slow(k);  // the warp's segment is full (duplicate-heavy bucket)
-      }
-      if (c + 2 < npc) {  // refill this buffer with chunk c + 2 once every thread is done with it
-        __syncthreads();
-        if (tid == 0) {
-          fence_proxy_async_smem();
-          const uint32_t n2 = min(nprobe - (c + 2) * kProbeChunk, (uint32_t)kProbeChunk);
-          bulk_load(T.pkeys[pb], pk + (c + 2) * kProbeChunk, 8u * ((n2 + 1u) & ~1u), &T.mbar[1 + pb]);
+    for (uint32_t c = 0; c < nbc + npc; ++c, ++k_chunk) {
+      const uint32_t bf = k_chunk & 1u;
+      mbar_wait(&T.mbar[bf], bf ? ph1 : ph0);
+      if (bf) ph1 ^= 1u; else ph0 ^= 1u;
+      const unsigned long long *ck = T.buf[bf];
+      if (c < nbc) {  // ---- build chunk: insert
+        const uint32_t n = min(nbuild - c * kJChunk, (uint32_t)kJChunk);
+        for (uint32_t i = tid; i < n; i += NT) {
+          const unsigned long long k = ck[i];
+          if (k != 0ull) join_insert(T, k);  // (0: a run pad)
         }
+        __syncthreads();  // buffer released; after the last build chunk the table is complete
+        if (c + 1 == nbc) {
+          nstash = min(T.nstash, (uint32_t)kStash);
+          if (T.ovf && tid == 0) { atomicOr(S.batch_ovf + gid, 1u); if (S.dbg) atomicAdd(S.dbg + 14, 1ull); }
+          if (S.dbg && tid == 0) tp1 = clock64();
+        }
+      } else {        // ---- probe chunk: fast test, branch-free; possible hits to the warp's queue
+        const uint32_t n = min(nprobe - (c - nbc) * kJChunk, (uint32_t)kJChunk);
+        for (uint32_t i = tid; i - lane < n; i += NT) {  // (whole warps iterate: the exit is warp-uniform)
+          const unsigned long long k = ck[min(i, n - 1)];
+          const uint32_t pat = jfp4(k);
+          const unsigned long long w = T.fp[jb1(jmix(k))];
+          const bool maybe = ((has_zero_byte((uint32_t)w ^ pat) | has_zero_byte((uint32_t)(w >> 32) ^ pat)) != 0u ||
+                              (long long)w < 0) && i < n && k != 0ull;
+          const uint32_t mm = __ballot_sync(0xffffffffu, maybe);
+          if (nqw + __popc(mm) > kQW) {  // the warp's segment is full: count its queued probes now
+            for (uint32_t q = lane; q < nqw; q += 32) probe_slow(qw[q]);
+            nqw = 0;
+            __syncwarp();
+          }
+          if (maybe) qw[nqw + __popc(mm & lt)] = k;
+          nqw += __popc(mm);
+        }
+        __syncthreads();  // buffer released
       }
+      if (tid == 0) issue(ic, bf);  // the chunk after next into the released buffer
     }
-    for (uint32_t i = lane; i < min(nqw, kQW); i += 32) probe_slow(qw[i]);
+    if (nbc == 0 && S.dbg && tid == 0) tp1 = clock64();
+    for (uint32_t q = lane; q < nqw; q += 32) probe_slow(qw[q]);
     const unsigned long long wh = warp_sum((unsigned long long)hits);
     if (lane == 0) T.bhits[tid >> 5] = wh;
     __syncthreads();
@@ -796,7 +781,7 @@ __device__ MSP_JOIN_INLINE void join_group(JoinSmem &T, const PartArgs &S, uint3
     }
   }
   __syncthreads();
-  if (tid == 0) { mbar_inval(&T.mbar[0]); mbar_inval(&T.mbar[1]); mbar_inval(&T.mbar[2]); }
+  if (tid == 0) { mbar_inval(&T.mbar[0]); mbar_inval(&T.mbar[1]); }
   __syncthreads();
 }
 
