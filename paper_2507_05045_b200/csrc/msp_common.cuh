@@ -14,7 +14,7 @@
 namespace msp {
 
 constexpr int kTQ = 32;            // loop entries per warp tile
-constexpr int kMaxMC = 15;         // companion coordinates supported by P16 (m <= 16)
+constexpr int kMaxMC = 15;         // companion coordinates supported by P16 (m <= 16); P32: m <= 9
 constexpr uint64_t kFnvOffset = 0xCBF29CE484222325ull;  // validate.py:34, fastval.py:42
 constexpr uint64_t kFnvPrime = 0x100000001B3ull;         // validate.py:35, fastval.py:43
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
@@ -117,9 +117,26 @@ __device__ __forceinline__ void load_vec(const uint32_t *__restrict__ base, uint
   }
 }
 
-__host__ __device__ constexpr int words_for(int mc) { return (mc + 1) / 2; }
-__host__ __device__ constexpr int stride_for(int mc) {
-  return words_for(mc) <= 1 ? 1 : words_for(mc) <= 2 ? 2 : words_for(mc) <= 4 ? 4 : 8;
+// Companion layouts, selected by the kernels' compile-time MCX = MC (+ kWide):
+//   P16 (MCX = MC <= 15): two companion coordinates per u32 word, 16 bits each; exact while every
+//        block row sum is <= 16384 and d_j <= 32767 (right residual d - s kept with a guard bit
+//        per half: (d + 0x8000) - s keeps bit 15 iff s <= d);
+//   P32 (MCX = MC + kWide, MC <= 8): one coordinate per word, 31-bit values; exact while every
+//        block row sum is < 2^30 and d_j < 2^31 (guard bit 31).
+constexpr int kWide = 16;
+constexpr int kMaxWideMC = 8;
+__host__ __device__ constexpr int mc_of(int mcx) { return mcx & (kWide - 1); }
+__host__ __device__ constexpr bool wide_of(int mcx) { return mcx >= kWide; }
+__host__ __device__ constexpr int words_for(int mcx) { return wide_of(mcx) ? mc_of(mcx) : (mc_of(mcx) + 1) / 2; }
+__host__ __device__ constexpr int stride_for(int mcx) {
+  return words_for(mcx) <= 1 ? 1 : words_for(mcx) <= 2 ? 2 : words_for(mcx) <= 4 ? 4 : 8;
+}
+__host__ __device__ constexpr uint32_t guard_mask(int mcx) { return wide_of(mcx) ? 0x80000000u : 0x80008000u; }
+// Coordinate c (< MC) of a companion word vector: left (a plain sum) or right (the guarded residual).
+template <int MCX, bool RIGHT>
+__host__ __device__ __forceinline__ uint32_t coord(const uint32_t *w, int c) {
+  if constexpr (wide_of(MCX)) return RIGHT ? (w[c] & 0x7FFFFFFFu) : w[c];
+  else return ((c & 1) ? (w[c >> 1] >> 16) : w[c >> 1]) & (RIGHT ? 0x7FFFu : 0xFFFFu);
 }
 
 struct HitRec { uint32_t gid, pad; uint64_t key; };

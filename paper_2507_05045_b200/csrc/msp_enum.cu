@@ -357,7 +357,8 @@ int launch_enum(int mc, SinkKind kind, const EnumArgs &args, const JoinTable &jt
 #define MSP_CASE(N) case N: launch_mc<N>(kind, args, jt, grid, st); break;
     MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
     MSP_CASE(8) MSP_CASE(9) MSP_CASE(10) MSP_CASE(11) MSP_CASE(12) MSP_CASE(13) MSP_CASE(14)
-    MSP_CASE(15)
+    MSP_CASE(15) MSP_CASE(17) MSP_CASE(18) MSP_CASE(19) MSP_CASE(20) MSP_CASE(21) MSP_CASE(22)
+    MSP_CASE(23) MSP_CASE(24)
 #undef MSP_CASE
     default: return -1;
   }

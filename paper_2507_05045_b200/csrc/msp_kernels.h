@@ -1,6 +1,8 @@
 // msp_kernels.h -- host-visible argument structs and launch wrappers of the solver kernels.
 #pragma once
 #include <cstdint>
+#include <string>
+#include <vector>
 #include <cuda_runtime.h>
 #include "msp_common.cuh"
 
@@ -17,7 +19,7 @@ struct MergeStep {
 struct MergeArgs { MergeStep s[4]; };
 
 struct PackTable { const uint32_t *mask; uint32_t *comp; uint32_t size; int start, b; };
-struct PackArgs { PackTable t[4]; const uint64_t *a; int m, n, sw; };
+struct PackArgs { PackTable t[4]; const uint64_t *a; int m, n, sw, wide; };  // wide: P32 layout
 
 struct RunTable { const uint64_t *w; uint32_t *run_start, *run_end; uint32_t size; };
 struct RunArgs { RunTable t[4]; };
@@ -69,6 +71,22 @@ struct JoinTable {
   int *err;
   uint32_t nkeys;              // recovery: slots of `keys` (all regions), scanned for the filter
 };
+
+// Sparse alpha plan (msp_plan.cu) for arbitrary u64 row-0 weights: batch headers in alpha order,
+// per (batch, side) rectangle bases / counts / tile totals, and the rectangle list on the device
+// (owned by the plan's per-device workspace, valid until its next call).
+struct SparsePlanIn {
+  const uint64_t *w[4];                // sorted table weights (device)
+  uint32_t size[4];
+  uint64_t target, alpha_lo, alpha_hi; // alpha band [lo, hi) of this shard (hi = ~0: unbounded)
+};
+struct SparsePlanOut {
+  std::vector<uint64_t> alpha, nl, nr, tiles;   // tiles: [2g + side]
+  std::vector<uint32_t> rect_base, nrect;       // [2g + side]
+  RectDesc *rects = nullptr;
+};
+int sparse_plan(int device, const SparsePlanIn &in, SparsePlanOut &out, cudaStream_t st, int64_t &launches,
+                std::string &err);
 
 void launch_merge_step(const MergeArgs &a, uint32_t max_n, cudaStream_t st);
 void launch_pack(const PackArgs &a, uint32_t max_size, cudaStream_t st);

@@ -307,7 +307,8 @@ __device__ __forceinline__ void tile_vecs(const ScatterArgs &A, uint32_t side, c
   load_vec<SW>(yt, d.y + min(lane, qn - 1u), yv);
 }
 
-// kUS keys of the current tile (loop entries q .. q+kUS-1) into the stage.
+// kUS keys of the current tile (loop entries q .. q+kUS-1) into the stage.  (MC: the companion
+// layout MCX of msp_common.cuh -- coordinate count plus kWide for P32.)
 template <int MC, bool RIGHT>
 __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uint32_t *ybuf,
                                           const uint32_t (&lv)[stride_for(MC)],
@@ -332,16 +333,13 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
       uint32_t acc = 0xFFFFFFFFu;
 #pragma unroll
       for (int k = 0; k < NW0; ++k) { sv[k] = dg[k] - sv[k]; acc &= sv[k]; }
-      const bool fit = (acc & 0x80008000u) == 0x80008000u;
+      const bool fit = (acc & guard_mask(MC)) == guard_mask(MC);
       filt += (in && !fit) ? 1u : 0u;
       in = in && fit;
     }
     uint32_t lo = ui.h0lo, hi = ui.h0hi;
 #pragma unroll
-    for (int c = 0; c < MC; ++c) {
-      const uint32_t w = sv[c >> 1];
-      fold(lo, hi, (c & 1) ? (w >> 16) & (RIGHT ? 0x7FFFu : 0xFFFFu) : w & (RIGHT ? 0x7FFFu : 0xFFFFu));
-    }
+    for (int c = 0; c < mc_of(MC); ++c) fold(lo, hi, coord<MC, RIGHT>(sv, c));
     key[u] = ((unsigned long long)hi << 32) | lo;
     const bool z = in && (hi | lo) == 0u;  // a real key 0: counted per (batch, side), never staged
     nzero += z ? 1u : 0u;
@@ -936,7 +934,8 @@ cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, i
 #define MSP_CASE(N) case N: return launch_scatter_mc<N>(args, p, grid, st);
     MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
     MSP_CASE(8) MSP_CASE(9) MSP_CASE(10) MSP_CASE(11) MSP_CASE(12) MSP_CASE(13) MSP_CASE(14)
-    MSP_CASE(15)
+    MSP_CASE(15) MSP_CASE(17) MSP_CASE(18) MSP_CASE(19) MSP_CASE(20) MSP_CASE(21) MSP_CASE(22)
+    MSP_CASE(23) MSP_CASE(24)
 #undef MSP_CASE
     default: return cudaErrorInvalidValue;
   }
@@ -956,7 +955,8 @@ cudaError_t launch_waves(int mc, const WavesArgs &w, int num_sms, cudaStream_t s
 #define MSP_CASE(N) case N: return launch_waves_mc<N>(w, num_sms, st);
     MSP_CASE(0) MSP_CASE(1) MSP_CASE(2) MSP_CASE(3) MSP_CASE(4) MSP_CASE(5) MSP_CASE(6) MSP_CASE(7)
     MSP_CASE(8) MSP_CASE(9) MSP_CASE(10) MSP_CASE(11) MSP_CASE(12) MSP_CASE(13) MSP_CASE(14)
-    MSP_CASE(15)
+    MSP_CASE(15) MSP_CASE(17) MSP_CASE(18) MSP_CASE(19) MSP_CASE(20) MSP_CASE(21) MSP_CASE(22)
+    MSP_CASE(23) MSP_CASE(24)
 #undef MSP_CASE
     default: return cudaErrorInvalidValue;
   }

@@ -161,6 +161,10 @@ constexpr uint64_t kDefaultWaveKeys = 40ull << 20;
 // Everything msp_solve needs after K1 + K2.
 struct Plan {
   int m = 0, n = 0, mc = 0, sw = 1;
+  int mcx = 0;            // companion layout (msp_common.cuh): mc, + kWide for P32
+  bool wide = false;      // P32 companions
+  bool sparse = false;    // sparse (sorted pair-sum) alpha plan instead of the dense histograms
+  uint64_t S64[4] = {0, 0, 0, 0};  // exact block row-0 sums
   int b[4] = {0, 0, 0, 0}, start[4] = {0, 0, 0, 0};
   uint32_t S[4] = {0, 0, 0, 0};
   uint64_t target = 0;
@@ -179,7 +183,16 @@ const uint32_t *table_m(Device &D, const Plan &P, int t) {
   return P.merge_w_cur[t] ? D.tm2[t].as<uint32_t>() : D.tm[t].as<uint32_t>();
 }
 
-// Checks the arithmetic mode preconditions (P16 packing, dense row-0 plan).
+// Dense row-0 plan limits: block row-0 sums up to kDenseMaxWeight and a convolution of at most
+// kDenseMaxWork (weight, Y-run) steps; beyond them the sparse plan (msp_plan.cu) takes over.
+constexpr uint64_t kDenseMaxWeight = 1ull << 24;
+constexpr double kDenseMaxWork = 4.0e9;
+bool force_sparse_plan() {
+  const char *e = getenv("MSP_SPARSE_PLAN");
+  return e && atoi(e) != 0;
+}
+
+// Checks the arithmetic mode preconditions (companion layout, row-0 plan).
 int check_instance(const msp_problem *pr, Plan &P) {
   P.m = pr->m;
   P.n = pr->n;
@@ -189,24 +202,46 @@ int check_instance(const msp_problem *pr, Plan &P) {
   for (int t = 0, s = 0; t < 4; ++t) { P.start[t] = s; s += P.b[t]; }
   if (P.b[0] > 24) { set_err("block size %d > 24 unsupported", P.b[0]); return MSP_UNSUPPORTED; }
   P.mc = P.m - 1;
-  if (P.mc > kMaxMC) { set_err("m=%d > %d rows unsupported by the packed-16 path", P.m, kMaxMC + 1); return MSP_UNSUPPORTED; }
-  P.sw = stride_for(P.mc);
+  if (P.mc > kMaxMC) { set_err("m=%d > %d rows unsupported", P.m, kMaxMC + 1); return MSP_UNSUPPORTED; }
+  // companion layout: P16 when every block row sum fits 16384 and d_j <= 32767, else P32
+  unsigned __int128 cmax = 0, dmax = 0;
   for (int t = 0; t < 4; ++t) {
-    unsigned __int128 s0 = 0;
-    for (int j = 0; j < P.b[t]; ++j) s0 += pr->a[P.start[t] + j];
-    if (s0 > (1u << 24)) { set_err("row-0 block sum exceeds the dense alpha plan (2^24)"); return MSP_UNSUPPORTED; }
-    P.S[t] = (uint32_t)s0;
     for (int r = 1; r < P.m; ++r) {
       unsigned __int128 s = 0;
       for (int j = 0; j < P.b[t]; ++j) s += pr->a[(size_t)r * P.n + P.start[t] + j];
-      if (s > 16384) { set_err("row %d block sum exceeds the packed-16 companion range", r + 1); return MSP_UNSUPPORTED; }
+      cmax = std::max(cmax, s);
     }
   }
-  for (int r = 1; r < P.m; ++r)
-    if (pr->d[r] > 32767) { set_err("d[%d] exceeds the packed-16 residual range", r); return MSP_UNSUPPORTED; }
+  for (int r = 1; r < P.m; ++r) dmax = std::max<unsigned __int128>(dmax, pr->d[r]);
+  P.wide = !(cmax <= 16384 && dmax <= 32767);
+  if (P.wide && (P.mc > kMaxWideMC || cmax >= (1u << 30) || dmax >= (1u << 31))) {
+    set_err("companion rows outside the packed layouts (P16: block sums <= 16384, d <= 32767; P32: m <= %d, "
+            "block sums < 2^30, d < 2^31)", kMaxWideMC + 1);
+    return MSP_UNSUPPORTED;
+  }
+  P.mcx = P.mc + (P.wide ? kWide : 0);
+  P.sw = stride_for(P.mcx);
+  // row-0 plan: dense per-weight histograms while the block sums are small, else the sparse plan
+  bool big = false;
+  for (int t = 0; t < 4; ++t) {
+    unsigned __int128 s0 = 0;
+    for (int j = 0; j < P.b[t]; ++j) s0 += pr->a[P.start[t] + j];
+    if (s0 > kDenseMaxWeight) big = true;
+    P.S[t] = (uint32_t)std::min<unsigned __int128>(s0, 0xFFFFFFFFu);
+    P.S64[t] = (uint64_t)std::min<unsigned __int128>(s0, ~0ull);
+  }
+  {  // dense plan cost: the convolution loops over (S_X + 1) x (distinct Y weights <= min(S_Y + 1, 2^b_Y))
+    const double nyB = std::min<double>((double)P.S[1] + 1, (double)(1ull << P.b[1]));
+    const double nyD = std::min<double>((double)P.S[3] + 1, (double)(1ull << P.b[3]));
+    const double work = ((double)P.S[0] + P.S[1] + 1) * nyB + ((double)P.S[2] + P.S[3] + 1) * nyD;
+    if (work > kDenseMaxWork) big = true;
+  }
+  P.sparse = big || (force_sparse_plan());
   P.target = pr->d[0];
   return MSP_OK;
 }
+
+void fill_enum_base(Device &D, Plan &P, const msp_problem *pr, const RectDesc *rects);
 
 // K1 + K2 on the device; ends with the batch list and tile totals on the host.
 int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uint64_t alpha_hi,
@@ -223,7 +258,7 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
     CK(D.tw[t].ensure(8 * sz)); CK(D.tw2[t].ensure(8 * sz));
     CK(D.tm[t].ensure(4 * sz)); CK(D.tm2[t].ensure(4 * sz));
     CK(D.comp[t].ensure(4 * sz * P.sw));
-    CK(D.rs[t].ensure(4 * ((size_t)P.S[t] + 1))); CK(D.re[t].ensure(4 * ((size_t)P.S[t] + 1)));
+    if (!P.sparse) { CK(D.rs[t].ensure(4 * ((size_t)P.S[t] + 1))); CK(D.re[t].ensure(4 * ((size_t)P.S[t] + 1))); }
     CK(cudaMemsetAsync(D.tw[t].p, 0, 8, st));  // the empty subset: weight 0, mask 0
     CK(cudaMemsetAsync(D.tm[t].p, 0, 4, st));
     P.merge_w_cur[t] = 0;
@@ -255,17 +290,35 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   RunArgs ra{};
   for (int t = 0; t < 4; ++t) {
     pa.t[t] = PackTable{table_m(D, P, t), D.comp[t].as<uint32_t>(), 1u << P.b[t], P.start[t], P.b[t]};
+    if (P.sparse) continue;
     ra.t[t] = RunTable{table_w(D, P, t), D.rs[t].as<uint32_t>(), D.re[t].as<uint32_t>(), 1u << P.b[t]};
     CK(cudaMemsetAsync(D.rs[t].p, 0, 4 * ((size_t)P.S[t] + 1), st));
     CK(cudaMemsetAsync(D.re[t].p, 0, 4 * ((size_t)P.S[t] + 1), st));
   }
-  pa.a = D.a.as<uint64_t>(); pa.m = m; pa.n = n; pa.sw = P.sw;
+  pa.a = D.a.as<uint64_t>(); pa.m = m; pa.n = n; pa.sw = P.sw; pa.wide = P.wide;
   launch_pack(pa, maxsize, st);
-  launch_runs(ra, maxsize, st);
-  launches += 2;
+  ++launches;
+  if (!P.sparse) { launch_runs(ra, maxsize, st); ++launches; }
   if (t_tables) {  // K1 done: the stats split t_build (tables) from t_enumerate (the plan)
     CK(cudaStreamSynchronize(st));
     *t_tables = now_s();
+  }
+  if (P.sparse) {  // ---- K2/K3 for arbitrary weights: the sorted pair-sum plan (msp_plan.cu)
+    SparsePlanIn si{};
+    for (int t = 0; t < 4; ++t) { si.w[t] = table_w(D, P, t); si.size[t] = 1u << P.b[t]; }
+    si.target = P.target;
+    si.alpha_lo = alpha_lo;
+    si.alpha_hi = alpha_hi ? alpha_hi : ~0ull;
+    SparsePlanOut so;
+    std::string perr;
+    const int prc = sparse_plan(D.dev, si, so, st, launches, perr);
+    if (prc) { set_err("%s", perr.c_str()); return prc; }
+    P.G = (uint32_t)so.alpha.size();
+    P.alpha = so.alpha; P.nl = so.nl; P.nr = so.nr; P.tiles = so.tiles;
+    P.rect_base = so.rect_base; P.nrect = so.nrect;
+    P.ny[0] = P.ny[1] = 0;
+    fill_enum_base(D, P, pr, so.rects);
+    return MSP_OK;
   }
   // ---- K2: Y-run lists, convolution, batch list
   CK(D.yn.ensure(8));
@@ -345,21 +398,32 @@ int build_plan(Device &D, const msp_problem *pr, Plan &P, uint64_t alpha_lo, uin
   ra2.rects = D.rects.as<RectDesc>();
   launch_rects(ra2, P.G, st);
   ++launches;
-  // ---- launch-invariant enumeration arguments
+  fill_enum_base(D, P, pr, D.rects.as<RectDesc>());
+  return MSP_OK;
+}
+
+// Launch-invariant enumeration arguments (tables, rectangle list, packed d).
+void fill_enum_base(Device &D, Plan &P, const msp_problem *pr, const RectDesc *rects) {
+  const int m = P.m;
   EnumArgs &A = P.base;
   for (int t = 0; t < 4; ++t)
-    A.tab[t] = TableDev{table_w(D, P, t), table_m(D, P, t), D.comp[t].as<uint32_t>(), D.rs[t].as<uint32_t>(),
-                        D.re[t].as<uint32_t>(), P.S[t], 1u << P.b[t]};
+    A.tab[t] = TableDev{table_w(D, P, t), table_m(D, P, t), D.comp[t].as<uint32_t>(),
+                        P.sparse ? nullptr : D.rs[t].as<uint32_t>(), P.sparse ? nullptr : D.re[t].as<uint32_t>(),
+                        P.S[t], 1u << P.b[t]};
   for (int s = 0; s < 2; ++s)
-    A.yr[s] = YRuns{D.yw[s].as<uint32_t>(), D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), P.ny[s]};
-  A.rects = D.rects.as<RectDesc>();
+    A.yr[s] = P.sparse ? YRuns{nullptr, nullptr, nullptr, 0}
+                       : YRuns{D.yw[s].as<uint32_t>(), D.ys[s].as<uint32_t>(), D.yl[s].as<uint32_t>(), P.ny[s]};
+  A.rects = rects;
   for (int k = 0; k < 8; ++k) {
     const int c0 = 2 * k + 1, c1 = 2 * k + 2;  // rows c0, c1 (1-based companion rows)
+    if (P.wide) {  // P32: word k = d[k + 1] + 2^31 (guard bit 31)
+      A.dpack[k] = (k + 1 < m ? (uint32_t)pr->d[k + 1] : 0u) + 0x80000000u;
+      continue;
+    }
     const uint32_t lo = (c0 < m ? (uint32_t)pr->d[c0] : 0u) + 0x8000u;
     const uint32_t hi = (c1 < m ? (uint32_t)pr->d[c1] : 0u) + 0x8000u;
     A.dpack[k] = lo | (hi << 16);
   }
-  return MSP_OK;
 }
 
 struct Wave {
@@ -781,7 +845,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       rj.nrecs = D.nrecs.as<unsigned long long>();
       rj.rec_cap = rec_cap;
       set_enum_range(RA, D.runits.as<UnitDesc>(), ru.size(), tb, D.num_sms);
-      launch_enum(P.mc, SINK_RECOVER, RA, rj, D.num_sms, st);
+      launch_enum(P.mcx, SINK_RECOVER, RA, rj, D.num_sms, st);
       ++S.kernel_launches;
       CK(cudaGetLastError());
       unsigned long long nr = 0;
@@ -912,7 +976,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       W.ntasks = (uint32_t)tasks.size();
       if (profile && timed) CK(cudaEventRecord(D.pev[0], st));
       mark("k_waves launch");
-      CK(launch_waves(P.mc, W, D.num_sms, st));
+      CK(launch_waves(P.mcx, W, D.num_sms, st));
       mark("k_waves returned");
       S.kernel_launches += 1;
       if (profile && timed) {
@@ -1147,7 +1211,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         sa.units = D.uinfo.as<UnitInfo>() + w.u0;
         sa.nunits = (uint32_t)(w.u1 - w.u0);
         if (profile) CK(cudaEventRecord(D.pev[0], st));
-        rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_scatter(P.mc, sa, p2, D.num_sms, s2); }, pa);
+        rc = launch_pair(wi, [&](const PartArgs &p2, cudaStream_t s2) { return launch_scatter(P.mcx, sa, p2, D.num_sms, s2); }, pa);
         if (rc) return rc;
         S.kernel_launches += 2;
         if (profile) {
@@ -1293,7 +1357,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         sa.nchunks = 1;
         sa.units = D.hunits.as<UnitInfo>() + role;
         sa.nunits = 1;
-        CK(launch_scatter(P.mc, sa, c1, D.num_sms, st));
+        CK(launch_scatter(P.mcx, sa, c1, D.num_sms, st));
         S.kernel_launches += 2;
       }
       // level 2 waves over the coarse buckets
@@ -1554,9 +1618,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       if (profile) CK(cudaEventRecord(D.pev[0], st));
       set_enum_range(A, udev + w.ub0, w.ub1 - w.ub0, w.build_tiles, D.num_sms);
       const bool diag = opt->flags & MSP_FLAG_DIAG_HASH_ONLY;
-      if (launch_enum(P.mc, diag ? SINK_NONE : SINK_BUILD, A, jt, D.num_sms, st)) { set_err("unsupported m"); return MSP_INTERNAL; }
+      if (launch_enum(P.mcx, diag ? SINK_NONE : SINK_BUILD, A, jt, D.num_sms, st)) { set_err("unsupported m"); return MSP_INTERNAL; }
       set_enum_range(A, udev + w.up0, w.up1 - w.up0, w.probe_tiles, D.num_sms);
-      launch_enum(P.mc, diag ? SINK_NONE : SINK_PROBE, A, jt, D.num_sms, st);
+      launch_enum(P.mcx, diag ? SINK_NONE : SINK_PROBE, A, jt, D.num_sms, st);
       S.kernel_launches += 2;
       if (profile) {
         CK(cudaEventRecord(D.pev[1], st));
@@ -1764,7 +1828,7 @@ int msp_build_tables(const msp_problem *prob, int32_t device, uint64_t **weights
     for (size_t e = 0; e < sz; ++e) {
       contribs[t][e * m] = weights[t][e];
       for (int c = 0; c < P.mc; ++c)
-        contribs[t][e * m + 1 + c] = (comp[e * P.sw + (c >> 1)] >> (16 * (c & 1))) & 0xFFFFu;
+        contribs[t][e * m + 1 + c] = P.wide ? comp[e * P.sw + c] : (comp[e * P.sw + (c >> 1)] >> (16 * (c & 1))) & 0xFFFFu;
     }
     int64_t end = (int64_t)sz;
     for (int64_t i = (int64_t)sz - 1; i >= 0; --i) {

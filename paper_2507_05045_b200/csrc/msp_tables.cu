@@ -60,7 +60,7 @@ __global__ void k_merge_step(MergeArgs args) {
   }
 }
 
-// Companion rows 1..m-1 of every entry, packed P16 (two u16 per word, low half = lower row).
+// Companion rows 1..m-1 of every entry, packed P16 (two u16 per word, low half = lower row) or P32.
 __global__ void k_pack(PackArgs args) {
   const PackTable t = args.t[blockIdx.y];
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < t.size; e += gridDim.x * blockDim.x) {
@@ -71,7 +71,8 @@ __global__ void k_pack(PackArgs args) {
       for (int b = 0; b < t.b; ++b)
         if ((mk >> b) & 1u) s += (uint32_t)args.a[(size_t)r * args.n + t.start + b];
       const int j = r - 1;
-      words[j >> 1] |= (s & 0xFFFFu) << (16 * (j & 1));
+      if (args.wide) words[j] = s;  // P32 (block sums < 2^30, checked on the host)
+      else words[j >> 1] |= (s & 0xFFFFu) << (16 * (j & 1));
     }
     for (int k = 0; k < args.sw; ++k) t.comp[(size_t)e * args.sw + k] = words[k];
   }

@@ -177,19 +177,19 @@ __device__ __forceinline__ void step_keys(const Walker &W, TileCursor<stride_for
       uint32_t acc = 0xFFFFFFFFu;
 #pragma unroll
       for (int k = 0; k < NW0; ++k) { sv[u][k] = dg[k] - sv[u][k]; acc &= sv[u][k]; }
-      const bool fit = (acc & 0x80008000u) == 0x80008000u;
+      const bool fit = (acc & guard_mask(MC)) == guard_mask(MC);
       if (ok[u] && !fit && cf) ++filt;
       ok[u] = ok[u] && fit;
     }
 #pragma unroll
-    for (int c = 0; c < MC; ++c)
+    for (int c = 0; c < mc_of(MC); ++c)
 #pragma unroll
-      for (int u = 0; u < U; ++u) fnv_step(lo[u], hi[u], (sv[u][c >> 1] >> (16 * (c & 1))) & 0x7FFFu);
+      for (int u = 0; u < U; ++u) fnv_step(lo[u], hi[u], coord<MC, true>(sv[u], c));
   } else {
 #pragma unroll
-    for (int c = 0; c < MC; ++c)
+    for (int c = 0; c < mc_of(MC); ++c)
 #pragma unroll
-      for (int u = 0; u < U; ++u) fnv_step(lo[u], hi[u], (sv[u][c >> 1] >> (16 * (c & 1))) & 0xFFFFu);
+      for (int u = 0; u < U; ++u) fnv_step(lo[u], hi[u], coord<MC, false>(sv[u], c));
   }
 #pragma unroll
   for (int u = 0; u < U; ++u)

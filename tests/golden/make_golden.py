@@ -271,6 +271,33 @@ def _pairs_vec(wx, wy, total):
     return np.stack([xs, np.repeat(ys, lens)], axis=1).astype(np.int64)
 
 
+def solves_generic():
+    """Generic u64 weights: K = 10^6 instances (companion sums past 16 bits,
+    row-0 block sums far past any dense histogram) and surrogate-reduced instances (reduce_rows 2, 3:
+    the merged row 0 is (nD)-based, instances.py:266-319), solved by the reference in all mode."""
+    out = []
+    for (m, s) in ((4, 1), (4, 2), (4, 3), (4, 7), (5, 1), (5, 2)):
+        inst = ms.generate_instance(m, 10**6, s)
+        rec = solve_record(f"gen_{m}_1e6_{s}", inst, per_batch=(m == 4))
+        rec["reduce_rows"] = 1
+        out.append(rec)
+    for (m, s) in ((4, 1), (5, 1)):
+        inst, _ = plant_instance(m, 10**6, s)
+        rec = solve_record(f"plant_{m}_1e6_{s}", inst)
+        rec["reduce_rows"] = 1
+        out.append(rec)
+    for (m, K, s, r) in ((4, 100, 11, 2), (4, 100, 11, 3), (4, 100, 1, 2), (4, 100, 12, 3), (5, 100, 1, 2),
+                         (5, 100, 3, 2), (5, 100, 3, 3), (5, 1000, 2, 2)):
+        inst = ms.generate_instance(m, K, s)
+        t0 = time.time()
+        res = ms.solve(inst, ms.SolverConfig(mode="all", reduce_rows=r))
+        out.append({"name": f"gen_{m}_{K}_{s}_reduce{r}", "instance": inst_json(inst), "reduce_rows": r,
+                    "verdict": res.verdict, "solutions": [ms.solution_to_string(x) for x in res.solutions],
+                    "stats": {k: getattr(res.stats, k) for k in STAT_KEYS}, "fallback": res.stats.fallback,
+                    "ref_seconds": round(time.time() - t0, 3)})
+    return out
+
+
 def dump(name, obj):
     path = os.path.join(HERE, name)
     with open(path, "w") as fh:
@@ -289,6 +316,7 @@ def main():
         "streams.json": streams_golden,
         "solves_small.json": solves_small,
         "solves_medium.json": solves_medium,
+        "solves_generic.json": solves_generic,
         "plan_counts.json": lambda: {f"{m},{s}": plan_counts(ms.generate_instance(m, 100, s))
                                      for (m, s) in ((4, 1), (4, 11), (6, 1), (6, 4), (7, 1),
                                                     (8, 1), (9, 1))},

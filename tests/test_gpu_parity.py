@@ -509,3 +509,49 @@ def test_engine_names_of_the_reference_run_the_cuda_engine():
     for engine in ("python", "jit", "cuda", None):
         res = msb.solve(inst, msb.SolverConfig(mode="all"), engine=engine)
         assert res.solutions == ref.solutions and res.stats.engine == "cuda"
+
+
+def test_generic_weights_match_reference():
+    """generic u64 weights through the CUDA engine -- K = 10^6 instances (P32
+    companion layout + sparse alpha plan) and surrogate-reduced instances (reduce_rows 2, 3: u64 merged
+    row 0, sparse plan) -- against the reference's solves: solutions and every counter."""
+    for rec in load_golden("solves_generic.json"):
+        inst = inst_from(rec["instance"])
+        res = msb.solve(inst, msb.SolverConfig(mode="all", reduce_rows=rec["reduce_rows"]))
+        assert _strings(res.solutions) == rec["solutions"], rec["name"]
+        assert res.verdict == rec["verdict"]
+        for k in STAT_KEYS:
+            assert getattr(res.stats, k) == rec["stats"][k], (rec["name"], k)
+
+
+def test_generic_weights_per_batch_stats():
+    """Per-batch counters of K = 10^6 instances (sparse plan) equal the reference's per-batch stats."""
+    for rec in load_golden("solves_generic.json"):
+        if "batches" not in rec:
+            continue
+        inst = inst_from(rec["instance"])
+        opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_BATCH_STATS)
+        rc, xb, st = _native.solve_raw(inst.a, inst.d, opts)
+        assert rc == 0, _native.last_error()
+        assert st.get("batch_stats", []) == [tuple(b[:5]) for b in rec["batches"]], rec["name"]
+
+
+def test_sparse_plan_matches_dense_plan(monkeypatch):
+    """The sparse (sorted pair-sum) alpha plan, forced on K = 100 instances, reproduces the dense
+    plan exactly: batch headers, per-batch counters, solutions."""
+    for (m, s) in ((4, 11), (5, 3), (6, 4), (7, 1)):
+        inst = msb.generate_instance(m, 100, s)
+        opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_BATCH_STATS)
+        monkeypatch.delenv("MSP_SPARSE_PLAN", raising=False)
+        rc0, xb0, st0 = _native.solve_raw(inst.a, inst.d, opts)
+        plan0 = _native.alpha_plan(inst.a, inst.d)
+        monkeypatch.setenv("MSP_SPARSE_PLAN", "1")
+        rc1, xb1, st1 = _native.solve_raw(inst.a, inst.d, opts)
+        plan1 = _native.alpha_plan(inst.a, inst.d)
+        monkeypatch.delenv("MSP_SPARSE_PLAN")
+        assert rc0 == 0 and rc1 == 0, _native.last_error()
+        assert plan1 == plan0, (m, s)
+        assert st1["batch_stats"] == st0["batch_stats"], (m, s)
+        assert sorted(map(tuple, xb1.tolist())) == sorted(map(tuple, xb0.tolist()))
+        for k in STAT_KEYS:
+            assert st1[k] == st0[k], (m, s, k)
