@@ -455,7 +455,13 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
   unsigned long long dacc = 0;
   __syncthreads();
   const uint32_t cend = __ldg(A.cta_first + blockIdx.x + 1);
+  __shared__ int s_stop;
   for (uint32_t c = __ldg(A.cta_first + blockIdx.x); c < cend; ++c) {
+    if (A.abort_host) {  // stop (deadline / cancel): checked per chunk
+      if (threadIdx.x == 0) s_stop = *A.abort_host;
+      __syncthreads();
+      if (s_stop) break;
+    }
     const unsigned long long cw = __ldg(A.chunks + c);
     const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
     scatter_chunk<MC>(g, ybuf, A, S, dg, A.units[unit], t0, n, dacc);
@@ -816,10 +822,11 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
   // Thread 0 keeps the NEXT task in flight while the CTA works: its index (atomic), word, wave
   // descriptor, chunk word and dependency target are loaded a whole task ahead; at the switch it
   // waits for the dependency (acquire load) and hands everything over through shared memory.
-  struct Next { unsigned long long tk, cw; WaveDesc wd; uint32_t need; const unsigned int *ctr; };
+  struct Next { unsigned long long tk, cw; WaveDesc wd; uint32_t need; const unsigned int *ctr; int stop; };
   __shared__ unsigned long long s_cw;
   __shared__ WaveDesc s_wd;
   auto fetch = [&](Next &x) {
+    x.stop = W.abort_host ? *W.abort_host : 0;  // (host-mapped: its latency overlaps the current task)
     const uint32_t i = atomicAdd(W.task_ctr, 1u);
     x.tk = i < W.ntasks ? W.tasks[i] : ~0ull;
     x.ctr = nullptr;
@@ -845,17 +852,25 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
     if (tid == 0) {
       const Next cur = nx;
       if (cur.tk != ~0ull) fetch(nx);
-      if (cur.ctr) {
+      // stop (deadline / cancel, MSP_OPTIONS): every CTA leaves at its next task switch, waits included
+      bool stop = cur.stop != 0 || *(volatile int *)W.abort_dev != 0;
+      if (stop) *(volatile int *)W.abort_dev = 1;
+      if (cur.ctr && !stop) {
         const long long tw = clock64();
         uint32_t v;
-        while (true) {
+        for (uint32_t spin = 0;; ++spin) {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cur.ctr) : "memory");
           if (v >= cur.need) break;
+          if (*(volatile int *)W.abort_dev || ((spin & 1023u) == 1023u && W.abort_host && *W.abort_host)) {
+            *(volatile int *)W.abort_dev = 1;
+            stop = true;
+            break;
+          }
           __nanosleep(256);
         }
         if (W.pa.dbg) atomicAdd(W.pa.dbg + 6, (unsigned long long)(clock64() - tw));
       }
-      s_task = cur.tk;
+      s_task = stop ? ~0ull : cur.tk;
       s_cw = cur.cw;
       s_wd = cur.wd;
     }

@@ -14,8 +14,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -85,6 +87,9 @@ struct Device {
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   uint64_t hit_cap = 0;  // distinct hit keys the hit list holds (grown on overflow, fastval.py:126-139)
+  volatile int *abort_h = nullptr;  // host-mapped stop word the kernels poll (deadline / cancel)
+  int *abort_hd = nullptr;          // its device address
+  DBuf abort_dev;                   // device-side copy of the stop, set by the first CTA that sees it
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
   uint64_t wstride = 0;  // keys per wave scratch buffer (D.scratch holds kWaveBuffers of them)
@@ -136,6 +141,14 @@ int get_device(int dev, Device **out, double *t_init = nullptr) {
   for (auto &e : D->ev_s) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto &e : D->ev_j) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&D->ev_x, cudaEventDisableTiming));
+  {
+    void *h = nullptr, *hd = nullptr;
+    CK(cudaHostAlloc(&h, 64, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(&hd, h, 0));
+    D->abort_h = reinterpret_cast<volatile int *>(h);
+    D->abort_hd = reinterpret_cast<int *>(hd);
+    *D->abort_h = 0;
+  }
   g_devices[dev] = D;
   *out = D;
   if (t_init) *t_init = now_s() - t0;
@@ -683,6 +696,30 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   rc = check_instance(pr, P);
   if (rc) return rc;
   const double deadline = opt->time_limit_s > 0 ? t0 + opt->time_limit_s : 0;
+  // Watchdog: a host thread turns the deadline and the cross-rank cancel word into the host-mapped
+  // stop word the running kernels poll (k_waves at every task switch, k_scatter per chunk), so a
+  // solve stops within one task instead of at the next host checkpoint.
+  *D.abort_h = 0;
+  CK(D.abort_dev.ensure(64));
+  CK(cudaMemsetAsync(D.abort_dev.p, 0, 4, st));
+  struct Watchdog {
+    std::atomic<bool> done{false};
+    std::thread th;
+    ~Watchdog() { done = true; if (th.joinable()) th.join(); }
+  } wd;
+  if (deadline > 0 || opt->cancel) {
+    volatile int *word = D.abort_h;
+    const volatile int32_t *cancel = opt->cancel;
+    wd.th = std::thread([&wd, word, cancel, deadline]() {
+      while (!wd.done.load()) {
+        if (deadline > 0 && now_s() > deadline) { *word = 1; return; }
+        if (cancel && *cancel) { *word = 2; return; }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+      }
+    });
+  }
+  // the stop word's verdict after a sync: timeout / cancelled / none
+  auto stop_state = [&]() { return *D.abort_h; };
   CK(cudaEventRecord(D.ev[0], st));
   const uint64_t key_budget = opt->wave_keys ? std::max<uint64_t>(4096, opt->wave_keys) : kDefaultWaveKeys;
   double t_tables = 0;
@@ -878,9 +915,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
-    if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
+    if ((deadline && now_s() > deadline) || stop_state() == 1) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
     if (nh > hit_cap) { D.hit_cap = 2 * nh; return kRetryHits; }  // regrow the hit list and re-run
-    if (opt->cancel && *opt->cancel) {  // another rank confirmed a solution (first mode)
+    if ((opt->cancel && *opt->cancel) || stop_state() == 2) {  // another rank confirmed a solution (first mode)
       S.cancelled = 1;
       stop_now = true;
       return MSP_OK;
@@ -896,7 +933,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
     return MSP_OK;
   };
-  const bool periodic = deadline || opt->mode == MSP_MODE_FIRST || opt->cancel;
+  // host checkpoints between pipeline segments: first mode only (its solutions are confirmed on the
+  // host); deadlines and cancels reach the running kernels through the watchdog's stop word
+  const bool periodic = opt->mode == MSP_MODE_FIRST;
   // asynchronous metadata upload through the pinned ring (wraps after a stream sync)
   auto upload = [&](void *dst, const void *src, size_t bytes) -> int {
     if (!bytes) return MSP_OK;
@@ -950,6 +989,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(D.wctr.ensure(4 * (1 + 2 * wds.size())));
     CK(cudaMemsetAsync(D.wctr.p, 0, 4 * (1 + 2 * wds.size()), st));
     W.task_ctr = D.wctr.as<unsigned int>();
+    W.abort_host = D.abort_hd;
+    W.abort_dev = D.abort_dev.as<int>();
     W.scat_done = W.task_ctr + 1;
     W.join_done = W.scat_done + wds.size();
     const size_t seg = periodic ? 16 : wds.size();
@@ -1149,6 +1190,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
       ScatterArgs sa = scatter_base(P, A);
+        sa.abort_host = D.abort_hd;
       if (!per_wave) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
         std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
         tch.reserve(all_tiles / kTaskTilesMin + units.size());
@@ -1270,6 +1312,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       if (rc) return rc;
     }
     for (size_t hi_ = 0; hi_ < huge_b.size() && !stopped; ++hi_) {
+      if (stop_state()) { stopped = true; break; }  // deadline / cancel (reported after the sync)
       rc = join_streams();  // the previous batch's joins still read the wave buffers
       if (rc) return rc;
       const uint32_t g = huge_b[hi_];
@@ -1351,6 +1394,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         c1.cap[0] = cbkd + (2 + role) * NC;
         c1.fill[0] = D.cfill.as<uint32_t>() + role * kMaxWaveBuckets;
         ScatterArgs sa = scatter_base(P, A);
+        sa.abort_host = D.abort_hd;
         sa.tiles = D.tdesc.as<TileDesc>();
         sa.chunks = D.cchunks.as<unsigned long long>() + (role ? cch1 : 0);
         sa.cta_first = D.ccfirst.as<uint32_t>() + (role ? ccf1 : 0);
@@ -1512,7 +1556,8 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(cudaMemcpyAsync(ovf.data(), D.bovf.p, 4 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&n_v2_hits, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (uint32_t g = 0; g < P.G; ++g) {
+    if (stop_state()) stopped = true;  // the kernels stopped early: nothing left to re-join
+    for (uint32_t g = 0; g < P.G && !stopped; ++g) {
       if (!ovf[g]) continue;
       dropped[g] = 1;
       global_b.push_back(g);
@@ -1606,6 +1651,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     jt.zero_hit = D.zhit.as<unsigned int>();
     const UnitDesc *udev = D.units.as<UnitDesc>();
     for (size_t wi = 0; wi < waves.size(); ++wi) {
+      if (stop_state()) { stopped = true; break; }
       const Wave &w = waves[wi];
       launch_clear(D.keys.p, 8 * w.slots, D.num_sms, st);
       if (++D.epoch >= (1ull << 24)) {  // tag space exhausted: clear and restart
@@ -1676,8 +1722,12 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       r[3] = (int64_t)bf[g]; r[4] = (int64_t)bh[g];
     }
   }
+  if (stop_state() == 1 || (deadline && now_s() > deadline)) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
+  if (stop_state() == 2) {  // cancelled mid-solve by another rank: counters are partial
+    S.cancelled = 1;
+    return emit();
+  }
   if (nh > hit_cap) { D.hit_cap = 2 * nh; return kRetryHits; }  // regrow the hit list and re-run
-  if (deadline && now_s() > deadline) { set_err("time limit exceeded"); return MSP_TIMEOUT; }
   if (!stopped) {
     // hits recorded by the partitioned join of dropped batches are superseded by their re-join
     std::vector<HitRec> hv;

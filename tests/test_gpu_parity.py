@@ -555,3 +555,43 @@ def test_sparse_plan_matches_dense_plan(monkeypatch):
         assert sorted(map(tuple, xb1.tolist())) == sorted(map(tuple, xb0.tolist()))
         for k in STAT_KEYS:
             assert st1[k] == st0[k], (m, s, k)
+
+
+def test_time_limit_stops_the_running_kernels():
+    """The deadline reaches the running kernels (host-mapped stop word polled at every task switch of
+    the persistent pipeline): a (9,80) full enumeration (~40 s) with a 1 s limit raises SolveTimeout
+    within a fraction of a second of the limit, not at the end of the enumeration."""
+    import time
+
+    inst = msb.generate_instance(9, 100, 1)
+    msb.solve(msb.generate_instance(4, 100, 11), msb.SolverConfig(mode="all"))  # (context already up)
+    t0 = time.perf_counter()
+    with pytest.raises(msb.SolveTimeout):
+        msb.solve(inst, msb.SolverConfig(mode="all"), time_limit=1.0)
+    assert time.perf_counter() - t0 < 4.0
+    # the device is usable right after an interrupted solve
+    res = msb.solve(msb.generate_instance(6, 100, 4), msb.SolverConfig(mode="all"))
+    assert len(res.solutions) == 2
+
+
+def test_cancel_word_stops_a_running_solve(tmp_path):
+    """Cross-rank early exit: a cancel word set while a (9,80) solve runs stops it
+    within a task switch; the solve returns cancelled with partial counters."""
+    import threading
+    import time
+
+    from paper_2507_05045_b200.distributed import CancelFlag
+    from paper_2507_05045_b200.solver import native_solve
+
+    inst = msb.generate_instance(9, 100, 1)
+    flag = CancelFlag(f"msp_cancel_run_{tmp_path.name}", create=True)
+    try:
+        timer = threading.Timer(1.0, flag.set)
+        timer.start()
+        t0 = time.perf_counter()
+        sols, st = native_solve(inst, "all", None, cancel=flag.address)
+        dt = time.perf_counter() - t0
+        timer.join()
+        assert st["cancelled"] == 1 and dt < 5.0
+    finally:
+        flag.close(unlink=True)
