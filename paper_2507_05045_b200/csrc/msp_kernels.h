@@ -175,7 +175,7 @@ struct ScatterArgs {
   const UnitInfo *units; uint32_t nunits;
   unsigned long long *batch_filtered;  // per batch (gid)
   uint32_t diag;                       // MSP_FLAG_DIAG_HASH_ONLY: hash without staging
-  const volatile int *abort_host;      // (k_scatter) host-mapped stop word, polled per chunk
+  const int *abort_dev;                // (k_scatter) the stop word, polled per chunk
 };
 cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, int num_sms, cudaStream_t st);
 // Huge batches, level 2: re-partition coarse bucket regions (already hashed keys) into fine buckets.
@@ -231,8 +231,8 @@ struct WavesArgs {
   const unsigned long long *tasks;     // join << 63 | wave << 32 | chunk or first bucket
   uint32_t ntasks;
   unsigned int *task_ctr, *scat_done, *join_done;  // zeroed before the launch
-  const volatile int *abort_host;      // host-mapped word: nonzero = stop (deadline / cross-rank cancel)
-  int *abort_dev;                      // device copy of the stop, seen by every CTA (zeroed per solve)
+  int *abort_dev;                      // stop word (deadline / cross-rank cancel): zeroed per solve, set
+                                       // by the host watchdog with an async copy while kernels run
 };
 cudaError_t launch_waves(int mc, const WavesArgs &w, int num_sms, cudaStream_t st);
 

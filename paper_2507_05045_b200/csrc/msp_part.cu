@@ -457,8 +457,8 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
   const uint32_t cend = __ldg(A.cta_first + blockIdx.x + 1);
   __shared__ int s_stop;
   for (uint32_t c = __ldg(A.cta_first + blockIdx.x); c < cend; ++c) {
-    if (A.abort_host) {  // stop (deadline / cancel): checked per chunk
-      if (threadIdx.x == 0) s_stop = *A.abort_host;
+    if (A.abort_dev) {  // stop (deadline / cancel): checked per chunk
+      if (threadIdx.x == 0) s_stop = *(volatile int *)A.abort_dev;
       __syncthreads();
       if (s_stop) break;
     }
@@ -826,7 +826,9 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
   __shared__ unsigned long long s_cw;
   __shared__ WaveDesc s_wd;
   auto fetch = [&](Next &x) {
-    x.stop = W.abort_host ? *W.abort_host : 0;  // (host-mapped: its latency overlaps the current task)
+    // the stop word (device memory, set by the host watchdog's copy): read a task ahead, so its
+    // latency overlaps the current task
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(x.stop) : "l"(W.abort_dev));
     const uint32_t i = atomicAdd(W.task_ctr, 1u);
     x.tk = i < W.ntasks ? W.tasks[i] : ~0ull;
     x.ctr = nullptr;
@@ -853,19 +855,14 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
       const Next cur = nx;
       if (cur.tk != ~0ull) fetch(nx);
       // stop (deadline / cancel, MSP_OPTIONS): every CTA leaves at its next task switch, waits included
-      bool stop = cur.stop != 0 || *(volatile int *)W.abort_dev != 0;
-      if (stop) *(volatile int *)W.abort_dev = 1;
+      bool stop = cur.stop != 0;
       if (cur.ctr && !stop) {
         const long long tw = clock64();
         uint32_t v;
-        for (uint32_t spin = 0;; ++spin) {
+        while (true) {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cur.ctr) : "memory");
           if (v >= cur.need) break;
-          if (*(volatile int *)W.abort_dev || ((spin & 1023u) == 1023u && W.abort_host && *W.abort_host)) {
-            *(volatile int *)W.abort_dev = 1;
-            stop = true;
-            break;
-          }
+          if (*(volatile int *)W.abort_dev) { stop = true; break; }
           __nanosleep(256);
         }
         if (W.pa.dbg) atomicAdd(W.pa.dbg + 6, (unsigned long long)(clock64() - tw));

@@ -87,9 +87,10 @@ struct Device {
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
   uint64_t hit_cap = 0;  // distinct hit keys the hit list holds (grown on overflow, fastval.py:126-139)
-  volatile int *abort_h = nullptr;  // host-mapped stop word the kernels poll (deadline / cancel)
-  int *abort_hd = nullptr;          // its device address
-  DBuf abort_dev;                   // device-side copy of the stop, set by the first CTA that sees it
+  volatile int *abort_h = nullptr;  // why the watchdog stopped the solve: 1 deadline, 2 cancel (pinned)
+  int *abort_one = nullptr;         // pinned source of the stop copy
+  cudaStream_t stream_wd = nullptr; // the watchdog's copy stream (runs beside the kernels)
+  DBuf abort_dev;                   // the stop word the kernels poll (device memory)
   cudaStream_t stream2 = nullptr;        // join stream (overlaps the next wave's scatter)
   cudaEvent_t ev_s[2] = {nullptr, nullptr}, ev_j[2] = {nullptr, nullptr}, ev_x = nullptr;
   uint64_t wstride = 0;  // keys per wave scratch buffer (D.scratch holds kWaveBuffers of them)
@@ -142,12 +143,13 @@ int get_device(int dev, Device **out, double *t_init = nullptr) {
   for (auto &e : D->ev_j) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&D->ev_x, cudaEventDisableTiming));
   {
-    void *h = nullptr, *hd = nullptr;
-    CK(cudaHostAlloc(&h, 64, cudaHostAllocMapped));
-    CK(cudaHostGetDevicePointer(&hd, h, 0));
+    void *h = nullptr;
+    CK(cudaHostAlloc(&h, 64, cudaHostAllocDefault));
     D->abort_h = reinterpret_cast<volatile int *>(h);
-    D->abort_hd = reinterpret_cast<int *>(hd);
+    D->abort_one = reinterpret_cast<int *>(h) + 4;
     *D->abort_h = 0;
+    D->abort_one[0] = 1;
+    CK(cudaStreamCreateWithFlags(&D->stream_wd, cudaStreamNonBlocking));
   }
   g_devices[dev] = D;
   *out = D;
@@ -696,9 +698,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   rc = check_instance(pr, P);
   if (rc) return rc;
   const double deadline = opt->time_limit_s > 0 ? t0 + opt->time_limit_s : 0;
-  // Watchdog: a host thread turns the deadline and the cross-rank cancel word into the host-mapped
-  // stop word the running kernels poll (k_waves at every task switch, k_scatter per chunk), so a
-  // solve stops within one task instead of at the next host checkpoint.
+  // Watchdog: a host thread turns the deadline and the cross-rank cancel word into the device stop
+  // word the running kernels poll (k_waves at every task switch, k_scatter per chunk) -- one async
+  // copy on its own stream, which runs beside the kernels -- so a solve stops within one task instead
+  // of at the next host checkpoint.
   *D.abort_h = 0;
   CK(D.abort_dev.ensure(64));
   CK(cudaMemsetAsync(D.abort_dev.p, 0, 4, st));
@@ -708,12 +711,24 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     ~Watchdog() { done = true; if (th.joinable()) th.join(); }
   } wd;
   if (deadline > 0 || opt->cancel) {
+    CK(cudaStreamSynchronize(st));  // (the stop word is zero before the watchdog can set it)
     volatile int *word = D.abort_h;
     const volatile int32_t *cancel = opt->cancel;
-    wd.th = std::thread([&wd, word, cancel, deadline]() {
+    int *dev_word = D.abort_dev.as<int>(), *one = D.abort_one;
+    cudaStream_t wst = D.stream_wd;
+    const int devno = D.dev;
+    wd.th = std::thread([&wd, word, cancel, deadline, dev_word, one, wst, devno]() {
       while (!wd.done.load()) {
-        if (deadline > 0 && now_s() > deadline) { *word = 1; return; }
-        if (cancel && *cancel) { *word = 2; return; }
+        int why = 0;
+        if (deadline > 0 && now_s() > deadline) why = 1;
+        else if (cancel && *cancel) why = 2;
+        if (why) {
+          *word = why;
+          cudaSetDevice(devno);
+          cudaMemcpyAsync(dev_word, one, 4, cudaMemcpyHostToDevice, wst);
+          cudaStreamSynchronize(wst);
+          return;
+        }
         std::this_thread::sleep_for(std::chrono::microseconds(200));
       }
     });
@@ -989,7 +1004,6 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(D.wctr.ensure(4 * (1 + 2 * wds.size())));
     CK(cudaMemsetAsync(D.wctr.p, 0, 4 * (1 + 2 * wds.size()), st));
     W.task_ctr = D.wctr.as<unsigned int>();
-    W.abort_host = D.abort_hd;
     W.abort_dev = D.abort_dev.as<int>();
     W.scat_done = W.task_ctr + 1;
     W.join_done = W.scat_done + wds.size();
@@ -1190,7 +1204,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
       ScatterArgs sa = scatter_base(P, A);
-        sa.abort_host = D.abort_hd;
+        sa.abort_dev = D.abort_dev.as<int>();
       if (!per_wave) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
         std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
         tch.reserve(all_tiles / kTaskTilesMin + units.size());
@@ -1394,7 +1408,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         c1.cap[0] = cbkd + (2 + role) * NC;
         c1.fill[0] = D.cfill.as<uint32_t>() + role * kMaxWaveBuckets;
         ScatterArgs sa = scatter_base(P, A);
-        sa.abort_host = D.abort_hd;
+        sa.abort_dev = D.abort_dev.as<int>();
         sa.tiles = D.tdesc.as<TileDesc>();
         sa.chunks = D.cchunks.as<unsigned long long>() + (role ? cch1 : 0);
         sa.cta_first = D.ccfirst.as<uint32_t>() + (role ? ccf1 : 0);
