@@ -41,6 +41,8 @@ WORKLOADS = {  # name -> (m, K, seed)
     "4,30": (4, 100, 11),
 }
 METRIC = "candidate pairs verified/sec (full enumeration, all solutions)"
+# ncu --set full capture of the current k_waves (update with the kernel; profiles/README.md)
+TRAFFIC_CAPTURE = "r2s_kernels.json"
 UNIT = "pairs/s"
 
 
@@ -380,15 +382,12 @@ def main() -> int:
                        "pairs": hot_pairs},
         "traffic": None,
     }
-    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/README.md)
-        import glob
-        caps = sorted(glob.glob(os.path.join(HERE, "profiles", "r*_kernels.json")),
-                      key=lambda f: (len(os.path.basename(f)), os.path.basename(f)))  # latest capture
-        with open(caps[-1]) as fh:
+    try:  # DRAM bytes per launch from the committed ncu --set full capture of this code (profiles/)
+        with open(os.path.join(HERE, "profiles", TRAFFIC_CAPTURE)) as fh:
             tr = json.load(fh)["traffic"]
         roofline["traffic"] = {"dram_bytes_per_launch": tr["launch_dram_bytes"],
                                "algorithmic_bytes_per_launch": tr["algorithmic_bytes_per_launch"],
-                               "source": tr["source"]}
+                               "capture": TRAFFIC_CAPTURE, "source": tr["source"]}
     except (OSError, KeyError, ValueError):
         pass
     roofline_hbm = {"bound": "hbm", "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
