@@ -165,8 +165,8 @@ struct RectSparseSide {
   uint32_t ny;
 };
 
-// Block (g, side): the batch side's rectangles X-run x Y-run, oriented for the warp tile (longer run
-// across lanes) with their tile offsets -- the records k_rects writes for the dense plan.
+// Block (g, side): the batch side's rectangles X-run x Y-run, oriented for the warp tile (lanes_over_x:
+// the cheaper orientation) with their tile offsets -- the records k_rects writes for the dense plan.
 __global__ void k_rects_sparse(RectSparseSide L, RectSparseSide R, const uint64_t *hdr, const uint32_t *rbase,
                                RectDesc *rects, unsigned long long *tiles, int *err) {
   const uint32_t g = blockIdx.x;
@@ -184,7 +184,7 @@ __global__ void k_rects_sparse(RectSparseSide L, RectSparseSide R, const uint64_
       const uint64_t p = S.val[off + r];
       const uint32_t x = (uint32_t)(p / S.ny), y = (uint32_t)(p - (uint64_t)x * S.ny);
       const uint32_t xs = S.xs[x], xl = S.xl[x], ys = S.ys[y], yl = S.yl[y];
-      const bool lx = xl >= yl;
+      const bool lx = lanes_over_x(xl, yl);
       D.gs_x = ((uint32_t)(g * 2 + side) << 1) | (lx ? 1u : 0u);
       D.lane_start = lx ? xs : ys;
       D.loop_start = lx ? ys : xs;

@@ -610,6 +610,12 @@ uint32_t region_cap(double mean, double side_keys, double chunks) {
 }
 
 constexpr uint32_t kChunkCounters = 1u << 16;
+// Level-1 coarse buckets of a huge batch side: at most 2^kCoarseBitsMax (each stage entry of the
+// level-1 scatter then keeps >= 46 slots, so its runs stay long and its rank overflow rare)
+#ifndef MSP_COARSE_BITS_MAX
+#define MSP_COARSE_BITS_MAX 9
+#endif
+constexpr uint32_t kCoarseBitsMax = MSP_COARSE_BITS_MAX;
 // Internal status: the hit list overflowed; msp_solve re-runs the (deterministic) solve with the
 // grown list, as fastval.join_pairs regrows its output buffer (fastval.py:126-139).
 constexpr int kRetryHits = 100;
@@ -1304,7 +1310,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         const int bs = P.nr[g] <= P.nl[g] ? 1 : 0;
         const uint64_t nb = bs ? P.nr[g] : P.nl[g], np = bs ? P.nl[g] : P.nr[g];
         uint32_t cbits = pow2ceil((nb + kCoarseTarget - 1) / kCoarseTarget);
-        cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, 10));
+        cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, kCoarseBitsMax));
         const double mb = (double)nb / (1u << cbits), mp = (double)np / (1u << cbits);
         mcb = std::max<uint64_t>(mcb, (uint64_t)region_cap(mb, (double)nb, 4.0 * D.num_sms) << cbits);
         mcp = std::max<uint64_t>(mcp, (uint64_t)region_cap(mp, (double)np, 4.0 * D.num_sms) << cbits);
@@ -1333,7 +1339,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       const int bside = P.nr[g] <= P.nl[g] ? 1 : 0;
       const uint64_t nb = bside ? P.nr[g] : P.nl[g], np = bside ? P.nl[g] : P.nr[g];
       uint32_t cbits = pow2ceil((nb + kCoarseTarget - 1) / kCoarseTarget);
-      cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, 10));
+      cbits = std::max<uint32_t>(1, std::min<uint32_t>(cbits, kCoarseBitsMax));
       const uint32_t NC = 1u << cbits;
       const double mb = (double)nb / NC, mp = (double)np / NC;
       const uint64_t cb = region_cap(mb, (double)nb, 4.0 * D.num_sms), cp = region_cap(mp, (double)np, 4.0 * D.num_sms);

@@ -173,7 +173,7 @@ __global__ void k_groups(GroupArgs g) {
 }
 
 // Per (batch, side): the nonempty rectangles X-run(xw_total - w) x Y-run(w) over the Y runs w,
-// oriented for the warp tile (longer run across lanes) with their warp-tile offsets.  Count mode
+// oriented for the warp tile (lanes_over_x: the cheaper way) with their warp-tile offsets.  Count mode
 // (rects == nullptr) only produces the per-(batch, side) tile and rectangle totals the host needs
 // to plan waves; write mode fills the compacted rectangle list at rect_base[2g + side].
 __global__ void k_rects(RectArgs p) {
@@ -200,7 +200,8 @@ __global__ void k_rects(RectArgs p) {
         ys = s.ys[r];
         yl = s.ylen[r];
         if (xl) {
-          const uint32_t L = xl > yl ? xl : yl, Q = xl > yl ? yl : xl;
+          const bool lx = lanes_over_x(xl, yl);
+          const uint32_t L = lx ? xl : yl, Q = lx ? yl : xl;
           tiles = ((L + 31) / 32) * ((Q + kTQ - 1) / kTQ);
         }
       }
@@ -210,7 +211,7 @@ __global__ void k_rects(RectArgs p) {
     const uint32_t rpos = block_excl_scan(tiles > 0, rtot);
     if (write && tiles) {
       RectDesc R;
-      const bool lx = xl >= yl;
+      const bool lx = lanes_over_x(xl, yl);
       R.gs_x = ((uint32_t)(g * 2 + side) << 1) | (lx ? 1u : 0u);
       R.lane_start = lx ? xs : ys;
       R.loop_start = lx ? ys : xs;

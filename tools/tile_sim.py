@@ -32,3 +32,18 @@ for a in range(len(hl)):
         slots16+=int((nl16*16*qslots).sum())
         slots_flat+=int((((L*Q)+31)//32*32).sum())
 print("keys",keys,"util cur %.3f q2 %.3f lane16 %.3f flat %.3f"%(keys/slots_cur, keys/slots_q2, keys/slots16, keys/slots_flat))
+# orientation by utilisation (lanes over whichever run wastes less)
+def slots(L, Q):
+    return ((L + 31) // 32) * 32 * ((Q // 32) * 32 + (((Q % 32) + 3) // 4) * 4)
+keys=0; s_cur=0; s_best=0
+for a in range(len(hl)):
+    b=T-a
+    if hl[a]==0 or b<0 or b>=len(hr) or hr[b]==0: continue
+    for X,Y,tot in ((h[0],h[1],a),(h[2],h[3],b)):
+        ys=np.nonzero(Y)[0]; xs=tot-ys; ok=(xs>=0)&(xs<len(X)); ys=ys[ok]; xs=xs[ok]
+        Lx=X[xs]; Ly=Y[ys]; ok=Lx>0; Lx=Lx[ok]; Ly=Ly[ok]
+        L=np.maximum(Lx,Ly); Q=np.minimum(Lx,Ly)
+        keys+=int((L*Q).sum())
+        a1=slots(L,Q); a2=slots(Q,L)
+        s_cur+=int(a1.sum()); s_best+=int(np.minimum(a1,a2).sum())
+print("orientation: longer-across %.3f best-of-two %.3f" % (keys/s_cur, keys/s_best))
