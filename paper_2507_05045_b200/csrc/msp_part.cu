@@ -471,50 +471,73 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
 
 // Level 2 of the huge-batch path: stream already-hashed keys back from coarse bucket regions
 // (HBM) and re-partition them into fine buckets (L2 scratch) for the join.  One work chunk: slots
-// [s0, s1) of ONE source (a coarse region of one role, holding exactly `fill` keys, which spread
-// uniformly over its NF fine buckets), re-partitioned by the CTA.  Fine bucket = floor(frac * NF /
-// 2^32), frac = the key's position inside its coarse bucket (the low word of hi * NC).  Ends with
-// a barrier.
+// [s0, s1) of ONE source (a coarse region of one role, holding `fill` keys and run pads, which
+// spread uniformly over its NF fine buckets), re-partitioned by the CTA.  Fine bucket = floor(frac *
+// NF / 2^32), frac = the key's position inside its coarse bucket (the low word of hi * NC).  The
+// keys arrive by TMA bulk copies in steps of kRStep keys through two shared buffers behind the
+// stage (the next step always in flight), so the pass is bound by the staging, not by HBM latency.
+// Ends with a barrier.
+constexpr uint32_t kRStep = 4 * kScatterThreads;  // keys per step: 4 per thread
+size_t rescatter_smem_bytes() { return sizeof(Stage) + 2ull * kRStep * 8; }
+
 __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, const RescatterSrc &src, uint32_t s0,
                                                 uint32_t s1) {
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  volatile uint32_t *round_end = &g.round_end;
-  constexpr int N = MSP_RESCATTER_N;  // keys per lane per step; the next step's keys are in flight meanwhile (HBM)
+  const uint32_t tid = threadIdx.x;
   const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
   uint32_t C, budget, staged = 0;
   stage_geometry(NB, C, budget);
-  const uint32_t stride = kScatterThreads;
-  uint32_t idx = s0 + warp * 32 + lane;
-  unsigned long long nxt[N];
-#pragma unroll
-  for (int u = 0; u < N; ++u) {
-    const uint32_t x = idx + u * stride;
-    nxt[u] = x < s1 ? __ldcs(src.keys + x) : 0ull;
-  }
-  while (true) {
-    while (idx - lane < s1 && !*round_end) {
-      unsigned long long key[N];
-      uint32_t j[N];
-      bool ok[N];
-#pragma unroll
-      for (int u = 0; u < N; ++u) {
-        key[u] = nxt[u];
-        ok[u] = idx + u * stride < s1 && key[u] != 0ull;  // (0: a run pad)
-        const uint32_t x = idx + (N + u) * stride;
-        nxt[u] = x < s1 ? __ldcs(src.keys + x) : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < N; ++u) j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
-      stage_keys<N>(g, S, ebase, C, staged, budget, key, j, ok);
-      idx += N * stride;
-    }
+  unsigned long long *buf = reinterpret_cast<unsigned long long *>(&g + 1);  // 2 x kRStep keys
+  __shared__ unsigned long long s_rbar[2];
+  const uint32_t nstep = s1 > s0 ? (s1 - s0 + kRStep - 1) / kRStep : 0;
+  auto issue = [&](uint32_t c) {  // thread 0: step c into buffer c & 1
+    const uint32_t a = s0 + c * kRStep, n = min(s1 - a, kRStep);
     fence_proxy_async_smem();
-    const bool more = __syncthreads_or(idx - lane < s1);
-    flush_round(g, S, ebase, NB, C);
-    staged = 0;
-    if (!more) break;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[c & 1])), "r"(8u * ((n + 1u) & ~1u)) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(buf + (c & 1) * kRStep)), "l"(src.keys + a),
+                    "r"(8u * ((n + 1u) & ~1u)), "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[c & 1])) : "memory");
+  };
+  if (tid == 0) {
+    for (int k = 0; k < 2; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[k])) : "memory");
+    for (uint32_t c = 0; c < 2 && c < nstep; ++c) issue(c);
   }
+  __syncthreads();
+  uint32_t ph[2] = {0, 0};
+  for (uint32_t c = 0; c < nstep; ++c) {
+    const uint32_t bsel = c & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(done) : "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[bsel])), "r"(ph[bsel]) : "memory");
+    ph[bsel] ^= 1u;
+    const uint32_t n = min(s1 - (s0 + c * kRStep), kRStep);
+    const unsigned long long *bk = buf + bsel * kRStep;
+    unsigned long long key[4];
+    uint32_t j[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = tid + u * kScatterThreads;
+      key[u] = bk[min(i, kRStep - 1)];
+      ok[u] = i < n && key[u] != 0ull;  // (0: a run pad)
+      j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
+    }
+    stage_keys<4>(g, S, ebase, C, staged, budget, key, j, ok);
+    fence_proxy_async_smem();  // (the staged keys -> a flush's bulk copies)
+    const bool end = __syncthreads_or(g.round_end != 0u) || c + 1 == nstep;  // (the buffer is free)
+    if (tid == 0 && c + 2 < nstep) issue(c + 2);
+    if (end) {
+      flush_round(g, S, ebase, NB, C);
+      staged = 0;
+    }
+  }
+  if (tid == 0)
+    for (int k = 0; k < 2; ++k)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[k])) : "memory");
   bulk_complete();
+  __syncthreads();
 }
 
 // Level 2 of the huge-batch path as its own launch (MSP_FLAG_WAVE_LAUNCHES): stream already-hashed
@@ -955,7 +978,7 @@ cudaError_t launch_scatter(int mc, const ScatterArgs &args, const PartArgs &p, i
 
 template <int MC>
 static cudaError_t launch_waves_mc(const WavesArgs &w, int grid, cudaStream_t st) {
-  const size_t sm = std::max(scatter_smem_bytes(stride_for(MC)), sizeof(JoinSmem));
+  const size_t sm = std::max({scatter_smem_bytes(stride_for(MC)), sizeof(JoinSmem), rescatter_smem_bytes()});
   if (cudaError_t e = smem_attr((const void *)k_waves<MC>, sm)) return e;
   k_waves<MC><<<grid, kScatterThreads, sm, st>>>(w);
   return cudaGetLastError();
@@ -975,7 +998,7 @@ cudaError_t launch_waves(int mc, const WavesArgs &w, int num_sms, cudaStream_t s
 }
 
 cudaError_t launch_rescatter(const RescatterArgs &r, const PartArgs &p, int num_sms, cudaStream_t st) {
-  const size_t sm = sizeof(Stage);
+  const size_t sm = rescatter_smem_bytes();
   if (cudaError_t e = smem_attr((const void *)k_rescatter, sm)) return e;
   if (!r.nchunks) return cudaSuccess;
   const uint32_t slots = (uint32_t)num_sms * kScatterCtas;
