@@ -75,3 +75,17 @@ def test_no_cpu_fallback_without_a_gpu(lib):
     inst = msb.generate_instance(4, 100, 11)
     with pytest.raises(RuntimeError, match="CUDA"):
         msb.solve(inst, msb.SolverConfig(mode="all"))
+
+
+def test_integration_stub_structs_match_the_abi(lib):
+    """The ctypes stub INTEGRATION.md tells a reference maintainer to paste matches the C layout."""
+    import re as _re
+
+    text = open(os.path.join(os.path.dirname(_native.INCLUDE), "INTEGRATION.md")).read()
+    code = _re.search(r"```python\n(import ctypes as C.*?)\n_cuda = None", text, flags=_re.S).group(1)
+    ns: dict = {}
+    exec(code, ns)  # noqa: S102 -- the documented stub itself
+    out = (C.c_int32 * 4)()
+    lib.msp_abi_sizes(out)
+    assert list(out) == [C.sizeof(ns["_Problem"]), C.sizeof(ns["_Options"]), C.sizeof(ns["_Stats"]),
+                         C.sizeof(ns["_Result"])]
