@@ -211,6 +211,16 @@ def workload_config(inst, name, total_pairs, plan) -> dict:
             "row1_candidate_pairs": int(sum(p[2] * p[3] for p in plan)), "batches": len(plan)}
 
 
+def all_reduce(t, dist, op):
+    """all_reduce that also works on gloo (CPU tensors)."""
+    if dist.get_backend() == "nccl":
+        dist.all_reduce(t, op=op)
+        return t
+    c = t.cpu()
+    dist.all_reduce(c, op=op)
+    return c.to(t.device)
+
+
 def headline_9_80(world, rank, local, dist, dev):
     """One full (9,80) s1 enumeration (BASELINE north star), sharded over the ranks like the bench
     workload; device time of each rank's band by CUDA events, max over ranks."""
@@ -240,10 +250,8 @@ def headline_9_80(world, rank, local, dist, dev):
     t = torch.tensor([e0.elapsed_time(e1) / 1e3, wall, float(len(sols)), float(st.get("hash_hits", 0))],
                      dtype=torch.float64, device=dev)
     if world > 1:
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        mx = all_reduce(t.clone(), dist, dist.ReduceOp.MAX)
+        sm = all_reduce(t.clone(), dist, dist.ReduceOp.SUM)
         t = torch.stack([mx[0], mx[1], sm[2], sm[3]])
     pairs = int(sum(p[2] + p[3] for p in plan))
     return {"workload": "(9,80) generate_instance(m=9, K=100, seed=1), full enumeration, one solve",
@@ -283,10 +291,17 @@ def main() -> int:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (test hooks for a one-GPU box: every rank on GPU 0, gloo collectives)
+    if os.environ.get("MSP_BENCH_SAME_DEVICE") == "1":
+        local = 0
+    backend = os.environ.get("MSP_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _native.load()
     plan = _native.alpha_plan(inst.a, inst.d, device=local)
     total_pairs = sum(p[2] + p[3] for p in plan)
@@ -327,7 +342,7 @@ def main() -> int:
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
     t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = all_reduce(t, dist, dist.ReduceOp.MAX)
     max_ms = float(t.item())
     value = total_pairs * args.steps / (max_ms * 1e-3)
 
@@ -346,7 +361,7 @@ def main() -> int:
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = all_reduce(te, dist, dist.ReduceOp.MAX)
     e2e_value = total_pairs * args.steps / float(te.item())
     h2d = 8 * inst.m * inst.n + 8 * inst.m
     d2h = inst.n * max(1, len(ref_sols)) + 256  # solution bit vectors + stats record
