@@ -477,7 +477,8 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
 // keys arrive by TMA bulk copies in steps of kRStep keys through two shared buffers behind the
 // stage (the next step always in flight), so the pass is bound by the staging, not by HBM latency.
 // Ends with a barrier.
-constexpr uint32_t kRStep = 4 * kScatterThreads;  // keys per step: 4 per thread
+constexpr uint32_t kRStep = 2048;                 // keys per step (two 16 KB buffers)
+constexpr int kRPerThread = (kRStep + kScatterThreads - 1) / kScatterThreads;
 size_t rescatter_smem_bytes() { return sizeof(Stage) + 2ull * kRStep * 8; }
 
 __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, const RescatterSrc &src, uint32_t s0,
@@ -514,17 +515,17 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
     ph[bsel] ^= 1u;
     const uint32_t n = min(s1 - (s0 + c * kRStep), kRStep);
     const unsigned long long *bk = buf + bsel * kRStep;
-    unsigned long long key[4];
-    uint32_t j[4];
-    bool ok[4];
+    unsigned long long key[kRPerThread];
+    uint32_t j[kRPerThread];
+    bool ok[kRPerThread];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kRPerThread; ++u) {
       const uint32_t i = tid + u * kScatterThreads;
       key[u] = bk[min(i, kRStep - 1)];
       ok[u] = i < n && key[u] != 0ull;  // (0: a run pad)
       j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
     }
-    stage_keys<4>(g, S, ebase, C, staged, budget, key, j, ok);
+    stage_keys<kRPerThread>(g, S, ebase, C, staged, budget, key, j, ok);
     fence_proxy_async_smem();  // (the staged keys -> a flush's bulk copies)
     const bool end = __syncthreads_or(g.round_end != 0u) || c + 1 == nstep;  // (the buffer is free)
     if (tid == 0 && c + 2 < nstep) issue(c + 2);
