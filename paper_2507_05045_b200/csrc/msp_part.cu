@@ -277,7 +277,19 @@ __device__ __forceinline__ uint4 ld_tile(const TileDesc *t, uint32_t i, uint32_t
 #define MSP_FOLD_PTX 0
 #endif
 __device__ __forceinline__ void fold(uint32_t &lo, uint32_t &hi, uint32_t v) {
-#if MSP_FOLD_PTX
+#if MSP_FOLD_PTX == 2
+  // LOP3 (x), IMAD.WIDE (x * 435), IMAD (hi * 435 + carry), LEA ((x << 8) + that): two FMA-pipe and
+  // two ALU-pipe instructions per step (the plain C++ form compiles the shift-add to a third IMAD,
+  // leaving the hash steps FMA-pipe bound)
+  asm("{\n\t.reg .u32 x, u, s, c;\n\t.reg .u64 p;\n\t"
+      "xor.b32 x, %0, %2;\n\t"
+      "mul.wide.u32 p, x, 435;\n\t"
+      "mov.b64 {%0, c}, p;\n\t"
+      "mad.lo.u32 u, %1, 435, c;\n\t"
+      "shl.b32 s, x, 8;\n\t"
+      "add.u32 %1, u, s;\n\t}"
+      : "+r"(lo), "+r"(hi) : "r"(v));
+#elif MSP_FOLD_PTX
   asm("{\n\t.reg .u32 x, t1, t3, c;\n\t.reg .u64 p;\n\t"
       "xor.b32 x, %0, %2;\n\t"
       "mul.lo.u32 t1, %1, 435;\n\t"
