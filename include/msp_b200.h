@@ -50,8 +50,12 @@ enum msp_flags {
                                        (results invalid; never set in a real solve) */
   MSP_FLAG_WAVE_LAUNCHES = 1u << 4, /* partitioned waves as per-wave scatter + join launches instead
                                        of the persistent pipeline (parity testing) */
-  MSP_FLAG_BATCH_STATS = 1u << 5    /* fill msp_result.batch_stats: one row per batch, the per-batch
+  MSP_FLAG_BATCH_STATS = 1u << 5,   /* fill msp_result.batch_stats: one row per batch, the per-batch
                                        ValidationStats of validate_chunked (validate.py:63-71,316-379) */
+  MSP_FLAG_DEGENERATE_HASH = 1u << 6 /* test seam: every key hashes to 0 (the reference's encode_fn
+                                       injection, validate.py:161-162,208-216): hash_hits = every
+                                       unfiltered (left, right) pair; exact confirmation unchanged.
+                                       Runs the global-table join. */
 };
 
 typedef struct {

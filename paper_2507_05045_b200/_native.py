@@ -28,6 +28,7 @@ MSP_FLAG_JOIN_GLOBAL = 1 << 2
 MSP_FLAG_DIAG_HASH_ONLY = 1 << 3
 MSP_FLAG_WAVE_LAUNCHES = 1 << 4
 MSP_FLAG_BATCH_STATS = 1 << 5
+MSP_FLAG_DEGENERATE_HASH = 1 << 6
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

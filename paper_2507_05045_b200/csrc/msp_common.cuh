@@ -88,6 +88,7 @@ struct EnumArgs {
   uint64_t nchunks;
   uint32_t dpack[8];         // d rows 1..m-1 packed, +0x8000 guard per half (right side)
   uint32_t diag;             // MSP_FLAG_DIAG_HASH_ONLY: hash without staging (timing only)
+  uint64_t key_mask;         // keys & key_mask (~0; MSP_FLAG_DEGENERATE_HASH: 0, every pair collides)
   unsigned long long *batch_filtered; // per batch (gid)
   unsigned long long *batch_hits;     // per batch (gid)
 };

@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTab
       begin_tile<MC>(A, W, lane, C);
       while (C.q < C.q1) {
         if constexpr (kBulk) {
-          step_keys<MC>(W, C, dg, filt, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
+          step_keys<MC>(W, C, dg, filt, A.key_mask, [&](int, uint64_t key, bool ok, uint32_t, uint32_t) {
             if (ok && W.d.npass > 1 && pass_of(key, W.d.npass) != W.d.pass) ok = false;
             const uint32_t m = __ballot_sync(0xffffffffu, ok);
             if (ok) stage[cnt + __popc(m & lt_mask)] = key;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(256, 2) k_enum(const EnumArgs A, const JoinTab
           uint32_t li[kU], qi[kU];
 #pragma unroll
           for (int u = 0; u < kU; ++u) { okk[u] = false; kk[u] = 0; li[u] = qi[u] = 0; }
-          step_keys<MC>(W, C, dg, filt, [&](int u, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
+          step_keys<MC>(W, C, dg, filt, A.key_mask, [&](int u, uint64_t key, bool ok, uint32_t lidx, uint32_t qidx) {
             kk[u] = key; okk[u] = ok; li[u] = lidx; qi[u] = qidx;
           });
           sink_batch<KIND>(jt, W.d, kk, okk, W.R, li, qi, A, hits, rfilt);

@@ -795,6 +795,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   jt.nhits = D.nhits.as<unsigned long long>();
   jt.hit_cap = hit_cap;
   jt.err = D.err.as<int>();
+  P.base.key_mask = (opt->flags & MSP_FLAG_DEGENERATE_HASH) ? 0ull : ~0ull;  // (every k_enum launch)
   EnumArgs A = P.base;
   A.diag = (opt->flags & MSP_FLAG_DIAG_HASH_ONLY) ? 1u : 0u;
   A.batch_filtered = D.bfilt.as<unsigned long long>();
@@ -1067,7 +1068,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   for (uint32_t g = 0; g < P.G; ++g) {
     const uint64_t nb = std::min(P.nl[g], P.nr[g]), np = std::max(P.nl[g], P.nr[g]);
     const uint64_t nbk = std::max<uint64_t>(1, (nb + kBucketTargetMax - 1) / kBucketTargetMax);
-    if (opt->flags & MSP_FLAG_JOIN_GLOBAL)
+    if (opt->flags & (MSP_FLAG_JOIN_GLOBAL | MSP_FLAG_DEGENERATE_HASH))
       global_b.push_back(g);
     else if (nbk > (uint64_t)std::min<uint32_t>(wave_buckets, kMaxUnitBuckets) || nb + np > key_budget)
       huge_b.push_back(g);

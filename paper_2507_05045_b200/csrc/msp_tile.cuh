@@ -149,7 +149,7 @@ __device__ __forceinline__ void lds_vec(const uint32_t *p, uint32_t (&v)[SW]) {
 template <int MC, class Walker, class Fn>
 __device__ __forceinline__ void step_keys(const Walker &W, TileCursor<stride_for(MC)> &C,
                                           const uint32_t (&dg)[words_for(MC) > 0 ? words_for(MC) : 1],
-                                          unsigned long long &filt, Fn &&fn) {
+                                          unsigned long long &filt, uint64_t kmask, Fn &&fn) {
   constexpr int NW0 = words_for(MC);           // companion words (0 when m == 1)
   constexpr int NW = NW0 > 0 ? NW0 : 1;        // array extent
   constexpr int SW = stride_for(MC);
@@ -193,7 +193,7 @@ __device__ __forceinline__ void step_keys(const Walker &W, TileCursor<stride_for
   }
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (q + u < C.q1) fn(u, ((uint64_t)hi[u] << 32) | lo[u], ok[u], C.lidx, W.R.loop_start + q + u);
+    if (q + u < C.q1) fn(u, (((uint64_t)hi[u] << 32) | lo[u]) & kmask, ok[u], C.lidx, W.R.loop_start + q + u);
   C.q = q + U;
 }
 

@@ -595,3 +595,22 @@ def test_cancel_word_stops_a_running_solve(tmp_path):
         assert st["cancelled"] == 1 and dt < 5.0
     finally:
         flag.close(unlink=True)
+
+
+def test_degenerate_hash_seam_counts_every_pair():
+    """The reference's degenerate-hash injection (validate.py:161-162,208-216; test_validate.py:197-241):
+    with every key hashed to one value, every unfiltered (left, right) pair of a batch is a hash hit,
+    so hash_hits = sum over batches of n_left x (n_right - filtered); the exact confirmation still
+    finds exactly the true solutions."""
+    for (m, s) in ((3, 5), (4, 11), (4, 12)):
+        inst = msb.generate_instance(m, 100, s) if m > 3 else seeded_instance(s, m=3, n=16, k=20)
+        ref = _solve_all(inst)
+        opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_DEGENERATE_HASH | _native.MSP_FLAG_BATCH_STATS
+                                    | _native.MSP_FLAG_FORCE_TABLE_PATH)
+        rc, xb, st = _native.solve_raw(inst.a, inst.d, opts)
+        assert rc == 0, _native.last_error()
+        expect = sum(nl * (nr - filt) for _, nl, nr, filt, _ in st["batch_stats"])
+        assert st["hash_hits"] == expect, (m, s)
+        assert st["exact_hits"] == ref.stats.exact_hits
+        assert sorted(map(tuple, xb.tolist())) == sorted(ref.solutions)
+        assert st["filtered_residuals"] == ref.stats.filtered_residuals
