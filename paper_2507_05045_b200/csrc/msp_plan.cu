@@ -184,14 +184,8 @@ __global__ void k_rects_sparse(RectSparseSide L, RectSparseSide R, const uint64_
       const uint64_t p = S.val[off + r];
       const uint32_t x = (uint32_t)(p / S.ny), y = (uint32_t)(p - (uint64_t)x * S.ny);
       const uint32_t xs = S.xs[x], xl = S.xl[x], ys = S.ys[y], yl = S.yl[y];
-      const bool lx = lanes_over_x(xl, yl);
-      D.gs_x = ((uint32_t)(g * 2 + side) << 1) | (lx ? 1u : 0u);
-      D.lane_start = lx ? xs : ys;
-      D.loop_start = lx ? ys : xs;
-      D.L = lx ? xl : yl;
-      D.Q = lx ? yl : xl;
-      D.nl = (D.L + 31) / 32;
-      D.nq = (D.Q + kTQ - 1) / kTQ;
+      // one piece per run pair (the segment counts fixed the rectangle bases): the cheaper orientation
+      D = rect_piece(g * 2 + side, lanes_over_x(xl, yl), xs, xl, ys, yl);
       t = D.nl * D.nq;
     }
     uint32_t tot;

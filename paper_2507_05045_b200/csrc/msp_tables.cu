@@ -190,37 +190,27 @@ __global__ void k_rects(RectArgs p) {
   const size_t gs = (size_t)g * 2 + side;
   for (uint32_t r0 = 0; r0 < ny; r0 += blockDim.x) {
     const uint32_t r = r0 + threadIdx.x;
-    uint32_t tiles = 0, xs = 0, xl = 0, ys = 0, yl = 0;
+    uint32_t tiles = 0, np = 0;
+    RectDesc pc[2];
     if (r < ny) {
       const uint32_t wy = s.yw[r];
       if (wy <= xw_total && xw_total - wy <= s.SX) {
         const uint32_t wx = (uint32_t)(xw_total - wy);
-        xs = s.x_start[wx];
-        xl = s.x_end[wx] - xs;
-        ys = s.ys[r];
-        yl = s.ylen[r];
-        if (xl) {
-          const bool lx = lanes_over_x(xl, yl);
-          const uint32_t L = lx ? xl : yl, Q = lx ? yl : xl;
-          tiles = ((L + 31) / 32) * ((Q + kTQ - 1) / kTQ);
-        }
+        const uint32_t xs = s.x_start[wx];
+        np = rect_pieces((uint32_t)gs, xs, s.x_end[wx] - xs, s.ys[r], s.ylen[r], pc);
+        for (uint32_t k = 0; k < np; ++k) tiles += pc[k].nl * pc[k].nq;
       }
     }
     uint32_t ttot, rtot;
     const uint32_t tpos = block_excl_scan(tiles, ttot);
-    const uint32_t rpos = block_excl_scan(tiles > 0, rtot);
-    if (write && tiles) {
-      RectDesc R;
-      const bool lx = lanes_over_x(xl, yl);
-      R.gs_x = ((uint32_t)(g * 2 + side) << 1) | (lx ? 1u : 0u);
-      R.lane_start = lx ? xs : ys;
-      R.loop_start = lx ? ys : xs;
-      R.L = lx ? xl : yl;
-      R.Q = lx ? yl : xl;
-      R.tile_off = (uint32_t)(tbase + tpos);
-      R.nl = (R.L + 31) / 32;
-      R.nq = (R.Q + kTQ - 1) / kTQ;
-      out[rbase + rpos] = R;
+    const uint32_t rpos = block_excl_scan(np, rtot);
+    if (write) {
+      uint32_t t = (uint32_t)(tbase + tpos);
+      for (uint32_t k = 0; k < np; ++k) {
+        pc[k].tile_off = t;
+        t += pc[k].nl * pc[k].nq;
+        out[rbase + rpos + k] = pc[k];
+      }
     }
     tbase += ttot;
     rbase += rtot;

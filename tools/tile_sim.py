@@ -47,3 +47,24 @@ for a in range(len(hl)):
         a1=slots(L,Q); a2=slots(Q,L)
         s_cur+=int(a1.sum()); s_best+=int(np.minimum(a1,a2).sum())
 print("orientation: longer-across %.3f best-of-two %.3f" % (keys/s_cur, keys/s_best))
+# split each rectangle into its full 32-lane part and the remainder, each oriented the cheaper way
+def best(L, Q):
+    return np.minimum(slots(L, Q), slots(Q, L))
+def split_slots(L, Q, depth=2):
+    # orient the rectangle the cheaper way, then carve off the full lane tiles and re-plan the rest
+    lx = slots(L, Q) <= slots(Q, L)
+    A = np.where(lx, L, Q); B = np.where(lx, Q, L)
+    full = (A // 32) * 32; r = A - full
+    main = np.where(full > 0, slots(full, B), 0)
+    rem = np.where(r > 0, (split_slots(r, B, depth - 1) if depth > 1 else best(r, B)), 0)
+    return np.where((full > 0) & (r > 0), main + rem, best(L, Q))
+keys=0; s_split=0; s_split3=0
+for a in range(len(hl)):
+    b=T-a
+    if hl[a]==0 or b<0 or b>=len(hr) or hr[b]==0: continue
+    for X,Y,tot in ((h[0],h[1],a),(h[2],h[3],b)):
+        ys=np.nonzero(Y)[0]; xs=tot-ys; ok=(xs>=0)&(xs<len(X)); ys=ys[ok]; xs=xs[ok]
+        Lx=X[xs]; Ly=Y[ys]; ok=Lx>0; Lx=Lx[ok].astype(np.int64); Ly=Ly[ok].astype(np.int64)
+        keys+=int((Lx*Ly).sum())
+        s_split+=int(split_slots(Lx,Ly,1).sum()); s_split3+=int(split_slots(Lx,Ly,3).sum())
+print("split remainder: depth1 %.3f depth3 %.3f" % (keys/s_split, keys/s_split3))
