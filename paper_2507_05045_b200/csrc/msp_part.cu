@@ -603,7 +603,8 @@ struct JoinSmem {
   unsigned long long bhits[kJoinThreads / 32];
   unsigned long long mbar[2];           // one per chunk buffer
   uint32_t nstash, ovf, pad[2];
-  alignas(16) unsigned long long buf[2][kJChunk];  // (bulk-copy destinations: 16-byte aligned)
+  alignas(16) unsigned long long buf[2][kJChunk + 64];  // (bulk-copy destinations: 16-byte aligned;
+                                                          // +64: unrolled warps read past a chunk's end)
 };
 static_assert(offsetof(JoinSmem, buf) % 16 == 0, "bulk copy alignment");
 
@@ -645,6 +646,13 @@ __device__ __forceinline__ uint32_t zero_byte_mask32(uint32_t x) {
 }
 // Some byte of x is zero (exact for presence).
 __device__ __forceinline__ uint32_t has_zero_byte(uint32_t x) { return (x - 0x01010101u) & ~x & 0x80808080u; }
+// 64-bit load from a 32-bit shared-window address (keeps the compiler from re-deriving the
+// window base from a generic pointer on every access in the join's inner loops)
+__device__ __forceinline__ unsigned long long lds64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
 
 __device__ __forceinline__ void join_insert(JoinSmem &T, unsigned long long k) {
   const uint32_t t = jmix(k), fpb = jfp4(k) & 0xFFu;
@@ -767,11 +775,13 @@ __device__ MSP_JOIN_INLINE void join_group(JoinSmem &T, const PartArgs &S, uint3
       mbar_wait(&T.mbar[bf], bf ? ph1 : ph0);
       if (bf) ph1 ^= 1u; else ph0 ^= 1u;
       const unsigned long long *ck = T.buf[bf];
-      if (c < nbc) {  // ---- build chunk: insert
+      const uint32_t cks = smem_u32(ck);
+      if (c < nbc) {  // ---- build chunk: insert (two keys per thread per step)
         const uint32_t n = min(nbuild - c * kJChunk, (uint32_t)kJChunk);
-        for (uint32_t i = tid; i < n; i += NT) {
-          const unsigned long long k = ck[i];
-          if (k != 0ull) join_insert(T, k);  // (0: a run pad)
+        for (uint32_t i = tid; i < n; i += 2 * NT) {
+          const unsigned long long k0 = lds64(cks + 8u * i), k1 = lds64(cks + 8u * min(i + NT, (uint32_t)kJChunk));
+          if (k0 != 0ull) join_insert(T, k0);  // (0: a run pad)
+          if (k1 != 0ull && i + NT < n) join_insert(T, k1);
         }
         __syncthreads();  // buffer released; after the last build chunk the table is complete
         if (c + 1 == nbc) {
@@ -781,12 +791,15 @@ __device__ MSP_JOIN_INLINE void join_group(JoinSmem &T, const PartArgs &S, uint3
         }
       } else {        // ---- probe chunk: fast test, branch-free; possible hits to the warp's queue
         const uint32_t n = min(nprobe - (c - nbc) * kJChunk, (uint32_t)kJChunk);
+        const uint32_t fps = smem_u32(T.fp);
         for (uint32_t i = tid; i - lane < n; i += NT) {  // (whole warps iterate: the exit is warp-uniform)
-          const unsigned long long k = ck[min(i, n - 1)];
+          // (a pad -- key 0 -- may be probed: pads are never inserted and real zero keys never reach
+          // the scratch, so its count is 0)
+          const unsigned long long k = lds64(cks + 8u * i);
           const uint32_t pat = jfp4(k);
-          const unsigned long long w = T.fp[jb1(jmix(k))];
+          const unsigned long long w = lds64(fps + 8u * jb1(jmix(k)));
           const bool maybe = ((has_zero_byte((uint32_t)w ^ pat) | has_zero_byte((uint32_t)(w >> 32) ^ pat)) != 0u ||
-                              (long long)w < 0) && i < n && k != 0ull;
+                              (long long)w < 0) && i < n;
           const uint32_t mm = __ballot_sync(0xffffffffu, maybe);
           if (nqw + __popc(mm) > kQW) {  // the warp's segment is full: count its queued probes now
             for (uint32_t q = lane; q < nqw; q += 32) probe_slow(qw[q]);
