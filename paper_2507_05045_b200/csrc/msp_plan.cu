@@ -14,7 +14,10 @@
 //   4. a batch per distinct alpha whose beta = t - alpha is a right sum (binary search), in the
 //      alpha band of this shard,
 //   5. the oriented rectangle lists (RectDesc, as the dense k_rects writes them) of every batch side.
-// Work is O(runs_A * runs_B + runs_C * runs_D); bounded here at 2^27 pair sums per side.
+// Work is O(runs_A * runs_B + runs_C * runs_D) pair sums, streamed through alpha WINDOWS: the alpha
+// range is cut into consecutive windows [lo, hi) each holding at most a budget of run pairs per side
+// (left sums in [lo, hi), right sums in (t - hi, t - lo]; default 2^27, MSP_SPARSE_WINDOW_PAIRS),
+// found by binary search on the per-side pair-count function; steps 2-5 run per window and append.
 // The sort, scans and compactions are CUB device primitives (library code for the plan stage; the
 // hot path stays hand-written).
 #include <cstdint>
@@ -23,6 +26,8 @@
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <cstdlib>
 
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -46,6 +51,21 @@ struct Buf {
     if (e == cudaSuccess) cap = c;
     return e;
   }
+  // grow to at least `bytes`, keeping the first `keep` bytes (stream-ordered copy)
+  cudaError_t grow_keep(size_t bytes, size_t keep, cudaStream_t st) {
+    if (bytes <= cap) return cudaSuccess;
+    void *q = nullptr;
+    const size_t c = bytes + bytes / 2 + 256;
+    cudaError_t e = cudaMalloc(&q, c);
+    if (e != cudaSuccess) return e;
+    if (keep) e = cudaMemcpyAsync(q, p, keep, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { cudaFree(q); return e; }
+    if (p) cudaFree(p);
+    p = q;
+    cap = c;
+    return cudaSuccess;
+  }
   template <class T> T *as() const { return reinterpret_cast<T *>(p); }
 };
 
@@ -53,6 +73,7 @@ struct Work {
   Buf flag, starts, cnt1;                      // run compaction
   Buf rw[4], rs[4], rl[4];                     // distinct-weight runs of each table
   Buf k0, k1, v0, v1, pc, tmp;                 // pair sort and pair counts (scratch)
+  Buf xcnt, xoff, wtot;                        // window: pairs per X-run, their offsets, side totals
   Buf ids[2], ukey[2], usum[2], ulen[2], uoff[2], nun[2], ukey2;  // per side
   Buf bflag, ridx, sel, nb, hdr, rbase, tiles, rects, err;        // batches
 };
@@ -84,14 +105,76 @@ __global__ void k_run_info(const uint64_t *w, uint32_t n, const uint32_t *starts
   }
 }
 
-// Every (X-run, Y-run) pair: its weight sum (key) and the pair id x * ny + y (payload).
-__global__ void k_pair_sums(const uint64_t *xw, uint32_t nx, const uint64_t *yw, uint32_t ny, uint64_t *key,
-                            uint64_t *val) {
-  const uint64_t np = (uint64_t)nx * ny;
-  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < np; p += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t x = (uint32_t)(p / ny), y = (uint32_t)(p - (uint64_t)x * ny);
-    key[p] = xw[x] + yw[y];
-    val[p] = p;
+// Y-runs y with wx + wy in [lo, hi): an index range of the sorted Y run weights (ascending for B,
+// descending for D).
+template <bool DESC>
+__device__ __forceinline__ void y_range(const uint64_t *yw, uint32_t ny, uint64_t wx, uint64_t lo, uint64_t hi,
+                                        uint32_t &b, uint32_t &e) {
+  b = e = 0;
+  if (wx >= hi) return;
+  const uint64_t a = lo > wx ? lo - wx : 0, z = hi - wx;  // wy in [a, z)
+  auto first = [&](uint64_t v) {  // ASC: first wy >= v; DESC: first wy < v
+    uint32_t l = 0, h = ny;
+    while (l < h) {
+      const uint32_t m = (l + h) >> 1;
+      if (DESC ? (yw[m] >= v) : (yw[m] < v)) l = m + 1; else h = m;
+    }
+    return l;
+  };
+  if (DESC) { b = first(z); e = first(a); } else { b = first(a); e = first(z); }
+  if (e < b) e = b;
+}
+
+// Pairs of one side whose sum lies in [lo, hi): per X-run count (optional) and the side total.
+template <bool DESC>
+__global__ void k_window_count(const uint64_t *xw, uint32_t nx, const uint64_t *yw, uint32_t ny, uint64_t lo,
+                               uint64_t hi, uint64_t *xcnt, unsigned long long *total) {
+  uint64_t acc = 0;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nx; x += gridDim.x * blockDim.x) {
+    uint32_t b, e;
+    y_range<DESC>(yw, ny, xw[x], lo, hi, b, e);
+    if (xcnt) xcnt[x] = e - b;
+    acc += e - b;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc && total) atomicAdd(total, (unsigned long long)acc);
+}
+
+// Window search: pairs of one side with sums in [a[c], z[c]) for up to kProbe candidate windows at
+// once (blockIdx.y = candidate), one 64-bit total per candidate.
+constexpr int kProbe = 32;
+struct WinProbe { uint64_t a[kProbe], z[kProbe]; };
+template <bool DESC>
+__global__ void k_window_probe(const uint64_t *xw, uint32_t nx, const uint64_t *yw, uint32_t ny, WinProbe pr,
+                               unsigned long long *total) {
+  const int c = blockIdx.y;
+  uint64_t acc = 0;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nx; x += gridDim.x * blockDim.x) {
+    uint32_t b, e;
+    y_range<DESC>(yw, ny, xw[x], pr.a[c], pr.z[c], b, e);
+    acc += e - b;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total + c, (unsigned long long)acc);
+}
+
+// The window's pairs of one side: weight sum (key) and pair id x * ny + y (payload), X-run x at xoff[x]
+// (one warp per X-run).
+template <bool DESC>
+__global__ void k_window_pairs(const uint64_t *xw, uint32_t nx, const uint64_t *yw, uint32_t ny, uint64_t lo,
+                               uint64_t hi, const uint64_t *xoff, uint64_t *key, uint64_t *val) {
+  const uint32_t lane = threadIdx.x & 31, nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t x = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); x < nx; x += nw) {
+    const uint64_t wx = xw[x];
+    uint32_t b, e;
+    y_range<DESC>(yw, ny, wx, lo, hi, b, e);
+    const uint64_t o = xoff[x];
+    for (uint32_t y = b + lane; y < e; y += 32) {
+      key[o + (y - b)] = wx + yw[y];
+      val[o + (y - b)] = (uint64_t)x * ny + y;
+    }
   }
 }
 
@@ -168,8 +251,8 @@ struct RectSparseSide {
 // Block (g, side): the batch side's rectangles X-run x Y-run, oriented for the warp tile (lanes_over_x:
 // the cheaper orientation) with their tile offsets -- the records k_rects writes for the dense plan.
 __global__ void k_rects_sparse(RectSparseSide L, RectSparseSide R, const uint64_t *hdr, const uint32_t *rbase,
-                               RectDesc *rects, unsigned long long *tiles, int *err) {
-  const uint32_t g = blockIdx.x;
+                               uint32_t g0, RectDesc *rects, unsigned long long *tiles, int *err) {
+  const uint32_t g = blockIdx.x;  // batch g0 + g of the plan
   const int side = blockIdx.y;
   const RectSparseSide &S = side ? R : L;
   const uint64_t *h = hdr + 7 * (size_t)g;
@@ -185,7 +268,7 @@ __global__ void k_rects_sparse(RectSparseSide L, RectSparseSide R, const uint64_
       const uint32_t x = (uint32_t)(p / S.ny), y = (uint32_t)(p - (uint64_t)x * S.ny);
       const uint32_t xs = S.xs[x], xl = S.xl[x], ys = S.ys[y], yl = S.yl[y];
       // one piece per run pair (the segment counts fixed the rectangle bases): the cheaper orientation
-      D = rect_piece(g * 2 + side, lanes_over_x(xl, yl), xs, xl, ys, yl);
+      D = rect_piece((g0 + g) * 2 + side, lanes_over_x(xl, yl), xs, xl, ys, yl);
       t = D.nl * D.nq;
     }
     uint32_t tot;
@@ -203,6 +286,151 @@ __global__ void k_rects_sparse(RectSparseSide L, RectSparseSide R, const uint64_
 }
 
 unsigned grid_for(uint64_t n) { return (unsigned)std::min<uint64_t>((n + 255) / 256, 4096); }
+
+// One alpha window [lo, hi): steps 2-5 on its pair sums (cnt[side] pairs per side), batches and
+// rectangles appended to `out` (batch index from Gtot, rectangle index from nrt).
+template <class CountF>
+int sparse_window(Work *W, const SparsePlanIn &in, const uint32_t nr[4], uint64_t lo, uint64_t hi,
+                  const uint64_t cnt[2], CountF &launch_count, cudaStream_t st, int64_t &launches,
+                  SparsePlanOut &out, uint64_t &nrt, uint32_t &Gtot, std::string &err) {
+  thrust::counting_iterator<uint32_t> ci(0);
+  size_t tb = 0;
+  const uint64_t t = in.target;
+  uint32_t nu[2];
+  // ---- 2./3. per side: the window's run-pair sums, sorted; distinct sums with their n and segment
+  for (int side = 0; side < 2; ++side) {
+    const int X = side ? 2 : 0, Y = side ? 3 : 1;
+    const uint64_t P = cnt[side];
+    if (P >= (1ull << 31)) {
+      char b[200];
+      snprintf(b, sizeof b, "sparse alpha plan: %llu run pairs of one alpha window side", (unsigned long long)P);
+      err = b;
+      return MSP_UNSUPPORTED_CODE;
+    }
+    PCK(W->k0.ensure(8 * P)); PCK(W->k1.ensure(8 * P)); PCK(W->v0.ensure(8 * P)); PCK(W->v1.ensure(8 * P));
+    PCK(W->pc.ensure(8 * P));
+    PCK(W->xcnt.ensure(8ull * nr[X] + 8)); PCK(W->xoff.ensure(8ull * nr[X] + 8));
+    launch_count(side, lo, hi, W->xcnt.as<uint64_t>(), nullptr);
+    tb = 0;
+    PCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, W->xcnt.as<uint64_t>(), W->xoff.as<uint64_t>(), (int)nr[X], st));
+    PCK(W->tmp.ensure(tb));
+    PCK(cub::DeviceScan::ExclusiveSum(W->tmp.p, tb, W->xcnt.as<uint64_t>(), W->xoff.as<uint64_t>(), (int)nr[X], st));
+    const uint64_t a = side ? t + 1 - hi : lo, z = side ? t + 1 - lo : hi;
+    const unsigned gp = (unsigned)std::min<uint64_t>((nr[X] + 7) / 8, 4096);
+    if (side)
+      k_window_pairs<true><<<gp, 256, 0, st>>>(W->rw[X].as<uint64_t>(), nr[X], W->rw[Y].as<uint64_t>(), nr[Y], a, z,
+                                               W->xoff.as<uint64_t>(), W->k0.as<uint64_t>(), W->v0.as<uint64_t>());
+    else
+      k_window_pairs<false><<<gp, 256, 0, st>>>(W->rw[X].as<uint64_t>(), nr[X], W->rw[Y].as<uint64_t>(), nr[Y], a, z,
+                                                W->xoff.as<uint64_t>(), W->k0.as<uint64_t>(), W->v0.as<uint64_t>());
+    cub::DoubleBuffer<uint64_t> dk(W->k0.as<uint64_t>(), W->k1.as<uint64_t>());
+    cub::DoubleBuffer<uint64_t> dv(W->v0.as<uint64_t>(), W->v1.as<uint64_t>());
+    tb = 0;
+    PCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)P, 0, 64, st));
+    PCK(W->tmp.ensure(tb));
+    PCK(cub::DeviceRadixSort::SortPairs(W->tmp.p, tb, dk, dv, (int)P, 0, 64, st));
+    const uint64_t *skey = dk.Current();
+    PCK(W->ids[side].ensure(8 * P));
+    PCK(cudaMemcpyAsync(W->ids[side].p, dv.Current(), 8 * P, cudaMemcpyDeviceToDevice, st));  // the rectangles
+    k_pair_counts<<<grid_for(P), 256, 0, st>>>(W->ids[side].as<uint64_t>(), P, W->rl[X].as<uint32_t>(),
+                                               W->rl[Y].as<uint32_t>(), nr[Y], W->pc.as<uint64_t>());
+    PCK(W->ukey[side].ensure(8 * P)); PCK(W->usum[side].ensure(8 * P)); PCK(W->ulen[side].ensure(4 * P));
+    PCK(W->uoff[side].ensure(4 * P)); PCK(W->nun[side].ensure(8)); PCK(W->ukey2.ensure(8 * P));
+    PCK(W->cnt1.ensure(8));
+    tb = 0;  // distinct sums with their total pair counts (n_left / n_right)
+    PCK(cub::DeviceReduce::ReduceByKey(nullptr, tb, skey, W->ukey[side].as<uint64_t>(), W->pc.as<uint64_t>(),
+                                       W->usum[side].as<uint64_t>(), W->nun[side].as<uint32_t>(), cub::Sum(), (int)P, st));
+    PCK(W->tmp.ensure(tb));
+    PCK(cub::DeviceReduce::ReduceByKey(W->tmp.p, tb, skey, W->ukey[side].as<uint64_t>(), W->pc.as<uint64_t>(),
+                                       W->usum[side].as<uint64_t>(), W->nun[side].as<uint32_t>(), cub::Sum(), (int)P, st));
+    tb = 0;  // ... and their pair segments (run lengths, exclusive scan)
+    PCK(cub::DeviceRunLengthEncode::Encode(nullptr, tb, skey, W->ukey2.as<uint64_t>(), W->ulen[side].as<uint32_t>(),
+                                           W->cnt1.as<uint32_t>(), (int)P, st));
+    PCK(W->tmp.ensure(tb));
+    PCK(cub::DeviceRunLengthEncode::Encode(W->tmp.p, tb, skey, W->ukey2.as<uint64_t>(), W->ulen[side].as<uint32_t>(),
+                                           W->cnt1.as<uint32_t>(), (int)P, st));
+    PCK(cudaMemcpyAsync(&nu[side], W->nun[side].p, 4, cudaMemcpyDeviceToHost, st));
+    PCK(cudaStreamSynchronize(st));
+    tb = 0;
+    PCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, W->ulen[side].as<uint32_t>(), W->uoff[side].as<uint32_t>(),
+                                      (int)nu[side], st));
+    PCK(W->tmp.ensure(tb));
+    PCK(cub::DeviceScan::ExclusiveSum(W->tmp.p, tb, W->ulen[side].as<uint32_t>(), W->uoff[side].as<uint32_t>(),
+                                      (int)nu[side], st));
+    launches += 4;
+  }
+  // ---- 4. batches: distinct alpha (ascending) of the window with t - alpha a right sum
+  PCK(W->bflag.ensure(nu[0] + 16));
+  PCK(W->ridx.ensure(4ull * nu[0] + 4));
+  PCK(W->sel.ensure(4ull * nu[0] + 4));
+  PCK(W->nb.ensure(8));
+  k_match<<<grid_for(nu[0]), 256, 0, st>>>(W->ukey[0].as<uint64_t>(), W->nun[0].as<uint32_t>(),
+                                            W->ukey[1].as<uint64_t>(), W->nun[1].as<uint32_t>(), t, lo, hi,
+                                            W->bflag.as<uint8_t>(), W->ridx.as<uint32_t>());
+  tb = 0;
+  PCK(cub::DeviceSelect::Flagged(nullptr, tb, ci, W->bflag.as<uint8_t>(), W->sel.as<uint32_t>(), W->nb.as<uint32_t>(),
+                                 (int)nu[0], st));
+  PCK(W->tmp.ensure(tb));
+  PCK(cub::DeviceSelect::Flagged(W->tmp.p, tb, ci, W->bflag.as<uint8_t>(), W->sel.as<uint32_t>(), W->nb.as<uint32_t>(),
+                                 (int)nu[0], st));
+  uint32_t G = 0;
+  PCK(cudaMemcpyAsync(&G, W->nb.p, 4, cudaMemcpyDeviceToHost, st));
+  PCK(cudaStreamSynchronize(st));
+  launches += 2;
+  if (!G) return 0;
+  if ((uint64_t)Gtot + G >= (1u << 30)) { err = "sparse alpha plan: more than 2^30 batches"; return MSP_UNSUPPORTED_CODE; }
+  PCK(W->hdr.ensure(8ull * 7 * G));
+  k_batch_headers<<<grid_for(G), 256, 0, st>>>(W->sel.as<uint32_t>(), W->nb.as<uint32_t>(), W->ridx.as<uint32_t>(),
+                                                W->ukey[0].as<uint64_t>(), W->usum[0].as<uint64_t>(),
+                                                W->uoff[0].as<uint32_t>(), W->ulen[0].as<uint32_t>(),
+                                                W->usum[1].as<uint64_t>(), W->uoff[1].as<uint32_t>(),
+                                                W->ulen[1].as<uint32_t>(), W->hdr.as<uint64_t>());
+  std::vector<uint64_t> h(7 * (size_t)G);
+  PCK(cudaMemcpyAsync(h.data(), W->hdr.p, 8ull * 7 * G, cudaMemcpyDeviceToHost, st));
+  PCK(cudaStreamSynchronize(st));
+  const size_t g0 = Gtot, nrt0 = nrt;
+  out.alpha.resize(g0 + G);
+  out.nl.resize(g0 + G);
+  out.nr.resize(g0 + G);
+  out.tiles.resize(2 * (g0 + G), 0);
+  out.rect_base.resize(2 * (g0 + G), 0);
+  out.nrect.resize(2 * (g0 + G), 0);
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint64_t *r = &h[7 * (size_t)g];
+    out.alpha[g0 + g] = r[0];
+    out.nl[g0 + g] = r[1];
+    out.nr[g0 + g] = r[2];
+    for (int side = 0; side < 2; ++side) {
+      out.rect_base[2 * (g0 + g) + side] = (uint32_t)nrt;
+      out.nrect[2 * (g0 + g) + side] = (uint32_t)r[side ? 6 : 4];
+      nrt += r[side ? 6 : 4];
+    }
+  }
+  if (nrt > 0xFFFFFFFFull) { err = "rectangle list too large"; return MSP_UNSUPPORTED_CODE; }
+  // ---- 5. the oriented rectangle lists of the window's batch sides, after the earlier windows' ones
+  PCK(W->rects.grow_keep(sizeof(RectDesc) * std::max<uint64_t>(nrt, 1), sizeof(RectDesc) * nrt0, st));
+  PCK(W->rbase.ensure(4ull * 2 * G));
+  PCK(cudaMemcpyAsync(W->rbase.p, out.rect_base.data() + 2 * g0, 4ull * 2 * G, cudaMemcpyHostToDevice, st));
+  PCK(W->tiles.ensure(8ull * 2 * G));
+  PCK(W->err.ensure(8));
+  PCK(cudaMemsetAsync(W->err.p, 0, 4, st));
+  RectSparseSide L{W->ids[0].as<uint64_t>(), W->rs[0].as<uint32_t>(), W->rl[0].as<uint32_t>(), W->rs[1].as<uint32_t>(),
+                   W->rl[1].as<uint32_t>(), nr[1]};
+  RectSparseSide R{W->ids[1].as<uint64_t>(), W->rs[2].as<uint32_t>(), W->rl[2].as<uint32_t>(), W->rs[3].as<uint32_t>(),
+                   W->rl[3].as<uint32_t>(), nr[3]};
+  k_rects_sparse<<<dim3(G, 2), 256, 0, st>>>(L, R, W->hdr.as<uint64_t>(), W->rbase.as<uint32_t>(), (uint32_t)g0,
+                                              W->rects.as<RectDesc>(), W->tiles.as<unsigned long long>(), W->err.as<int>());
+  launches += 2;
+  int rerr = 0;
+  static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "tiles");
+  PCK(cudaMemcpyAsync(out.tiles.data() + 2 * g0, W->tiles.p, 8ull * 2 * G, cudaMemcpyDeviceToHost, st));
+  PCK(cudaMemcpyAsync(&rerr, W->err.p, 4, cudaMemcpyDeviceToHost, st));
+  PCK(cudaStreamSynchronize(st));
+  PCK(cudaGetLastError());
+  if (rerr) { err = "tile count of one batch side exceeds 2^32"; return MSP_UNSUPPORTED_CODE; }
+  Gtot += G;
+  return 0;
+}
 
 }  // namespace
 
@@ -241,123 +469,93 @@ int sparse_plan(int device, const SparsePlanIn &in, SparsePlanOut &out, cudaStre
     PCK(cudaMemcpyAsync(&nr[t], W->cnt1.p, 4, cudaMemcpyDeviceToHost, st));
     PCK(cudaStreamSynchronize(st));
   }
-  // ---- 2./3. per side: every run pair's weight sum, sorted; distinct sums with their n and segment
-  uint32_t nu[2];
-  for (int side = 0; side < 2; ++side) {
+  // ---- the alpha windows: [lo, hi) within the band and alpha <= t, at most `budget` run pairs per side
+  const uint64_t t = in.target;
+  if (t == ~0ull) { err = "sparse alpha plan: target 2^64 - 1"; return MSP_UNSUPPORTED_CODE; }
+  const uint64_t A0 = in.alpha_lo, A1 = std::min<uint64_t>(in.alpha_hi, t + 1);
+  uint64_t budget = 1ull << 27;
+  if (const char *e = getenv("MSP_SPARSE_WINDOW_PAIRS")) {
+    const unsigned long long v = strtoull(e, nullptr, 0);
+    if (v) budget = v;
+  }
+  PCK(W->wtot.ensure(16));
+  // side 0: left sums in [lo, hi); side 1: right sums in [t + 1 - hi, t + 1 - lo)
+  auto sums_lo = [&](int side, uint64_t lo, uint64_t hi) { return side ? t + 1 - hi : lo; };
+  auto sums_hi = [&](int side, uint64_t lo, uint64_t hi) { return side ? t + 1 - lo : hi; };
+  auto launch_count = [&](int side, uint64_t lo, uint64_t hi, uint64_t *xcnt, unsigned long long *tot) {
     const int X = side ? 2 : 0, Y = side ? 3 : 1;
-    const uint64_t P = (uint64_t)nr[X] * nr[Y];
-    if (P > (1ull << 27)) {
-      char b[200];
-      snprintf(b, sizeof b, "sparse alpha plan: %llu run pairs on one side exceed 2^27", (unsigned long long)P);
-      err = b;
-      return MSP_UNSUPPORTED_CODE;
-    }
-    PCK(W->k0.ensure(8 * P)); PCK(W->k1.ensure(8 * P)); PCK(W->v0.ensure(8 * P)); PCK(W->v1.ensure(8 * P));
-    PCK(W->pc.ensure(8 * P));
-    k_pair_sums<<<grid_for(P), 256, 0, st>>>(W->rw[X].as<uint64_t>(), nr[X], W->rw[Y].as<uint64_t>(), nr[Y],
-                                             W->k0.as<uint64_t>(), W->v0.as<uint64_t>());
-    cub::DoubleBuffer<uint64_t> dk(W->k0.as<uint64_t>(), W->k1.as<uint64_t>());
-    cub::DoubleBuffer<uint64_t> dv(W->v0.as<uint64_t>(), W->v1.as<uint64_t>());
-    tb = 0;
-    PCK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)P, 0, 64, st));
-    PCK(W->tmp.ensure(tb));
-    PCK(cub::DeviceRadixSort::SortPairs(W->tmp.p, tb, dk, dv, (int)P, 0, 64, st));
-    const uint64_t *skey = dk.Current();
-    PCK(W->ids[side].ensure(8 * P));
-    PCK(cudaMemcpyAsync(W->ids[side].p, dv.Current(), 8 * P, cudaMemcpyDeviceToDevice, st));  // the rectangles
-    k_pair_counts<<<grid_for(P), 256, 0, st>>>(W->ids[side].as<uint64_t>(), P, W->rl[X].as<uint32_t>(),
-                                               W->rl[Y].as<uint32_t>(), nr[Y], W->pc.as<uint64_t>());
-    PCK(W->ukey[side].ensure(8 * P)); PCK(W->usum[side].ensure(8 * P)); PCK(W->ulen[side].ensure(4 * P));
-    PCK(W->uoff[side].ensure(4 * P)); PCK(W->nun[side].ensure(8)); PCK(W->ukey2.ensure(8 * P));
-    tb = 0;  // distinct sums with their total pair counts (n_left / n_right)
-    PCK(cub::DeviceReduce::ReduceByKey(nullptr, tb, skey, W->ukey[side].as<uint64_t>(), W->pc.as<uint64_t>(),
-                                       W->usum[side].as<uint64_t>(), W->nun[side].as<uint32_t>(), cub::Sum(), (int)P, st));
-    PCK(W->tmp.ensure(tb));
-    PCK(cub::DeviceReduce::ReduceByKey(W->tmp.p, tb, skey, W->ukey[side].as<uint64_t>(), W->pc.as<uint64_t>(),
-                                       W->usum[side].as<uint64_t>(), W->nun[side].as<uint32_t>(), cub::Sum(), (int)P, st));
-    tb = 0;  // ... and their pair segments (run lengths, exclusive scan)
-    PCK(cub::DeviceRunLengthEncode::Encode(nullptr, tb, skey, W->ukey2.as<uint64_t>(), W->ulen[side].as<uint32_t>(),
-                                           W->cnt1.as<uint32_t>(), (int)P, st));
-    PCK(W->tmp.ensure(tb));
-    PCK(cub::DeviceRunLengthEncode::Encode(W->tmp.p, tb, skey, W->ukey2.as<uint64_t>(), W->ulen[side].as<uint32_t>(),
-                                           W->cnt1.as<uint32_t>(), (int)P, st));
-    PCK(cudaMemcpyAsync(&nu[side], W->nun[side].p, 4, cudaMemcpyDeviceToHost, st));
-    PCK(cudaStreamSynchronize(st));
-    tb = 0;
-    PCK(cub::DeviceScan::ExclusiveSum(nullptr, tb, W->ulen[side].as<uint32_t>(), W->uoff[side].as<uint32_t>(),
-                                      (int)nu[side], st));
-    PCK(W->tmp.ensure(tb));
-    PCK(cub::DeviceScan::ExclusiveSum(W->tmp.p, tb, W->ulen[side].as<uint32_t>(), W->uoff[side].as<uint32_t>(),
-                                      (int)nu[side], st));
-    launches += 2;
-  }
-  // ---- 4. batches: distinct alpha (ascending) in the band with t - alpha a right sum
-  PCK(W->bflag.ensure(nu[0] + 16));
-  PCK(W->ridx.ensure(4ull * nu[0] + 4));
-  PCK(W->sel.ensure(4ull * nu[0] + 4));
-  PCK(W->nb.ensure(8));
-  k_match<<<grid_for(nu[0]), 256, 0, st>>>(W->ukey[0].as<uint64_t>(), W->nun[0].as<uint32_t>(),
-                                            W->ukey[1].as<uint64_t>(), W->nun[1].as<uint32_t>(), in.target,
-                                            in.alpha_lo, in.alpha_hi, W->bflag.as<uint8_t>(), W->ridx.as<uint32_t>());
-  tb = 0;
-  PCK(cub::DeviceSelect::Flagged(nullptr, tb, ci, W->bflag.as<uint8_t>(), W->sel.as<uint32_t>(), W->nb.as<uint32_t>(),
-                                 (int)nu[0], st));
-  PCK(W->tmp.ensure(tb));
-  PCK(cub::DeviceSelect::Flagged(W->tmp.p, tb, ci, W->bflag.as<uint8_t>(), W->sel.as<uint32_t>(), W->nb.as<uint32_t>(),
-                                 (int)nu[0], st));
-  uint32_t G = 0;
-  PCK(cudaMemcpyAsync(&G, W->nb.p, 4, cudaMemcpyDeviceToHost, st));
-  PCK(cudaStreamSynchronize(st));
-  launches += 2;
-  out.alpha.resize(G);
-  out.nl.resize(G);
-  out.nr.resize(G);
-  out.tiles.assign(2 * (size_t)G, 0);
-  out.rect_base.assign(2 * (size_t)G, 0);
-  out.nrect.assign(2 * (size_t)G, 0);
-  if (!G) return 0;
-  PCK(W->hdr.ensure(8ull * 7 * G));
-  k_batch_headers<<<grid_for(G), 256, 0, st>>>(W->sel.as<uint32_t>(), W->nb.as<uint32_t>(), W->ridx.as<uint32_t>(),
-                                                W->ukey[0].as<uint64_t>(), W->usum[0].as<uint64_t>(),
-                                                W->uoff[0].as<uint32_t>(), W->ulen[0].as<uint32_t>(),
-                                                W->usum[1].as<uint64_t>(), W->uoff[1].as<uint32_t>(),
-                                                W->ulen[1].as<uint32_t>(), W->hdr.as<uint64_t>());
-  std::vector<uint64_t> h(7 * (size_t)G);
-  PCK(cudaMemcpyAsync(h.data(), W->hdr.p, 8ull * 7 * G, cudaMemcpyDeviceToHost, st));
-  PCK(cudaStreamSynchronize(st));
-  uint64_t nrt = 0;
-  for (uint32_t g = 0; g < G; ++g) {
-    const uint64_t *r = &h[7 * (size_t)g];
-    out.alpha[g] = r[0];
-    out.nl[g] = r[1];
-    out.nr[g] = r[2];
+    const uint64_t a = sums_lo(side, lo, hi), z = sums_hi(side, lo, hi);
+    if (side)
+      k_window_count<true><<<grid_for(nr[X]), 256, 0, st>>>(W->rw[X].as<uint64_t>(), nr[X], W->rw[Y].as<uint64_t>(),
+                                                             nr[Y], a, z, xcnt, tot);
+    else
+      k_window_count<false><<<grid_for(nr[X]), 256, 0, st>>>(W->rw[X].as<uint64_t>(), nr[X], W->rw[Y].as<uint64_t>(),
+                                                              nr[Y], a, z, xcnt, tot);
+    ++launches;
+  };
+  // pair totals of both sides for the windows [lo, his[c]), c < nc (kProbe candidates per launch)
+  PCK(W->wtot.ensure(16 * kProbe));
+  uint64_t pc[2][kProbe];
+  auto probe = [&](uint64_t lo, const uint64_t *his, int nc) -> cudaError_t {
+    cudaError_t e = cudaMemsetAsync(W->wtot.p, 0, 16 * kProbe, st);
+    if (e != cudaSuccess) return e;
     for (int side = 0; side < 2; ++side) {
-      out.rect_base[2 * (size_t)g + side] = (uint32_t)nrt;
-      out.nrect[2 * (size_t)g + side] = (uint32_t)r[side ? 6 : 4];
-      nrt += r[side ? 6 : 4];
+      const int X = side ? 2 : 0, Y = side ? 3 : 1;
+      WinProbe pr{};
+      for (int c = 0; c < nc; ++c) { pr.a[c] = sums_lo(side, lo, his[c]); pr.z[c] = sums_hi(side, lo, his[c]); }
+      const dim3 grid((unsigned)std::min<uint64_t>((nr[X] + 255) / 256, 256), nc);
+      unsigned long long *tot = W->wtot.as<unsigned long long>() + side * kProbe;
+      if (side)
+        k_window_probe<true><<<grid, 256, 0, st>>>(W->rw[X].as<uint64_t>(), nr[X], W->rw[Y].as<uint64_t>(), nr[Y], pr, tot);
+      else
+        k_window_probe<false><<<grid, 256, 0, st>>>(W->rw[X].as<uint64_t>(), nr[X], W->rw[Y].as<uint64_t>(), nr[Y], pr, tot);
+      ++launches;
     }
+    e = cudaMemcpyAsync(pc, W->wtot.p, 16 * kProbe, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e;
+  };
+  uint64_t nrt = 0;  // rectangles written so far (the rect_base of the next batch side)
+  uint32_t Gtot = 0;
+  for (uint64_t lo = A0; lo < A1;) {
+    uint64_t hi = A1, cnt[2];
+    PCK(probe(lo, &hi, 1));
+    cnt[0] = pc[0][0]; cnt[1] = pc[1][0];
+    if (cnt[0] > budget || cnt[1] > budget) {
+      // the largest hi with both sides within budget (at least one alpha: lo + 1); the counts are
+      // monotone in hi, so a kProbe-ary search: `good` fits (or is lo + 1), `bad` does not
+      uint64_t good = lo + 1, bad = A1;
+      PCK(probe(lo, &good, 1));
+      cnt[0] = pc[0][0]; cnt[1] = pc[1][0];
+      while (bad - good > 1) {
+        uint64_t his[kProbe];
+        const uint64_t span = bad - good;
+        int nc = 0;
+        for (int c = 1; c <= kProbe; ++c) {
+          const uint64_t h = good + (uint64_t)((unsigned __int128)span * c / (kProbe + 1));
+          if (h > good && h < bad && (nc == 0 || h > his[nc - 1])) his[nc++] = h;
+        }
+        if (!nc) break;
+        PCK(probe(lo, his, nc));
+        for (int c = 0; c < nc; ++c) {
+          if (pc[0][c] <= budget && pc[1][c] <= budget) {
+            good = his[c];
+            cnt[0] = pc[0][c]; cnt[1] = pc[1][c];
+          } else {
+            bad = his[c];
+            break;
+          }
+        }
+      }
+      hi = good;
+    }
+    if (cnt[0] && cnt[1]) {
+      const int rc = sparse_window(W, in, nr, lo, hi, cnt, launch_count, st, launches, out, nrt, Gtot, err);
+      if (rc) return rc;
+    }
+    lo = hi;
   }
-  if (nrt > 0xFFFFFFFFull) { err = "rectangle list too large"; return MSP_UNSUPPORTED_CODE; }
-  // ---- 5. the oriented rectangle lists of every batch side
-  PCK(W->rects.ensure(sizeof(RectDesc) * std::max<uint64_t>(nrt, 1)));
-  PCK(W->rbase.ensure(4ull * 2 * G));
-  PCK(cudaMemcpyAsync(W->rbase.p, out.rect_base.data(), 4ull * 2 * G, cudaMemcpyHostToDevice, st));
-  PCK(W->tiles.ensure(8ull * 2 * G));
-  PCK(W->err.ensure(8));
-  PCK(cudaMemsetAsync(W->err.p, 0, 4, st));
-  RectSparseSide L{W->ids[0].as<uint64_t>(), W->rs[0].as<uint32_t>(), W->rl[0].as<uint32_t>(), W->rs[1].as<uint32_t>(),
-                   W->rl[1].as<uint32_t>(), nr[1]};
-  RectSparseSide R{W->ids[1].as<uint64_t>(), W->rs[2].as<uint32_t>(), W->rl[2].as<uint32_t>(), W->rs[3].as<uint32_t>(),
-                   W->rl[3].as<uint32_t>(), nr[3]};
-  k_rects_sparse<<<dim3(G, 2), 256, 0, st>>>(L, R, W->hdr.as<uint64_t>(), W->rbase.as<uint32_t>(),
-                                              W->rects.as<RectDesc>(), W->tiles.as<unsigned long long>(), W->err.as<int>());
-  launches += 2;
-  int rerr = 0;
-  PCK(cudaMemcpyAsync(out.tiles.data(), W->tiles.p, 8ull * 2 * G, cudaMemcpyDeviceToHost, st));
-  PCK(cudaMemcpyAsync(&rerr, W->err.p, 4, cudaMemcpyDeviceToHost, st));
-  PCK(cudaStreamSynchronize(st));
   PCK(cudaGetLastError());
-  if (rerr) { err = "tile count of one batch side exceeds 2^32"; return MSP_UNSUPPORTED_CODE; }
   out.rects = W->rects.as<RectDesc>();
   return 0;
 }

@@ -557,6 +557,40 @@ def test_sparse_plan_matches_dense_plan(monkeypatch):
             assert st1[k] == st0[k], (m, s, k)
 
 
+def test_sparse_plan_alpha_windows(monkeypatch):
+    """The sparse plan streamed through alpha windows (MSP_SPARSE_WINDOW_PAIRS run pairs per window
+    side: 1 forces single-alpha windows past the budget, 37 .. 65536 cut the range into many windows)
+    reproduces the one-window plan: batch headers, per-batch counters, solutions, counters -- on K = 100
+    instances and the generic-weight (K = 10^6) goldens, and inside an alpha band."""
+    cases = [(msb.generate_instance(5, 100, 3), ("1", "37", "4096")),
+             (msb.generate_instance(6, 100, 4), ("37", "4096")), (msb.generate_instance(7, 100, 1), ("4096",))]
+    cases += [(inst_from(r["instance"]), ("4096", "65536")) for r in load_golden("solves_generic.json")
+              if r["reduce_rows"] == 1][:4]
+    monkeypatch.setenv("MSP_SPARSE_PLAN", "1")
+    for inst, budgets in cases:
+        opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_BATCH_STATS)
+        monkeypatch.delenv("MSP_SPARSE_WINDOW_PAIRS", raising=False)
+        rc0, xb0, st0 = _native.solve_raw(inst.a, inst.d, opts)
+        plan0 = _native.alpha_plan(inst.a, inst.d)
+        assert rc0 == 0, _native.last_error()
+        alphas = [b[0] for b in st0["batch_stats"]]
+        lo, hi = (alphas[len(alphas) // 3], alphas[2 * len(alphas) // 3]) if len(alphas) > 2 else (0, 0)
+        band = _native.make_options(mode="all", flags=_native.MSP_FLAG_BATCH_STATS, alpha_lo=lo, alpha_hi=hi)
+        for w in budgets:
+            monkeypatch.setenv("MSP_SPARSE_WINDOW_PAIRS", w)
+            rc1, xb1, st1 = _native.solve_raw(inst.a, inst.d, opts)
+            assert rc1 == 0, _native.last_error()
+            assert _native.alpha_plan(inst.a, inst.d) == plan0, w
+            assert st1["batch_stats"] == st0["batch_stats"], w
+            assert sorted(map(tuple, xb1.tolist())) == sorted(map(tuple, xb0.tolist()))
+            for k in STAT_KEYS:
+                assert st1[k] == st0[k], (w, k)
+            if hi:
+                rc2, _, st2 = _native.solve_raw(inst.a, inst.d, band)
+                assert rc2 == 0, _native.last_error()
+                assert st2["batch_stats"] == [b for b in st0["batch_stats"] if lo <= b[0] < hi], w
+
+
 def test_time_limit_stops_the_running_kernels():
     """The deadline reaches the running kernels (host-mapped stop word polled at every task switch of
     the persistent pipeline): a (9,80) full enumeration (~40 s) with a 1 s limit raises SolveTimeout
