@@ -228,7 +228,7 @@ struct WavesArgs {
   const WaveDesc *waves;
   const RescatterSrc *srcs;            // level-2 sources (kind 1 waves)
   const unsigned long long *chunks;    // scatter chunks of all waves
-  const unsigned long long *tasks;     // join << 63 | wave << 32 | chunk or first bucket
+  const unsigned long long *tasks;     // join << 63 | wave << 32 | first bucket, or wave << 32 | chunk (index into chunks)
   uint32_t ntasks;
   unsigned int *task_ctr, *scat_done, *join_done;  // zeroed before the launch
   int *abort_dev;                      // stop word (deadline / cross-rank cancel): zeroed per solve, set

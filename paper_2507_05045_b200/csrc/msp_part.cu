@@ -487,9 +487,14 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
 // spread uniformly over its NF fine buckets), re-partitioned by the CTA.  Fine bucket = floor(frac *
 // NF / 2^32), frac = the key's position inside its coarse bucket (the low word of hi * NC).  The
 // keys arrive by TMA bulk copies in steps of kRStep keys through two shared buffers behind the
-// stage (the next step always in flight), so the pass is bound by the staging, not by HBM latency.
+// stage (the next step always in flight), each step prefetched into L2 kRPrefetch steps earlier
+// (cp.async.bulk.prefetch.L2), so a step copy waits on L2, not on HBM.
 // Ends with a barrier.
 constexpr uint32_t kRStep = 2048;                 // keys per step (two 16 KB buffers)
+#ifndef MSP_RPREFETCH
+#define MSP_RPREFETCH 8
+#endif
+constexpr uint32_t kRPrefetch = MSP_RPREFETCH;    // steps prefetched into L2 (TMA prefetch) ahead of the step copies
 constexpr int kRPerThread = (kRStep + kScatterThreads - 1) / kScatterThreads;
 size_t rescatter_smem_bytes() { return sizeof(Stage) + 2ull * kRStep * 8; }
 
@@ -502,7 +507,13 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
   unsigned long long *buf = reinterpret_cast<unsigned long long *>(&g + 1);  // 2 x kRStep keys
   __shared__ unsigned long long s_rbar[2];
   const uint32_t nstep = s1 > s0 ? (s1 - s0 + kRStep - 1) / kRStep : 0;
+  auto prefetch = [&](uint32_t c) {  // thread 0: step c into L2 (TMA prefetch, no shared memory)
+    if (kRPrefetch == 0 || c >= nstep) return;
+    const uint32_t a = s0 + c * kRStep, n = min(s1 - a, kRStep);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src.keys + a), "r"(8u * ((n + 1u) & ~1u)) : "memory");
+  };
   auto issue = [&](uint32_t c) {  // thread 0: step c into buffer c & 1
+    prefetch(c + kRPrefetch);
     const uint32_t a = s0 + c * kRStep, n = min(s1 - a, kRStep);
     fence_proxy_async_smem();
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
@@ -514,6 +525,7 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
   if (tid == 0) {
     for (int k = 0; k < 2; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[k])) : "memory");
+    for (uint32_t c = 2; c < kRPrefetch; ++c) prefetch(c);
     for (uint32_t c = 0; c < 2 && c < nstep; ++c) issue(c);
   }
   __syncthreads();
@@ -868,41 +880,43 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
   for (int k = 0; k < NW; ++k) dg[k] = W.sc.dpack[k];
   unsigned long long dacc = 0;
   long long t_prev = clock64();
-  // Thread 0 keeps the NEXT task in flight while the CTA works: its index (atomic), word, wave
-  // descriptor, chunk word and dependency target are loaded a whole task ahead; at the switch it
-  // waits for the dependency (acquire load) and hands everything over through shared memory.
+  // Thread 0 fetches the NEXT task at each switch: queue index (atomic), task word, then its wave
+  // descriptor, chunk word (the task word holds the chunk's global index, so both load in parallel),
+  // dependency target and the stop word, handed over through shared memory at the following switch.
+  // (Deeper lookahead -- tasks reserved two or three ahead, every load off the switch's critical
+  // path -- measured slower: reserved-but-unstarted scatter chunks delay the joins that wait on them.)
   struct Next { unsigned long long tk, cw; WaveDesc wd; uint32_t need; const unsigned int *ctr; int stop; };
   __shared__ unsigned long long s_cw;
   __shared__ WaveDesc s_wd;
-  auto fetch = [&](Next &x) {
+  auto task_word = [&](uint32_t i) -> unsigned long long { return i < W.ntasks ? W.tasks[i] : ~0ull; };
+  auto fetch = [&](unsigned long long tk, Next &x) {
     // the stop word (device memory, set by the host watchdog's copy): read a task ahead, so its
     // latency overlaps the current task
     asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(x.stop) : "l"(W.abort_dev));
-    const uint32_t i = atomicAdd(W.task_ctr, 1u);
-    x.tk = i < W.ntasks ? W.tasks[i] : ~0ull;
+    x.tk = tk;
     x.ctr = nullptr;
     x.need = 0;
     x.cw = 0;
-    if (x.tk == ~0ull) return;
-    const uint32_t w = (uint32_t)(x.tk >> 32) & 0x7FFFFFFFu;
+    if (tk == ~0ull) return;
+    const uint32_t w = (uint32_t)(tk >> 32) & 0x7FFFFFFFu;
     x.wd = W.waves[w];
-    if (x.tk >> 63) {
+    if (tk >> 63) {
       x.ctr = W.scat_done + w;
-      x.need = x.wd.nchunks;
+      x.need = W.waves[w].nchunks;
     } else {
-      x.cw = __ldg(W.chunks + x.wd.chunk0 + (uint32_t)x.tk);
+      x.cw = __ldg(W.chunks + (uint32_t)tk);
       if (w >= kWaveBuffers) {  // the last wave on this scratch buffer must be fully joined
         x.ctr = W.join_done + w - kWaveBuffers;
         x.need = W.waves[w - kWaveBuffers].njoin;
       }
     }
   };
-  Next nx;
-  if (tid == 0) fetch(nx);
+  Next nc;
+  if (tid == 0) fetch(task_word(atomicAdd(W.task_ctr, 1u)), nc);
   while (true) {
     if (tid == 0) {
-      const Next cur = nx;
-      if (cur.tk != ~0ull) fetch(nx);
+      const Next cur = nc;
+      if (cur.tk != ~0ull) fetch(task_word(atomicAdd(W.task_ctr, 1u)), nc);
       // stop (deadline / cancel, MSP_OPTIONS): every CTA leaves at its next task switch, waits included
       bool stop = cur.stop != 0;
       if (cur.ctr && !stop) {
@@ -914,7 +928,7 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
           if (*(volatile int *)W.abort_dev) { stop = true; break; }
           __nanosleep(256);
         }
-        if (W.pa.dbg) atomicAdd(W.pa.dbg + 6, (unsigned long long)(clock64() - tw));
+        if (W.pa.dbg) atomicAdd(W.pa.dbg + ((cur.tk >> 63) ? 6 : 7), (unsigned long long)(clock64() - tw));
       }
       s_task = stop ? ~0ull : cur.tk;
       s_cw = cur.cw;

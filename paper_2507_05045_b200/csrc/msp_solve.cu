@@ -627,6 +627,11 @@ constexpr int kRetryHits = 100;
 #endif
 constexpr uint64_t kTaskTiles = MSP_TASK_TILES;
 constexpr uint64_t kTaskTilesMin = 96;
+#ifndef MSP_L2_CHUNK
+#define MSP_L2_CHUNK 65536
+#endif
+constexpr uint64_t kL2ChunkSlots = MSP_L2_CHUNK;  // slots of a coarse region per level-2 task (multiple of 32)
+static_assert(kL2ChunkSlots % 32 == 0 && kL2ChunkSlots / 32 <= 0xFFFF, "level-2 chunk word");
 #ifndef MSP_TASKS_PER_SM
 #define MSP_TASKS_PER_SM 1
 #endif
@@ -1027,7 +1032,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks.push_back((1ull << 63) | ((unsigned long long)w << 32) | b);
       };
       for (size_t w = s0; w < s1; ++w) {
-        for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks.push_back(((unsigned long long)w << 32) | c);
+        for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks.push_back(((unsigned long long)w << 32) | (wds[w].chunk0 + c));
         if (w >= s0 + kWaveLookahead) push_join(w - kWaveLookahead);
       }
       for (size_t w = s1 > s0 + kWaveLookahead ? s1 - kWaveLookahead : s0; w < s1; ++w) push_join(w);
@@ -1400,6 +1405,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       c1.zero_keys = D.zkeys.as<unsigned long long>();
       c1.dbg = dbg_stats ? dbg_stats + 16 : nullptr;
       if (profile) CK(cudaEventRecord(D.pev[0], st));
+      mark("huge: level 1");
       CK(D.tdesc.ensure(sizeof(TileDesc) * std::max<uint64_t>(1, std::max(ltiles[0], ltiles[1]))));
       for (int role = 0; role < 2; ++role) {
         const int side = role == 0 ? bside : 1 - bside;
@@ -1426,11 +1432,12 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         S.kernel_launches += 2;
       }
       // level 2 waves over the coarse buckets
+      mark("huge: level 2 setup");
       const uint32_t NF = (uint32_t)std::max<uint64_t>(1, (uint64_t)std::ceil(mb / kBucketTargetMax));
       if (NF > (uint32_t)kMaxUnitBuckets) { set_err("coarse bucket too large for one level-2 wave"); return MSP_UNSUPPORTED; }
       const double fmb = mb / NF, fmp = mp / NF;
-      // level-2 sources: one coarse region per role, read in 16K-slot chunks
-      const uint32_t fcb = region_cap(fmb, (double)cb, (double)cb / 16384 + 2), fcp = region_cap(fmp, (double)cp, (double)cp / 16384 + 2);
+      // level-2 sources: one coarse region per role, read in kL2ChunkSlots-slot chunks
+      const uint32_t fcb = region_cap(fmb, (double)cb, (double)cb / kL2ChunkSlots + 2), fcp = region_cap(fmp, (double)cp, (double)cp / kL2ChunkSlots + 2);
       struct L2Wave { size_t s0, ns, b0, nb; uint64_t total, scratch; };
       std::vector<L2Wave> lw;
       std::vector<RescatterSrc> srcs;
@@ -1487,14 +1494,14 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
-      std::vector<unsigned long long> l2ch;  // per wave: 16K-slot chunks of each source region
+      std::vector<unsigned long long> l2ch;  // per wave: kL2ChunkSlots-slot chunks of each source region
       std::vector<size_t> l2off;
       for (const L2Wave &w : lw) {
         l2off.push_back(l2ch.size());
         for (size_t si = 0; si < w.ns; ++si) {
           const uint64_t cap = srcs[w.s0 + si].cap;
-          for (uint64_t o = 0; o < cap; o += 16384) {
-            const uint64_t grp = std::min<uint64_t>(512, (cap - o + 31) / 32);
+          for (uint64_t o = 0; o < cap; o += kL2ChunkSlots) {
+            const uint64_t grp = std::min<uint64_t>(kL2ChunkSlots / 32, (cap - o + 31) / 32);
             l2ch.push_back(o | (grp << 32) | ((unsigned long long)si << 48));
           }
         }
@@ -1787,17 +1794,17 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     CK(cudaMemcpy(dva, dbg_stats, 3 * 128, cudaMemcpyDeviceToHost));
     for (int blk = 1; blk < 3; ++blk)
       fprintf(stderr, "[msp dbg] %s: rounds %llu staged %llu overflow %llu spilled %llu capacity-overflow %llu; "
-              "SM-ms (pipeline) scatter %.1f join %.1f wait %.1f, join phases %.1f / %.1f\n",
+              "SM-ms (pipeline) scatter %.1f join %.1f wait %.1f + %.1f, join phases %.1f / %.1f\n",
               blk == 1 ? "level-1 scatter" : "level-2", dva[16 * blk], dva[16 * blk + 1], dva[16 * blk + 2],
               dva[16 * blk + 13], dva[16 * blk + 12], dva[16 * blk + 4] / 1.965e6, dva[16 * blk + 5] / 1.965e6,
-              dva[16 * blk + 6] / 1.965e6, dva[16 * blk + 8] / 1.965e6, dva[16 * blk + 9] / 1.965e6);
+              dva[16 * blk + 6] / 1.965e6, dva[16 * blk + 7] / 1.965e6, dva[16 * blk + 8] / 1.965e6, dva[16 * blk + 9] / 1.965e6);
     unsigned long long *dv = dva;
     int nov = 0;
     for (uint32_t g = 0; g < P.G; ++g) nov += dropped[g];
     fprintf(stderr, "[msp dbg] scatter rounds %llu staged %llu overflow %llu; keys/round %.0f; overflowed batches %d of %u; "
-            "SM-ms scatter %.1f join %.1f (incl. wait %.1f)\n",
+            "SM-ms scatter %.1f join %.1f (incl. waits: joins for their scatters %.1f, scatters for their buffer %.1f)\n",
             dv[0], dv[1], dv[2], dv[0] ? (double)dv[1] / dv[0] : 0.0, nov, P.G, dv[4] / 1.965e6, dv[5] / 1.965e6,
-            dv[6] / 1.965e6);
+            dv[6] / 1.965e6, dv[7] / 1.965e6);
     fprintf(stderr, "[msp dbg] join buckets %llu: build phase %.1f SM-ms, probe phase %.1f SM-ms, mean stash %.2f\n",
             dv[11], dv[8] / 1.965e6, dv[9] / 1.965e6, dv[11] ? (double)dv[10] / dv[11] : 0.0);
     fprintf(stderr, "[msp dbg] overflow events: region capacity %llu, spilled keys %llu, join stash %llu\n",
