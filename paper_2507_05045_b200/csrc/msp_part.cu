@@ -46,6 +46,14 @@ constexpr int kMaxNB = kMaxUnitBuckets;                         // entries of on
 #ifndef MSP_STAGE_FILL_PCT
 #define MSP_STAGE_FILL_PCT 75
 #endif
+// (the huge-batch passes stage over ~500 coarse / fine entries, where a fuller stage spills more
+// keys past C; each spill is a global atomic the warp -- and the next barrier -- waits on)
+#ifndef MSP_L1STAGE_FILL_PCT
+#define MSP_L1STAGE_FILL_PCT 62
+#endif
+#ifndef MSP_RSTAGE_FILL_PCT
+#define MSP_RSTAGE_FILL_PCT 62
+#endif
 #ifndef MSP_RESCATTER_N
 #define MSP_RESCATTER_N 4
 #endif
@@ -205,9 +213,10 @@ __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_
 }
 
 // Stage slots per entry of a unit with NB buckets, and each lane's share of a round.
-__device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_t &budget) {
+__device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_t &budget,
+                                               uint32_t fill_pct = MSP_STAGE_FILL_PCT) {
   C = (kStageKeys / NB) & ~1u;  // even: every entry's run starts 16-byte aligned
-  budget = max(1u, NB * C * MSP_STAGE_FILL_PCT / (100u * kScatterThreads));
+  budget = max(1u, NB * C * fill_pct / (100u * kScatterThreads));
 }
 
 // ---------------------------------------------------------------- tile descriptors
@@ -377,14 +386,15 @@ __device__ __forceinline__ void hash_step(Stage &g, const PartArgs &S, const uin
 template <int MC>
 __device__ __forceinline__ void scatter_chunk(Stage &g, uint32_t *ybuf, const ScatterArgs &A, const PartArgs &S,
                                               const uint32_t (&dg)[words_for(MC) > 0 ? words_for(MC) : 1],
-                                              const UnitInfo ui, uint32_t t0, uint32_t n, unsigned long long &dacc) {
+                                              const UnitInfo ui, uint32_t t0, uint32_t n, unsigned long long &dacc,
+                                              uint32_t fill_pct = MSP_STAGE_FILL_PCT) {
   constexpr int SW = stride_for(MC);
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   volatile uint32_t *round_end = &g.round_end;
   const uint32_t ebase = ui.ent & 0x1FFFu, nbk = (ui.ent >> 13) & 0x7FFu, side = (ui.ent >> 24) & 1u;
   const bool right = side != 0;
   uint32_t C, budget, staged = 0;
-  stage_geometry(nbk, C, budget);
+  stage_geometry(nbk, C, budget, fill_pct);
   if (tid == 0) g.tctr = 0;
   __syncthreads();
   auto grab = [&]() {
@@ -476,7 +486,7 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
     }
     const unsigned long long cw = __ldg(A.chunks + c);
     const uint32_t t0 = (uint32_t)cw, n = t0 + (uint32_t)((cw >> 32) & 0xFFFFu), unit = (uint32_t)(cw >> 48);
-    scatter_chunk<MC>(g, ybuf, A, S, dg, A.units[unit], t0, n, dacc);
+    scatter_chunk<MC>(g, ybuf, A, S, dg, A.units[unit], t0, n, dacc, MSP_L1STAGE_FILL_PCT);
   }
   if (dacc == 0x123456789ull) A.batch_filtered[0] = dacc;  // keep the diagnostic keys live
 }
@@ -503,7 +513,7 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
   const uint32_t tid = threadIdx.x;
   const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
   uint32_t C, budget, staged = 0;
-  stage_geometry(NB, C, budget);
+  stage_geometry(NB, C, budget, MSP_RSTAGE_FILL_PCT);
   unsigned long long *buf = reinterpret_cast<unsigned long long *>(&g + 1);  // 2 x kRStep keys
   __shared__ unsigned long long s_rbar[2];
   const uint32_t nstep = s1 > s0 ? (s1 - s0 + kRStep - 1) / kRStep : 0;
