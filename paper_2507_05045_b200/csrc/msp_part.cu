@@ -73,11 +73,18 @@ constexpr int kUS = MSP_SCATTER_KEYS;                           // keys per lane
 // padded to an even length with key 0 so both ends stay 16-byte aligned; real keys equal to 0 are
 // never staged but counted per (batch, side) (zero_keys), and every reader skips key 0.
 // The producers' loop-vector buffers follow the struct (scatter only).
+#ifndef MSP_SPILL_LIST
+#define MSP_SPILL_LIST 64
+#endif
+constexpr int kSpillList = MSP_SPILL_LIST;  // keys ranked past C parked in shared memory until the flush
+struct SpillRec { unsigned long long key; uint32_t e, pad; };
 struct __align__(16) Stage {
   unsigned long long key[kStageKeys];
   uint32_t cnt[kMaxNB + 32];         // keys ranked into each entry this round (> C: the rest spilled);
                                      // + one dummy counter per lane (never read)
   uint32_t round_end, chunk, tctr, nstaged;
+  uint32_t nspill, spad[3];          // spill list fill (may pass kSpillList: the rest went global)
+  SpillRec spill[kSpillList];
 };
 
 // Reservation of n slots at *p, result left in flight in r (predicated: no-op when n == 0, so no
@@ -93,7 +100,7 @@ size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps
 
 __device__ __forceinline__ void stage_init(Stage &g) {
   for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
-  if (threadIdx.x == 0) { g.round_end = 0; g.nstaged = 0; }
+  if (threadIdx.x == 0) { g.round_end = 0; g.nstaged = 0; g.nspill = 0; }
 }
 
 // The CTA's next work chunk (dynamic: one global atomic per chunk), broadcast through shared memory.
@@ -150,10 +157,14 @@ __device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t
     spill |= ok[u] && r[u] >= C;
     staged += ok[u] ? 1u : 0u;
   }
-  if (__any_sync(0xffffffffu, spill)) {
+  if (__any_sync(0xffffffffu, spill)) {  // park them in the spill list (shared), flushed with the round
 #pragma unroll
     for (int u = 0; u < N; ++u)
-      if (ok[u] && r[u] >= C) stage_spill(S, ebase + j[u], key[u]);
+      if (ok[u] && r[u] >= C) {
+        const uint32_t q = atomicAdd(&g.nspill, 1u);
+        if (q < (uint32_t)kSpillList) g.spill[q] = SpillRec{key[u], ebase + j[u], 0u};
+        else stage_spill(S, ebase + j[u], key[u]);  // (list full: straight to the bucket region)
+      }
   }
   if (staged >= budget) *(volatile uint32_t *)&g.round_end = 1u;
 }
@@ -203,12 +214,15 @@ __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_
     }
     if (S.dbg) atomicAdd(S.dbg + 1, (unsigned long long)n);
   }
+  const uint32_t nsp = min(g.nspill, (uint32_t)kSpillList);
+  if (tid < nsp) stage_spill(S, g.spill[tid].e, g.spill[tid].key);
   if (issued) {
     bulk_commit();
     bulk_wait_read();
   }
   if (S.dbg && tid == 0) atomicAdd(S.dbg + 0, 1ull);
-  if (tid == 0) { g.round_end = 0u; g.nstaged = 0u; }
+  __syncthreads();  // (every thread has read nspill)
+  if (tid == 0) { g.round_end = 0u; g.nstaged = 0u; g.nspill = 0u; }
   __syncthreads();
 }
 
