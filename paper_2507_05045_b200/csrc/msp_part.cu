@@ -83,7 +83,8 @@ struct __align__(16) Stage {
   uint32_t cnt[kMaxNB + 32];         // keys ranked into each entry this round (> C: the rest spilled);
                                      // + one dummy counter per lane (never read)
   uint32_t round_end, chunk, tctr, nstaged;
-  uint32_t nspill, spad[3];          // spill list fill (may pass kSpillList: the rest went global)
+  uint32_t nspill, sbase, spad[2];   // spills so far (monotonic) and at the round's start: this
+                                     // round's list holds spills [sbase, nspill) (past kSpillList: global)
   SpillRec spill[kSpillList];
 };
 
@@ -100,7 +101,7 @@ size_t scatter_smem_bytes(int sw) { return sizeof(Stage) + (size_t)kScatterWarps
 
 __device__ __forceinline__ void stage_init(Stage &g) {
   for (uint32_t i = threadIdx.x; i < (uint32_t)kMaxNB; i += blockDim.x) g.cnt[i] = 0;
-  if (threadIdx.x == 0) { g.round_end = 0; g.nstaged = 0; g.nspill = 0; }
+  if (threadIdx.x == 0) { g.round_end = 0; g.nstaged = 0; g.nspill = 0; g.sbase = 0; }
 }
 
 // The CTA's next work chunk (dynamic: one global atomic per chunk), broadcast through shared memory.
@@ -161,7 +162,7 @@ __device__ __forceinline__ void stage_keys(Stage &g, const PartArgs &S, uint32_t
 #pragma unroll
     for (int u = 0; u < N; ++u)
       if (ok[u] && r[u] >= C) {
-        const uint32_t q = atomicAdd(&g.nspill, 1u);
+        const uint32_t q = atomicAdd(&g.nspill, 1u) - g.sbase;
         if (q < (uint32_t)kSpillList) g.spill[q] = SpillRec{key[u], ebase + j[u], 0u};
         else stage_spill(S, ebase + j[u], key[u]);  // (list full: straight to the bucket region)
       }
@@ -214,15 +215,18 @@ __device__ __forceinline__ void flush_round(Stage &g, const PartArgs &S, uint32_
     }
     if (S.dbg) atomicAdd(S.dbg + 1, (unsigned long long)n);
   }
-  const uint32_t nsp = min(g.nspill, (uint32_t)kSpillList);
-  if (tid < nsp) stage_spill(S, g.spill[tid].e, g.spill[tid].key);
+  if (tid < 32) {  // warp 0 writes the round's parked spills and alone moves the list base
+    const uint32_t nend = g.nspill, nsp = min(nend - g.sbase, (uint32_t)kSpillList);
+    for (uint32_t i = tid; i < nsp; i += 32) stage_spill(S, g.spill[i].e, g.spill[i].key);
+    __syncwarp();
+    if (tid == 0) g.sbase = nend;
+  }
   if (issued) {
     bulk_commit();
     bulk_wait_read();
   }
   if (S.dbg && tid == 0) atomicAdd(S.dbg + 0, 1ull);
-  __syncthreads();  // (every thread has read nspill)
-  if (tid == 0) { g.round_end = 0u; g.nstaged = 0u; g.nspill = 0u; }
+  if (tid == 0) { g.round_end = 0u; g.nstaged = 0u; }
   __syncthreads();
 }
 
