@@ -15,6 +15,7 @@
 // 32 entries of the rectangle's longer run (one per lane, companion vector in registers) x up to
 // kTQ entries of the shorter run (warp-uniform loads, broadcast).  Each warp takes a contiguous
 // chunk of tiles through the compacted rectangle lists (k_rects).
+#include <algorithm>
 #include <cstdint>
 #include "msp_common.cuh"
 #include "msp_kernels.h"
@@ -345,6 +346,75 @@ static void launch_mc(SinkKind kind, const EnumArgs &a, const JoinTable &jt, int
     case SINK_NONE: k_enum<MC, SINK_NONE><<<grid, 256, 0, st>>>(a, jt); break;
     default: k_enum<MC, SINK_RECOVER><<<grid, 256, 0, st>>>(a, jt); break;
   }
+}
+
+// ---------------------------------------------------------------- one-sided hit recovery
+
+// Hash of a table entry's (row-0 weight, companion words): build and lookup must agree.
+__device__ __forceinline__ uint64_t entry_hash(uint64_t w, const uint32_t *words, int nw) {
+  uint64_t h = w * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+  for (int k = 0; k < nw; ++k) {
+    h ^= words[k];
+    h *= 0x100000001B3ull;
+    h ^= h >> 29;
+  }
+  return h;
+}
+
+// Every Y entry into an open-addressing table of 2^log2 slots (entry + 1; 0 = empty).
+__global__ void k_vhash_build(const LookupArgs a, uint32_t *slots) {
+  const uint32_t msk = (1u << a.log2) - 1u;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < a.Y.n; v += gridDim.x * blockDim.x) {
+    uint32_t s = (uint32_t)(entry_hash(a.Y.w[v], a.Y.comp + (size_t)v * a.sw, a.nw) >> (64 - a.log2));
+    while (atomicCAS(slots + s, 0u, v + 1u) != 0u) s = (s + 1u) & msk;
+  }
+}
+
+// Target t (blockIdx.y stride) x X entry x: the Y entries equal to target - X[x] (row 0 and every
+// companion coordinate, exactly), emitted as pairs of the target's side.
+__global__ void k_lookup(const LookupArgs a) {
+  const uint32_t msk = (1u << a.log2) - 1u;
+  for (uint32_t t = blockIdx.y; t < a.ntg; t += gridDim.y) {
+    const LookupTarget &T = a.tg[t];
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < a.X.n; x += gridDim.x * blockDim.x) {
+      const uint64_t wx = a.X.w[x];
+      if (T.w0 < wx) continue;
+      const uint64_t wt = T.w0 - wx;
+      const uint32_t *cx = a.X.comp + (size_t)x * a.sw;
+      uint32_t words[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      bool ok = true;
+      for (int c = 0; c < a.mc; ++c) {
+        const uint32_t v = a.wide ? cx[c] : (((c & 1) ? cx[c >> 1] >> 16 : cx[c >> 1]) & 0xFFFFu);
+        if (T.tc[c] < v) { ok = false; break; }
+        const uint32_t r = T.tc[c] - v;
+        if (a.wide) words[c] = r;
+        else if (r > 0xFFFFu) { ok = false; break; }
+        else words[c >> 1] |= r << (16 * (c & 1));
+      }
+      if (!ok) continue;
+      uint32_t s = (uint32_t)(entry_hash(wt, words, a.nw) >> (64 - a.log2));
+      for (uint32_t e; (e = a.slots[s]) != 0u; s = (s + 1u) & msk) {
+        const uint32_t y = e - 1u;
+        if (a.Y.w[y] != wt) continue;
+        const uint32_t *cy = a.Y.comp + (size_t)y * a.sw;
+        bool eq = true;
+        for (int k = 0; k < a.nw; ++k) eq = eq && cy[k] == words[k];
+        if (!eq) continue;
+        const unsigned long long o = atomicAdd(a.nout, 1ull);
+        if (o < a.cap) a.out[o] = PairRec{T.gid, T.side, x, y, a.X.mask[x], a.Y.mask[y], T.key};
+      }
+    }
+  }
+}
+
+void launch_vhash_build(const LookupArgs &a, uint32_t *slots, cudaStream_t st) {
+  k_vhash_build<<<(unsigned)std::min<uint64_t>((a.Y.n + 255) / 256, 4096), 256, 0, st>>>(a, slots);
+}
+
+void launch_lookup(const LookupArgs &a, cudaStream_t st) {
+  if (!a.ntg) return;
+  const dim3 grid((unsigned)std::min<uint64_t>((a.X.n + 255) / 256, 1024), std::min<uint32_t>(a.ntg, 65535));
+  k_lookup<<<grid, 256, 0, st>>>(a);
 }
 
 int launch_enum(int mc, SinkKind kind, const EnumArgs &args, const JoinTable &jt, int num_sms,

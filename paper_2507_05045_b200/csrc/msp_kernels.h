@@ -238,6 +238,22 @@ cudaError_t launch_waves(int mc, const WavesArgs &w, int num_sms, cudaStream_t s
 
 void launch_clear(void *p, size_t bytes, int num_sms, cudaStream_t st);
 
+// One-sided hit recovery (msp_enum.cu): the pairs of the OTHER side of a batch whose companion
+// vector (row 0 included) equals a target exactly -- d minus a recovered pair's sums -- found by
+// X-entry x hash lookup of (target - X[x]) among the Y entries.
+constexpr int kLookupMaxMC = 16;
+struct LookupTarget { uint64_t w0, key; uint32_t tc[kLookupMaxMC]; uint32_t gid, side; };
+struct LookupTable { const uint64_t *w; const uint32_t *comp; const uint32_t *mask; uint32_t n; };
+struct LookupArgs {
+  LookupTable X, Y;                    // X scanned, Y hashed (slots: entry + 1, 0 empty)
+  const uint32_t *slots; uint32_t log2;
+  int sw, nw, mc, wide;                // companion layout of the tables
+  const LookupTarget *tg; uint32_t ntg;
+  PairRec *out; unsigned long long *nout; uint64_t cap;
+};
+void launch_vhash_build(const LookupArgs &a, uint32_t *slots, cudaStream_t st);
+void launch_lookup(const LookupArgs &a, cudaStream_t st);
+
 enum SinkKind { SINK_BUILD = 0, SINK_PROBE = 1, SINK_RECOVER = 2, SINK_NONE = 3 /* diagnostic: hash only */ };
 // Enumerate every pair of the launch's units, hash it, and hand the key to the sink.
 int launch_enum(int mc, SinkKind kind, const EnumArgs &args, const JoinTable &jt, int num_sms,

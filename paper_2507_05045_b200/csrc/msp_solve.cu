@@ -7,6 +7,7 @@
 // All arithmetic on the hot path runs in the kernels of msp_tables.cu / msp_enum.cu; the host only
 // plans waves and confirms the (rare) full-hash hits exactly, as the reference does on its CPU.
 #include <algorithm>
+#include <tuple>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -83,6 +84,7 @@ struct Device {
   DBuf keys, cnt, zero, zhit, hits, nhits, recs, nrecs;
   DBuf bout, bcnt;
   DBuf rkeys, runits, rfilt, rhits;
+  DBuf vslots, ltg, lout, lnout;  // one-sided recovery: hashed Y table, targets, matches
   DBuf bfilt, bhits, bovf, scratch, bk, bruns, fill, zkeys, dbg;
   DBuf cscratch[2], cfill, cbk, hunits, l2bk, l2src;
   uint64_t epoch = 0;  // tag of the last global-table wave (JoinTable::cnt)
@@ -854,16 +856,25 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     }
     return MSP_OK;
   };
-  // Recovery of a set of hit keys: re-enumerate those batches, emit the pairs whose key is a hit
-  // key, confirm exactly on the host (validate.py:285-313).  Own buffers: waves can resume after.
+  // Recovery of a set of hit keys (validate.py:285-313): re-enumerate ONE side of each hit batch (the
+  // one with fewer pairs) and emit its pairs whose key is a hit key; then, per recovered pair, find
+  // the other side's pairs whose companion vector is exactly d minus the pair's (an X-entry x hash
+  // lookup among the Y entries: k_lookup) -- a pair of the other side with the same key but another
+  // vector is an FNV collision, which the join already counted and which confirms nothing.  The
+  // exact pairs are confirmed on the host in 128-bit arithmetic.  When the one side yields more
+  // than kLookupMaxTargets pairs (degenerate multiplicities), the other side is enumerated too and
+  // every (left, right) pair of a hit key is compared, as before.  Own buffers: waves can resume.
   int64_t recovered_hh = 0;
+  bool recovered_one_sided = false;
+  constexpr size_t kLookupMaxTargets = 1u << 16;
   auto recover = [&](const std::vector<HitRec> &hv) -> int {
     if (hv.empty()) return MSP_OK;
     std::map<uint32_t, std::vector<uint64_t>> byg;
     for (const HitRec &h : hv) byg[h.gid].push_back(h.key);
-    std::vector<UnitDesc> ru;
+    std::vector<UnitDesc> ru[2];  // [0]: each batch's side with fewer pairs, [1]: the other side
+    uint64_t tb[2] = {0, 0};
     std::vector<unsigned long long> himg;
-    uint64_t tb = 0, slots = 0;
+    uint64_t slots = 0;
     for (auto &kv : byg) {
       const uint32_t g = kv.first;
       std::vector<uint64_t> ks = kv.second;
@@ -879,53 +890,150 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         while (himg[slots + sl]) sl = (sl + 1) & (uint32_t)(cap - 1);
         himg[slots + sl] = k;
       }
+      const int small = P.nl[g] <= P.nr[g] ? 0 : 1;
       for (int side = 0; side < 2; ++side) {
-        UnitDesc u = make_unit(P, g, side, tb);
+        const int pass = side == small ? 0 : 1;
+        UnitDesc u = make_unit(P, g, side, tb[pass]);
         u.region_base = (uint32_t)slots;
         u.region_log2 = l2;
         u.flags = has_zero ? 1u : 0u;
-        tb += P.tiles[2 * g + side];
-        ru.push_back(u);
+        tb[pass] += P.tiles[2 * g + side];
+        ru[pass].push_back(u);
       }
       slots += cap;
     }
     CK(D.rkeys.ensure(8 * std::max<uint64_t>(slots, 1)));
-    CK(D.runits.ensure(sizeof(UnitDesc) * ru.size()));
     CK(D.rfilt.ensure(8 * P.G));
     CK(D.rhits.ensure(8 * P.G));
     CK(cudaMemcpyAsync(D.rkeys.p, himg.data(), 8 * slots, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(D.runits.p, ru.data(), sizeof(UnitDesc) * ru.size(), cudaMemcpyHostToDevice, st));
     JoinTable rj = jt;
     rj.keys = D.rkeys.as<unsigned long long>();
     rj.nkeys = (uint32_t)slots;
     EnumArgs RA = P.base;
     RA.batch_filtered = D.rfilt.as<unsigned long long>();
     RA.batch_hits = D.rhits.as<unsigned long long>();
-    uint64_t rec_cap = std::max<uint64_t>(4096, 4 * hv.size());
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      CK(D.recs.ensure(sizeof(PairRec) * rec_cap));
-      CK(cudaMemsetAsync(D.nrecs.p, 0, 8, st));
-      rj.recs = D.recs.as<PairRec>();
-      rj.nrecs = D.nrecs.as<unsigned long long>();
-      rj.rec_cap = rec_cap;
-      set_enum_range(RA, D.runits.as<UnitDesc>(), ru.size(), tb, D.num_sms);
-      launch_enum(P.mcx, SINK_RECOVER, RA, rj, D.num_sms, st);
-      ++S.kernel_launches;
-      CK(cudaGetLastError());
-      unsigned long long nr = 0;
-      CK(cudaMemcpyAsync(&nr, D.nrecs.p, 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (nr > rec_cap) { rec_cap = nr; continue; }
-      std::vector<PairRec> recs(nr);
-      if (nr) CK(cudaMemcpy(recs.data(), D.recs.p, sizeof(PairRec) * nr, cudaMemcpyDeviceToHost));
+    std::vector<PairRec> recs;
+    auto run_pass = [&](int pass) -> int {  // enumerate the units ru[pass], append their hit pairs
+      if (ru[pass].empty()) return MSP_OK;
+      CK(D.runits.ensure(sizeof(UnitDesc) * ru[pass].size()));
+      CK(cudaMemcpyAsync(D.runits.p, ru[pass].data(), sizeof(UnitDesc) * ru[pass].size(), cudaMemcpyHostToDevice, st));
+      uint64_t rec_cap = std::max<uint64_t>(4096, 4 * hv.size());
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        CK(D.recs.ensure(sizeof(PairRec) * rec_cap));
+        CK(cudaMemsetAsync(D.nrecs.p, 0, 8, st));
+        rj.recs = D.recs.as<PairRec>();
+        rj.nrecs = D.nrecs.as<unsigned long long>();
+        rj.rec_cap = rec_cap;
+        set_enum_range(RA, D.runits.as<UnitDesc>(), ru[pass].size(), tb[pass], D.num_sms);
+        launch_enum(P.mcx, SINK_RECOVER, RA, rj, D.num_sms, st);
+        ++S.kernel_launches;
+        CK(cudaGetLastError());
+        unsigned long long nr = 0;
+        CK(cudaMemcpyAsync(&nr, D.nrecs.p, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (nr > rec_cap) { rec_cap = nr; continue; }
+        const size_t r0 = recs.size();
+        recs.resize(r0 + nr);
+        if (nr) CK(cudaMemcpy(recs.data() + r0, D.recs.p, sizeof(PairRec) * nr, cudaMemcpyDeviceToHost));
+        return MSP_OK;
+      }
+      set_err("hit recovery buffer overflow");
+      return MSP_INTERNAL;
+    };
+    if (int r = run_pass(0)) return r;
+    if (recs.size() > kLookupMaxTargets || getenv("MSP_RECOVER_TWO_SIDED")) {
+      // degenerate multiplicities (or the test seam): both sides, all pairs of a hit key compared
+      if (int r = run_pass(1)) return r;
       int64_t hh = 0;
-      const int rc2 = confirm(pr, P, recs, sols, hh);
-      if (rc2) return rc2;
+      if (int r = confirm(pr, P, recs, sols, hh)) return r;
       recovered_hh += hh;
       return MSP_OK;
     }
-    set_err("hit recovery buffer overflow");
-    return MSP_INTERNAL;
+    // targets per recovered pair: d minus its sums (128-bit; a negative row cannot be matched)
+    const int m = P.m, n = P.n;
+    std::vector<LookupTarget> tg[2];  // by the side to look up
+    for (const PairRec &r : recs) {
+      LookupTarget T{};
+      bool ok = true;
+      for (int i = 0; i < m && ok; ++i) {
+        unsigned __int128 sum = 0;
+        const uint32_t mk[2] = {r.xmask, r.ymask};
+        for (int h = 0; h < 2; ++h) {
+          const int t = 2 * (int)r.side + h;
+          for (int b = 0; b < P.b[t]; ++b)
+            if ((mk[h] >> b) & 1u) sum += pr->a[(size_t)i * n + P.start[t] + b];
+        }
+        if (sum > pr->d[i]) { ok = false; break; }
+        const unsigned __int128 rem = (unsigned __int128)pr->d[i] - sum;
+        if (i == 0) T.w0 = (uint64_t)rem;
+        else if (rem > 0xFFFFFFFFu) ok = false;  // past any companion sum of two table entries
+        else T.tc[i - 1] = (uint32_t)rem;
+      }
+      if (!ok) continue;
+      T.key = r.key;
+      T.gid = r.gid;
+      T.side = 1u - r.side;
+      tg[T.side].push_back(T);
+    }
+    const size_t nrec_side = recs.size();
+    for (int o = 0; o < 2; ++o) {
+      if (tg[o].empty()) continue;
+      const int tx = 2 * o, ty = 2 * o + 1;
+      LookupArgs la{};
+      la.X = LookupTable{table_w(D, P, tx), D.comp[tx].as<uint32_t>(), table_m(D, P, tx), 1u << P.b[tx]};
+      la.Y = LookupTable{table_w(D, P, ty), D.comp[ty].as<uint32_t>(), table_m(D, P, ty), 1u << P.b[ty]};
+      la.log2 = (uint32_t)P.b[ty] + 1;
+      la.sw = P.sw;
+      la.nw = words_for(P.mcx);
+      la.mc = m - 1;
+      la.wide = P.wide ? 1 : 0;
+      CK(D.vslots.ensure(4ull << la.log2));
+      CK(cudaMemsetAsync(D.vslots.p, 0, 4ull << la.log2, st));
+      launch_vhash_build(la, D.vslots.as<uint32_t>(), st);
+      la.slots = D.vslots.as<uint32_t>();
+      CK(D.ltg.ensure(sizeof(LookupTarget) * tg[o].size()));
+      CK(cudaMemcpyAsync(D.ltg.p, tg[o].data(), sizeof(LookupTarget) * tg[o].size(), cudaMemcpyHostToDevice, st));
+      la.tg = D.ltg.as<LookupTarget>();
+      la.ntg = (uint32_t)tg[o].size();
+      CK(D.lnout.ensure(8));
+      uint64_t cap = std::max<uint64_t>(1024, 4 * tg[o].size());
+      for (int attempt = 0;; ++attempt) {
+        CK(D.lout.ensure(sizeof(PairRec) * cap));
+        CK(cudaMemsetAsync(D.lnout.p, 0, 8, st));
+        la.out = D.lout.as<PairRec>();
+        la.nout = D.lnout.as<unsigned long long>();
+        la.cap = cap;
+        launch_lookup(la, st);
+        S.kernel_launches += 2;
+        CK(cudaGetLastError());
+        unsigned long long no = 0;
+        CK(cudaMemcpyAsync(&no, D.lnout.p, 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (no > cap) {
+          if (attempt) { set_err("hit lookup buffer overflow"); return MSP_INTERNAL; }
+          cap = no;
+          continue;
+        }
+        const size_t r0 = recs.size();
+        recs.resize(r0 + no);
+        if (no) CK(cudaMemcpy(recs.data() + r0, D.lout.p, sizeof(PairRec) * no, cudaMemcpyDeviceToHost));
+        break;
+      }
+    }
+    {  // recovered pairs with equal vectors share a target: keep each looked-up pair once
+      auto lt = [](const PairRec &a, const PairRec &b) {
+        return std::tie(a.gid, a.side, a.xidx, a.yidx) < std::tie(b.gid, b.side, b.xidx, b.yidx);
+      };
+      auto eq = [](const PairRec &a, const PairRec &b) {
+        return a.gid == b.gid && a.side == b.side && a.xidx == b.xidx && a.yidx == b.yidx;
+      };
+      std::sort(recs.begin() + nrec_side, recs.end(), lt);
+      recs.erase(std::unique(recs.begin() + nrec_side, recs.end(), eq), recs.end());
+    }
+    int64_t hh = 0;  // (counts only the exact pairs of the looked-up side: no hash-hit cross-check)
+    if (int r = confirm(pr, P, recs, sols, hh)) return r;
+    recovered_one_sided = true;
+    return MSP_OK;
   };
   auto fetch_hits = [&](uint64_t from, uint64_t to, std::vector<HitRec> &out) -> int {
     out.clear();
@@ -1773,7 +1881,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     rc = recover(hv);
     if (rc) return rc;
     mark("recovery done");
-    if (opt->mode == MSP_MODE_ALL && recovered_hh != S.hash_hits) {
+    if (opt->mode == MSP_MODE_ALL && !recovered_one_sided && recovered_hh != S.hash_hits) {
       set_err("internal error: recovered hash hits %lld != join hash hits %lld", (long long)recovered_hh,
               (long long)S.hash_hits);
       return MSP_INTERNAL;

@@ -591,6 +591,30 @@ def test_sparse_plan_alpha_windows(monkeypatch):
                 assert st2["batch_stats"] == [b for b in st0["batch_stats"] if lo <= b[0] < hi], w
 
 
+def test_one_sided_recovery_matches_two_sided(monkeypatch):
+    """Hit recovery enumerates one side of a hit batch and finds the other side's exact pairs by
+    table lookup; forcing the two-sided recovery (both sides enumerated, every pair of a hit key
+    compared) gives the same solutions and counters -- on solution-bearing K = 100 instances,
+    planted ones (equal-vector pairs on one side) and the hit-bearing (9,80) alpha-groups."""
+    cases = [(msb.generate_instance(m, 100, s), None) for (m, s) in ((4, 11), (6, 4), (7, 1))]
+    cases += [(msb.plant_instance(m, 100, s)[0], None) for (m, s) in ((5, 1), (6, 2))]
+    g = load_golden("alpha_groups_9_100_1_hits.json")
+    inst9 = inst_from(g["instance"])
+    cases += [(inst9, grp["alpha"]) for grp in g["groups"] if grp["solutions"]][:2]
+    for inst, alpha in cases:
+        opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_BATCH_STATS)
+        monkeypatch.delenv("MSP_RECOVER_TWO_SIDED", raising=False)
+        rc0, xb0, st0 = _native.solve_raw(inst.a, inst.d, opts, alpha=alpha)
+        monkeypatch.setenv("MSP_RECOVER_TWO_SIDED", "1")
+        rc1, xb1, st1 = _native.solve_raw(inst.a, inst.d, opts, alpha=alpha)
+        monkeypatch.delenv("MSP_RECOVER_TWO_SIDED")
+        assert rc0 == 0 and rc1 == 0, _native.last_error()
+        assert sorted(map(tuple, xb0.tolist())) == sorted(map(tuple, xb1.tolist()))
+        assert len(xb0) > 0
+        for k in STAT_KEYS:
+            assert st0[k] == st1[k], k
+
+
 def test_time_limit_stops_the_running_kernels():
     """The deadline reaches the running kernels (host-mapped stop word polled at every task switch of
     the persistent pipeline): a (9,80) full enumeration (~40 s) with a 1 s limit raises SolveTimeout
