@@ -231,6 +231,7 @@ struct WavesArgs {
   const unsigned long long *tasks;     // join << 63 | wave << 32 | first bucket, or wave << 32 | chunk (index into chunks)
   uint32_t ntasks;
   unsigned int *task_ctr, *scat_done, *join_done;  // zeroed before the launch
+  uint32_t fetch_ahead;                // 1: reserve the task after next one task early (level-2 launches)
   int *abort_dev;                      // stop word (deadline / cross-rank cancel): zeroed per solve, set
                                        // by the host watchdog with an async copy while kernels run
 };

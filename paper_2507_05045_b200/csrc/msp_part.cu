@@ -518,13 +518,23 @@ __global__ void __launch_bounds__(kScatterThreads, kScatterCtas) k_scatter(const
 // stage (the next step always in flight), each step prefetched into L2 kRPrefetch steps earlier
 // (cp.async.bulk.prefetch.L2), so a step copy waits on L2, not on HBM.
 // Ends with a barrier.
-constexpr uint32_t kRStep = 2048;                 // keys per step (two 16 KB buffers)
+#ifndef MSP_RSTEP
+#define MSP_RSTEP 2048
+#endif
+#ifndef MSP_RFENCE_AT_END
+#define MSP_RFENCE_AT_END 1
+#endif
+#ifndef MSP_RBUFS
+#define MSP_RBUFS 2
+#endif
+constexpr uint32_t kRStep = MSP_RSTEP;            // keys per step
+constexpr uint32_t kRBufs = MSP_RBUFS;            // step buffers behind the stage
 #ifndef MSP_RPREFETCH
 #define MSP_RPREFETCH 8
 #endif
 constexpr uint32_t kRPrefetch = MSP_RPREFETCH;    // steps prefetched into L2 (TMA prefetch) ahead of the step copies
 constexpr int kRPerThread = (kRStep + kScatterThreads - 1) / kScatterThreads;
-size_t rescatter_smem_bytes() { return sizeof(Stage) + 2ull * kRStep * 8; }
+size_t rescatter_smem_bytes() { return sizeof(Stage) + (size_t)kRBufs * kRStep * 8; }
 
 __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, const RescatterSrc &src, uint32_t s0,
                                                 uint32_t s1) {
@@ -532,39 +542,40 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
   const uint32_t ebase = src.role * S.nb + src.fine_base, NB = src.nf, nc = src.nc;
   uint32_t C, budget, staged = 0;
   stage_geometry(NB, C, budget, MSP_RSTAGE_FILL_PCT);
-  unsigned long long *buf = reinterpret_cast<unsigned long long *>(&g + 1);  // 2 x kRStep keys
-  __shared__ unsigned long long s_rbar[2];
+  unsigned long long *buf = reinterpret_cast<unsigned long long *>(&g + 1);  // kRBufs x kRStep keys
+  __shared__ unsigned long long s_rbar[kRBufs];
   const uint32_t nstep = s1 > s0 ? (s1 - s0 + kRStep - 1) / kRStep : 0;
   auto prefetch = [&](uint32_t c) {  // thread 0: step c into L2 (TMA prefetch, no shared memory)
     if (kRPrefetch == 0 || c >= nstep) return;
     const uint32_t a = s0 + c * kRStep, n = min(s1 - a, kRStep);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src.keys + a), "r"(8u * ((n + 1u) & ~1u)) : "memory");
   };
-  auto issue = [&](uint32_t c) {  // thread 0: step c into buffer c & 1
+  auto issue = [&](uint32_t c) {  // thread 0: step c into buffer c % kRBufs
     prefetch(c + kRPrefetch);
     const uint32_t a = s0 + c * kRStep, n = min(s1 - a, kRStep);
     fence_proxy_async_smem();
+    const uint32_t bi = c % kRBufs;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[c & 1])), "r"(8u * ((n + 1u) & ~1u)) : "memory");
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[bi])), "r"(8u * ((n + 1u) & ~1u)) : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"((uint32_t)__cvta_generic_to_shared(buf + (c & 1) * kRStep)), "l"(src.keys + a),
-                    "r"(8u * ((n + 1u) & ~1u)), "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[c & 1])) : "memory");
+                 :: "r"((uint32_t)__cvta_generic_to_shared(buf + bi * kRStep)), "l"(src.keys + a),
+                    "r"(8u * ((n + 1u) & ~1u)), "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[bi])) : "memory");
   };
   if (tid == 0) {
-    for (int k = 0; k < 2; ++k)
+    for (uint32_t k = 0; k < kRBufs; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[k])) : "memory");
-    for (uint32_t c = 2; c < kRPrefetch; ++c) prefetch(c);
-    for (uint32_t c = 0; c < 2 && c < nstep; ++c) issue(c);
+    for (uint32_t c = kRBufs; c < kRPrefetch; ++c) prefetch(c);
+    for (uint32_t c = 0; c < kRBufs && c < nstep; ++c) issue(c);
   }
   __syncthreads();
-  uint32_t ph[2] = {0, 0};
+  uint32_t phm = 0;  // bit k: the parity buffer k's barrier completes next
   for (uint32_t c = 0; c < nstep; ++c) {
-    const uint32_t bsel = c & 1;
+    const uint32_t bsel = c % kRBufs;
     uint32_t done = 0;
     while (!done)
       asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                   : "=r"(done) : "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[bsel])), "r"(ph[bsel]) : "memory");
-    ph[bsel] ^= 1u;
+                   : "=r"(done) : "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[bsel])), "r"((phm >> bsel) & 1u) : "memory");
+    phm ^= 1u << bsel;
     const uint32_t n = min(s1 - (s0 + c * kRStep), kRStep);
     const unsigned long long *bk = buf + bsel * kRStep;
     unsigned long long key[kRPerThread];
@@ -578,16 +589,20 @@ __device__ __forceinline__ void rescatter_chunk(Stage &g, const PartArgs &S, con
       j[u] = __umulhi((uint32_t)(key[u] >> 32) * nc, NB);
     }
     stage_keys<kRPerThread>(g, S, ebase, C, staged, budget, key, j, ok);
-    fence_proxy_async_smem();  // (the staged keys -> a flush's bulk copies)
+    if (!MSP_RFENCE_AT_END) fence_proxy_async_smem();  // (the staged keys -> a flush's bulk copies)
     const bool end = __syncthreads_or(g.round_end != 0u) || c + 1 == nstep;  // (the buffer is free)
-    if (tid == 0 && c + 2 < nstep) issue(c + 2);
+    if (tid == 0 && c + kRBufs < nstep) issue(c + kRBufs);
     if (end) {
+      if (MSP_RFENCE_AT_END) {  // the proxy fence once per round, not per step
+        fence_proxy_async_smem();
+        __syncthreads();
+      }
       flush_round(g, S, ebase, NB, C);
       staged = 0;
     }
   }
   if (tid == 0)
-    for (int k = 0; k < 2; ++k)
+    for (uint32_t k = 0; k < kRBufs; ++k)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];" :: "r"((uint32_t)__cvta_generic_to_shared(&s_rbar[k])) : "memory");
   bulk_complete();
   __syncthreads();
@@ -940,11 +955,22 @@ __global__ void __launch_bounds__(kScatterThreads, 1) k_waves(const WavesArgs W)
     }
   };
   Next nc;
-  if (tid == 0) fetch(task_word(atomicAdd(W.task_ctr, 1u)), nc);
+  uint32_t na = 0;  // (fetch_ahead: the queue index of the task after next, reserved a task early)
+  if (tid == 0) {
+    fetch(task_word(atomicAdd(W.task_ctr, 1u)), nc);
+    if (W.fetch_ahead) na = atomicAdd(W.task_ctr, 1u);
+  }
   while (true) {
     if (tid == 0) {
       const Next cur = nc;
-      if (cur.tk != ~0ull) fetch(task_word(atomicAdd(W.task_ctr, 1u)), nc);
+      if (cur.tk != ~0ull) {
+        if (W.fetch_ahead) {
+          fetch(task_word(na), nc);
+          na = atomicAdd(W.task_ctr, 1u);
+        } else {
+          fetch(task_word(atomicAdd(W.task_ctr, 1u)), nc);
+        }
+      }
       // stop (deadline / cancel, MSP_OPTIONS): every CTA leaves at its next task switch, waits included
       bool stop = cur.stop != 0;
       if (cur.ctr && !stop) {
