@@ -1540,6 +1540,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         S.kernel_launches += 2;
       }
       // level 2 waves over the coarse buckets
+      hmark("L1 launched");
       mark("huge: level 2 setup");
       const uint32_t NF = (uint32_t)std::max<uint64_t>(1, (uint64_t)std::ceil(mb / kBucketTargetMax));
       if (NF > (uint32_t)kMaxUnitBuckets) { set_err("coarse bucket too large for one level-2 wave"); return MSP_UNSUPPORTED; }
@@ -1615,6 +1616,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         }
       }
       l2off.push_back(l2ch.size());
+      hmark("L2 lists built");
       CK(D.l2chunks.ensure(8 * std::max<size_t>(1, l2ch.size())));
       if (int ru_ = upload(D.l2chunks.p, l2ch.data(), 8 * l2ch.size())) return ru_;
       if (!(opt->flags & MSP_FLAG_WAVE_LAUNCHES)) {  // level-2 waves through the persistent pipeline
@@ -1645,7 +1647,9 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         W.fetch_ahead = 1;  // level-2 tasks have no scatter -> join order to upset (measured -0.3%)
         if (const char *ev = getenv("MSP_L2_FETCH_AHEAD")) W.fetch_ahead = (uint32_t)atoi(ev);
         W.chunks = D.l2chunks.as<unsigned long long>();
+        hmark("L2 pipeline start");
         rc = run_pipeline(W, wds, std::vector<uint64_t>(lw.size(), 0), false);  // (timed per batch below)
+        hmark("L2 pipeline queued");
         if (rc) return rc;
       }
       for (size_t wi = 0; (opt->flags & MSP_FLAG_WAVE_LAUNCHES) && wi < lw.size(); ++wi) {
