@@ -103,6 +103,11 @@ def lib():
         L.oracle_alpha_group.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                          C.c_uint64, C.c_int, C.c_int, C.POINTER(GroupResult)]
         L.oracle_group_result_free.argtypes = [C.POINTER(GroupResult)]
+        L.oracle_groups_open.restype = C.c_void_p
+        L.oracle_groups_open.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.oracle_groups_close.argtypes = [C.c_void_p]
+        L.oracle_groups_run.restype = C.c_int
+        L.oracle_groups_run.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.POINTER(GroupResult)]
         _lib = L
     return _lib
 
@@ -212,6 +217,16 @@ def stream(a, d):
     return out
 
 
+def _group_dict(res: GroupResult, n: int) -> dict:
+    ns = res.n_solutions
+    xb = np.ctypeslib.as_array(res.xbits, shape=(ns * n,)).reshape(ns, n).copy() if ns else np.zeros((0, n), np.uint8)
+    keys = (np.ctypeslib.as_array(res.hit_keys, shape=(res.n_hit_keys,)).tolist() if res.n_hit_keys else [])
+    out = {k: int(getattr(res, k)) for k in ("n_left", "n_right", "filtered", "hash_hits", "exact_hits", "passes")}
+    out["hit_keys"] = [int(k) for k in keys]
+    out["solutions"] = sorted("".join(str(int(v)) for v in row) for row in xb)
+    return out
+
+
 def alpha_group(a, d, alpha: int, threads: int = 0, passes: int = 0) -> dict:
     """One alpha-group (batch) of the instance through the streaming CPU restatement
     (msp_oracle_groups.cc): validate_chunked's per-batch counters + solutions, for batches too big
@@ -224,12 +239,40 @@ def alpha_group(a, d, alpha: int, threads: int = 0, passes: int = 0) -> dict:
     try:
         if rc:
             raise ValueError("oracle_alpha_group failed")
-        ns = res.n_solutions
-        xb = np.ctypeslib.as_array(res.xbits, shape=(ns * n,)).reshape(ns, n).copy() if ns else np.zeros((0, n), np.uint8)
-        keys = (np.ctypeslib.as_array(res.hit_keys, shape=(res.n_hit_keys,)).tolist() if res.n_hit_keys else [])
-        out = {k: int(getattr(res, k)) for k in ("n_left", "n_right", "filtered", "hash_hits", "exact_hits", "passes")}
+        return _group_dict(res, n)
     finally:
         lib().oracle_group_result_free(C.byref(res))
-    out["hit_keys"] = [int(k) for k in keys]
-    out["solutions"] = sorted("".join(str(int(v)) for v in row) for row in xb)
-    return out
+
+
+class AlphaGroups:
+    """An instance's quarter tables built once for many alpha-group runs (msp_oracle_groups.cc).
+    run(alpha, method=1) is the filter join, method=0 the hash-range sort-merge of alpha_group();
+    both compute validate_chunked's per-batch counters exactly."""
+
+    def __init__(self, a, d):
+        self.a, self.d = _u64(a), _u64(d)
+        self.m, self.n = self.a.shape
+        self.h = lib().oracle_groups_open(self.m, self.n, _ptr(self.a), _ptr(self.d))
+        if not self.h:
+            raise ValueError("oracle_groups_open failed")
+
+    def run(self, alpha: int, method: int = 1, threads: int = 0, passes: int = 0) -> dict:
+        res = GroupResult()
+        rc = lib().oracle_groups_run(self.h, alpha, threads, method, passes, C.byref(res))
+        try:
+            if rc:
+                raise ValueError("oracle_groups_run failed")
+            return _group_dict(res, self.n)
+        finally:
+            lib().oracle_group_result_free(C.byref(res))
+
+    def close(self):
+        if self.h:
+            lib().oracle_groups_close(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

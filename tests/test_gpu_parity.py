@@ -345,6 +345,30 @@ def test_alpha_groups_with_hits_9_80():
 
 
 @pytest.mark.slow
+def test_full_9_80_hits_match_oracle_groups():
+    """The headline (9,80) s1 full enumeration, batch by batch against the CPU oracle: the GPU's
+    per-batch stats (MSP_FLAG_BATCH_STATS) put hash hits in exactly the 92 batches the oracle goldens
+    hold (alpha_groups_9_100_1_hits*.json), each batch's (n_left, n_right, filtered, hash_hits) equals
+    the oracle's, and the 7 solutions are the union of the oracle's per-batch solutions."""
+    g10 = load_golden("alpha_groups_9_100_1_hits.json")
+    gall = load_golden("alpha_groups_9_100_1_hits_all.json")
+    inst = inst_from(g10["instance"])
+    groups = {grp["alpha"]: grp for grp in g10["groups"] + gall["groups"]}
+    opts = _native.make_options(mode="all", flags=_native.MSP_FLAG_BATCH_STATS)
+    rc, xb, st = _native.solve_raw(inst.a, inst.d, opts)
+    assert rc == 0, _native.last_error()
+    assert st["hash_hits"] == 99 and st["exact_hits"] == 7 and st["batches"] == 1911
+    gpu_hits = {b[0]: b for b in st["batch_stats"] if b[4] > 0}
+    assert sorted(gpu_hits) == sorted(gall["hit_alphas"])
+    for alpha, grp in groups.items():
+        assert gpu_hits[alpha][1:] == (grp["n_left"], grp["n_right"], grp["filtered"], grp["hash_hits"]), alpha
+    if len(groups) == len(gall["hit_alphas"]):  # every hit batch pinned: the totals and solutions too
+        assert sum(grp["hash_hits"] for grp in groups.values()) == 99
+        sols = sorted(s for grp in groups.values() for s in grp["solutions"])
+        assert sorted("".join(map(str, r)) for r in xb.tolist()) == sols
+
+
+@pytest.mark.slow
 def test_planted_9_80_found():
     """BASELINE configs[4]: a planted-feasible (9,80) instance, full enumeration: x* is found."""
     inst, x = msb.plant_instance(9, 100, 1)
