@@ -239,26 +239,55 @@ __device__ __forceinline__ void stage_geometry(uint32_t NB, uint32_t &C, uint32_
 
 // ---------------------------------------------------------------- tile descriptors
 
-// One warp per rectangle, lanes over its nl x nq warp tiles (consecutive lanes write consecutive
-// 16-byte descriptors: coalesced).
+// A warp takes 32 rectangles at a time (one per lane: their descriptors load in parallel), scans
+// their tile counts, and writes the group's tiles as one flat range: lane l writes tile t0 + l of the
+// range, found in its rectangle by a 5-step search over the scanned counts.  Most rectangles hold
+// one or two tiles, so a warp per rectangle left the lanes idle behind its dependent loads.
 __global__ void k_tiles(const TileGenArgs a) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t wpg = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t r = a.rect_lo + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.rect_hi; r += wpg) {
-    const RectDesc R = a.rects[r];
-    const uint32_t gs = R.gs();
-    const uint32_t unit = a.gs_unit ? a.gs_unit[gs] : 0u;
-    if (unit == 0xFFFFFFFFu) continue;
-    TileDesc *out = a.out + (a.gs_tile_base ? a.gs_tile_base[gs] : 0ull) + R.tile_off;
-    const uint32_t lx = R.lane_is_x() ? 1u : 0u;
-    const uint32_t nt = R.nl * R.nq;
-    for (uint32_t t = lane; t < nt; t += 32) {
-      const uint32_t lc = t / R.nq, qc = t - lc * R.nq;
-      const uint32_t ln = min(32u, R.L - lc * 32);
-      const uint32_t qn = min((uint32_t)kTQ, R.Q - qc * kTQ);
-      const uint4 v = make_uint4(R.lane_start + lc * 32, R.loop_start + qc * kTQ,
-                                 unit | ((ln - 1) << 8) | ((qn - 1) << 13) | (lx << 18), 0u);
-      *reinterpret_cast<uint4 *>(out + t) = v;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  const uint32_t n = a.rect_hi - a.rect_lo;
+  for (uint32_t base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; base < n; base += nw * 32u) {
+    uint32_t nt = 0, ls = 0, qs = 0, L = 0, Q = 0, nq = 1, w2 = 0;
+    unsigned long long obase = 0;
+    if (base + lane < n) {
+      const RectDesc R = a.rects[a.rect_lo + base + lane];
+      const uint32_t gs = R.gs();
+      const uint32_t unit = a.gs_unit ? a.gs_unit[gs] : 0u;
+      if (unit != 0xFFFFFFFFu) {
+        nt = R.nl * R.nq;
+        ls = R.lane_start; qs = R.loop_start; L = R.L; Q = R.Q; nq = R.nq;
+        w2 = unit | ((R.lane_is_x() ? 1u : 0u) << 18);
+        obase = (unsigned long long)(a.out + (a.gs_tile_base ? a.gs_tile_base[gs] : 0ull) + R.tile_off);
+      }
+    }
+    uint32_t inc = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(~0u, inc, o);
+      if (lane >= (uint32_t)o) inc += v;
+    }
+    const uint32_t total = __shfl_sync(~0u, inc, 31), exc = inc - nt;
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      uint32_t k = 0;  // first lane whose inclusive count exceeds t
+#pragma unroll
+      for (uint32_t s = 16; s; s >>= 1) {
+        const uint32_t v = __shfl_sync(~0u, inc, k + s - 1);
+        if (v <= t) k += s;
+      }
+      const uint32_t kk = min(k, 31u);
+      const uint32_t tl = t - __shfl_sync(~0u, exc, kk);
+      const uint32_t knq = __shfl_sync(~0u, nq, kk), kls = __shfl_sync(~0u, ls, kk), kqs = __shfl_sync(~0u, qs, kk);
+      const uint32_t kL = __shfl_sync(~0u, L, kk), kQ = __shfl_sync(~0u, Q, kk), kw2 = __shfl_sync(~0u, w2, kk);
+      const unsigned long long ko = __shfl_sync(~0u, obase, kk);
+      if (t < total) {
+        const uint32_t lc = tl / knq, qc = tl - lc * knq;
+        const uint32_t ln = min(32u, kL - lc * 32);
+        const uint32_t qn = min((uint32_t)kTQ, kQ - qc * kTQ);
+        const uint4 v = make_uint4(kls + lc * 32, kqs + qc * kTQ, kw2 | ((ln - 1) << 8) | ((qn - 1) << 13), 0u);
+        *reinterpret_cast<uint4 *>(reinterpret_cast<TileDesc *>(ko) + tl) = v;
+      }
     }
   }
 }
@@ -266,7 +295,7 @@ __global__ void k_tiles(const TileGenArgs a) {
 void launch_tiles(const TileGenArgs &a, cudaStream_t st) {
   const uint32_t n = a.rect_hi - a.rect_lo;
   if (!n) return;
-  const uint32_t blocks = (n + 7) / 8;  // 8 warps per block
+  const uint32_t blocks = (n + 255) / 256;  // 8 warps per block, 32 rectangles per warp
   k_tiles<<<blocks < 2368 ? blocks : 2368, 256, 0, st>>>(a);
 }
 
