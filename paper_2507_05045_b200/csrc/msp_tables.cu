@@ -88,29 +88,30 @@ __global__ void k_runs(RunArgs args) {
   }
 }
 
-// Block-wide exclusive scan of one u32 per thread (blockDim.x multiple of 32, <= 1024).
-__device__ uint32_t block_excl_scan(uint32_t v, uint32_t &total) {
-  __shared__ uint32_t warp_sums[32];
+// Block-wide exclusive scan of one value per thread (blockDim.x multiple of 32, <= 1024).
+template <class T>
+__device__ T block_excl_scan(T v, T &total) {
+  __shared__ T warp_sums[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  uint32_t x = v;
+  T x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    const T y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) warp_sums[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    uint32_t s = lane < nw ? warp_sums[lane] : 0;
+    T s = lane < nw ? warp_sums[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      const T y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
     warp_sums[lane] = s;  // inclusive
   }
   __syncthreads();
-  const uint32_t base = wid ? warp_sums[wid - 1] : 0;
+  const T base = wid ? warp_sums[wid - 1] : 0;
   total = warp_sums[nw - 1];
   __syncthreads();
   return base + x - v;
@@ -124,7 +125,7 @@ __global__ void k_yruns(YRunArgs args) {
     const uint32_t w = w0 + threadIdx.x;
     const uint32_t len = w <= t.S ? t.run_end[w] - t.run_start[w] : 0;
     uint32_t tot;
-    const uint32_t pos = block_excl_scan(len > 0, tot);
+    const uint32_t pos = block_excl_scan<uint32_t>(len > 0, tot);
     if (len > 0) {
       t.out_w[base + pos] = w;
       t.out_start[base + pos] = t.run_start[w];
@@ -136,19 +137,24 @@ __global__ void k_yruns(YRunArgs args) {
 }
 
 // hl[alpha] = sum_r |A_{alpha - w_r}| |B_r| (left) and hr[beta] = sum_r |C_{beta - w_r}| |D_r|.
+// One warp per value v, lanes over the Y runs, then a warp sum (a thread per v left the GPU nearly
+// empty: ~3000 values at (7,60), each a loop over ~1500 runs).
 __global__ void k_conv(ConvArgs args) {
   const ConvSide s = args.s[blockIdx.y];
-  const uint32_t ny = *s.ny;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= s.vmax; v += gridDim.x * blockDim.x) {
+  const uint32_t ny = *s.ny, lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v <= s.vmax; v += nw) {
     unsigned long long acc = 0;
-    for (uint32_t r = 0; r < ny; ++r) {
+    for (uint32_t r = lane; r < ny; r += 32) {
       const uint32_t wy = s.yw[r];
       if (wy > v) continue;
       const uint32_t wx = v - wy;
       if (wx > s.SX) continue;
       acc += (unsigned long long)(s.x_end[wx] - s.x_start[wx]) * s.ylen[r];
     }
-    s.out[v] = acc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(~0u, acc, o);
+    if (lane == 0) s.out[v] = acc;
   }
 }
 
@@ -161,7 +167,7 @@ __global__ void k_groups(GroupArgs g) {
     uint64_t be = ok ? g.target - al : 0;
     ok = ok && be <= g.bmax && g.hr[be] > 0;
     uint32_t tot;
-    const uint32_t pos = block_excl_scan(ok, tot);
+    const uint32_t pos = block_excl_scan<uint32_t>(ok, tot);
     if (ok && base + pos < g.max_groups) {
       g.alpha[base + pos] = al;
       g.nl[base + pos] = g.hl[al];
@@ -201,9 +207,12 @@ __global__ void k_rects(RectArgs p) {
         for (uint32_t k = 0; k < np; ++k) tiles += pc[k].nl * pc[k].nq;
       }
     }
-    uint32_t ttot, rtot;
-    const uint32_t tpos = block_excl_scan(tiles, ttot);
-    const uint32_t rpos = block_excl_scan(np, rtot);
+    // one scan of both counts: tiles in the low 48 bits, rectangles (<= 2 per thread) in the high 16
+    unsigned long long tot;
+    const unsigned long long pos = block_excl_scan<unsigned long long>(tiles | (unsigned long long)np << 48, tot);
+    const unsigned long long kLow = (1ull << 48) - 1;
+    const uint64_t tpos = pos & kLow, ttot = tot & kLow;
+    const uint32_t rpos = (uint32_t)(pos >> 48), rtot = (uint32_t)(tot >> 48);
     if (write) {
       uint32_t t = (uint32_t)(tbase + tpos);
       for (uint32_t k = 0; k < np; ++k) {
@@ -261,8 +270,8 @@ void launch_runs(const RunArgs &a, uint32_t max_size, cudaStream_t st) {
 }
 void launch_yruns(const YRunArgs &a, cudaStream_t st) { k_yruns<<<2, 1024, 0, st>>>(a); }
 void launch_conv(const ConvArgs &a, uint32_t vmax, cudaStream_t st) {
-  uint32_t blocks = (vmax + 256) / 256;
-  if (blocks > 4096) blocks = 4096;
+  uint32_t blocks = (vmax + 8) / 8;  // 8 warps per block, a warp per value
+  if (blocks > 8192) blocks = 8192;
   k_conv<<<dim3(blocks, 2), 256, 0, st>>>(a);
 }
 void launch_groups(const GroupArgs &a, cudaStream_t st) { k_groups<<<1, 1024, 0, st>>>(a); }
