@@ -73,6 +73,10 @@ struct DBuf {
 
 struct Device {
   int dev = -1;
+  // host staging vectors of the partitioned-wave path, kept across solves: their capacity (up to a
+  // few hundred KB each) would otherwise be fresh mmap'd memory that page-faults on every solve
+  std::vector<unsigned long long> h_tasks, h_tch;
+  std::vector<UnitDesc> h_units;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   std::mutex mu;
@@ -797,6 +801,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   CK(D.nrecs.ensure(8));
   CK(cudaMemsetAsync(D.nhits.p, 0, 8, st));
   CK(cudaMemsetAsync(D.err.p, 0, 16, st));
+  hmark("counters zeroed");
   JoinTable jt{};
   jt.hits = D.hits.as<HitRec>();
   jt.nhits = D.nhits.as<unsigned long long>();
@@ -1093,6 +1098,27 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     D.ring_off = (D.ring_off + bytes + 255) & ~(size_t)255;
     return MSP_OK;
   };
+  // Room for `bytes` in the pinned upload ring, to be filled in place and sent with ring_send (no
+  // staging copy); nullptr when the ring cannot hold it (the caller then uses upload).
+  auto ring_take = [&](size_t bytes) -> char * {
+    constexpr size_t kRing = 64ull << 20;
+    if (!bytes || bytes > kRing) return nullptr;
+    if (!D.ring) {
+      if (cudaMallocHost(&D.ring, kRing) != cudaSuccess) { D.ring = nullptr; return nullptr; }
+      D.ring_cap = kRing;
+      D.ring_off = 0;
+    }
+    if (D.ring_off + bytes > D.ring_cap) {
+      if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
+      D.ring_off = 0;
+    }
+    return reinterpret_cast<char *>(D.ring) + D.ring_off;
+  };
+  auto ring_send = [&](void *dst, size_t bytes) -> int {
+    CK(cudaMemcpyAsync(dst, D.ring + D.ring_off, bytes, cudaMemcpyHostToDevice, st));
+    D.ring_off = (D.ring_off + bytes + 255) & ~(size_t)255;
+    return MSP_OK;
+  };
   // buckets per role of one partitioned wave (scatter entries = 2x): fewer entries give longer
   // runs per round; MSP_WAVE_BUCKETS overrides for tuning
   uint32_t wave_buckets = kMaxWaveBuckets;
@@ -1130,25 +1156,36 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
     const size_t seg = periodic ? 16 : wds.size();
     for (size_t s0 = 0; s0 < wds.size() && !stopped; s0 += seg) {
       const size_t s1 = std::min(wds.size(), s0 + seg);
-      std::vector<unsigned long long> tasks;  // S(s0) S(s0+1) S(s0+2) J(s0) S(s0+3) J(s0+1) ... J(s1-1)
-      {
-        size_t nt = 0;
-        for (size_t w = s0; w < s1; ++w) nt += wds[w].nchunks + (wds[w].nb + kJoinGroup - 1) / kJoinGroup;
-        tasks.reserve(nt);
-      }
-      auto push_join = [&](size_t w) {
-        for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks.push_back((1ull << 63) | ((unsigned long long)w << 32) | b);
+      // task list S(s0) S(s0+1) S(s0+2) J(s0) S(s0+3) J(s0+1) ... J(s1-1), written in place into the
+      // pinned upload ring (ranges filled by index: no per-task push)
+      size_t nt = 0;
+      for (size_t w = s0; w < s1; ++w) nt += wds[w].nchunks + (wds[w].nb + kJoinGroup - 1) / kJoinGroup;
+      unsigned long long *tasks = reinterpret_cast<unsigned long long *>(ring_take(8 * nt));
+      std::vector<unsigned long long> &tv = D.h_tasks;
+      if (!tasks) { tv.resize(nt); tasks = tv.data(); }
+      size_t o = 0;
+      auto put_join = [&](size_t w) {
+        const unsigned long long hi = (1ull << 63) | ((unsigned long long)w << 32);
+        for (uint32_t b = 0; b < wds[w].nb; b += kJoinGroup) tasks[o++] = hi | b;
       };
       for (size_t w = s0; w < s1; ++w) {
-        for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks.push_back(((unsigned long long)w << 32) | (wds[w].chunk0 + c));
-        if (w >= s0 + kWaveLookahead) push_join(w - kWaveLookahead);
+        const unsigned long long hi = (unsigned long long)w << 32, c0 = wds[w].chunk0;
+        for (uint32_t c = 0; c < wds[w].nchunks; ++c) tasks[o + c] = hi | (c0 + c);
+        o += wds[w].nchunks;
+        if (w >= s0 + kWaveLookahead) put_join(w - kWaveLookahead);
       }
-      for (size_t w = s1 > s0 + kWaveLookahead ? s1 - kWaveLookahead : s0; w < s1; ++w) push_join(w);
-      CK(D.tasks.ensure(8 * tasks.size()));
-      if (int ru_ = upload(D.tasks.p, tasks.data(), 8 * tasks.size())) return ru_;
+      for (size_t w = s1 > s0 + kWaveLookahead ? s1 - kWaveLookahead : s0; w < s1; ++w) put_join(w);
+      hmark("task list built");
+      CK(D.tasks.ensure(8 * nt));
+      if (tasks == tv.data()) {
+        if (int ru_ = upload(D.tasks.p, tasks, 8 * nt)) return ru_;
+      } else if (int ru_ = ring_send(D.tasks.p, 8 * nt)) {
+        return ru_;
+      }
+      hmark("task list uploaded");
       CK(cudaMemsetAsync(W.task_ctr, 0, 4, st));
       W.tasks = D.tasks.as<unsigned long long>();
-      W.ntasks = (uint32_t)tasks.size();
+      W.ntasks = (uint32_t)nt;
       if (profile && timed) CK(cudaEventRecord(D.pev[0], st));
       mark("k_waves launch");
       CK(launch_waves(P.mcx, W, D.num_sms, st));
@@ -1189,11 +1226,13 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       part_b.push_back(g);
   }
 
+  hmark("classified");
   // ---- partitioned waves
   {
     struct PWave { size_t u0, u1, b0, nb; uint64_t t0, ntiles, scratch, pairs; uint32_t g0, g1; };
     std::vector<PWave> pw;
-    std::vector<UnitDesc> units;
+    std::vector<UnitDesc> &units = D.h_units;
+    units.clear();
     std::vector<BucketRun> bruns;  // per batch: its buckets' regions (expanded on the device)
     uint32_t nbt_all = 0;
     PWave cur{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -1323,41 +1362,57 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       pa.nhits = D.nhits.as<unsigned long long>();
       pa.hit_cap = hit_cap;
       pa.batch_hits = D.bhits.as<unsigned long long>();
+      hmark("tiles launched");
       ScatterArgs sa = scatter_base(P, A);
         sa.abort_dev = D.abort_dev.as<int>();
       if (!per_wave) {  // one persistent launch per segment of waves (msp_part.cu k_waves)
-        std::vector<unsigned long long> tch;  // task chunks: <= kTaskTiles tiles of one unit
-        tch.reserve(all_tiles / kTaskTilesMin + units.size());
+        // task chunks (<= tt tiles of one unit each): counted per wave, then written in place into the
+        // pinned upload ring
         std::vector<WaveDesc> wds(pw.size());
+        std::vector<uint64_t> wtt(pw.size());
+        size_t ntch = 0;
         for (size_t wi = 0; wi < pw.size(); ++wi) {
           const PWave &w = pw[wi];
           WaveDesc &wd = wds[wi];
-          wd.tile0 = (uint32_t)w.t0;
-          wd.chunk0 = (uint32_t)tch.size();
-          uint64_t t = 0;
           const uint64_t ntask = (uint64_t)D.num_sms * MSP_TASKS_PER_SM;
           const uint64_t tt = kTaskTiles ? kTaskTiles
                                          : std::min<uint64_t>(0xFFFF, std::max(kTaskTilesMin, (w.ntiles + ntask - 1) / ntask));
-          for (size_t i = w.u0; i < w.u1; ++i) {
-            const uint64_t nt = P.tiles[2 * (size_t)units[i].gid + units[i].side];
-            for (uint64_t k = 0; k < nt; k += tt) {
-              const uint64_t c = std::min<uint64_t>(tt, nt - k);
-              tch.push_back((t + k) | (c << 32) | ((unsigned long long)(i - w.u0) << 48));
-            }
-            t += nt;
-          }
-          wd.nchunks = (uint32_t)(tch.size() - wd.chunk0);
+          wtt[wi] = tt;
+          wd.tile0 = (uint32_t)w.t0;
+          wd.chunk0 = (uint32_t)ntch;
+          for (size_t i = w.u0; i < w.u1; ++i) ntch += (P.tiles[2 * (size_t)units[i].gid + units[i].side] + tt - 1) / tt;
+          wd.nchunks = (uint32_t)(ntch - wd.chunk0);
           wd.unit0 = (uint32_t)w.u0;
           wd.b0 = (uint32_t)w.b0;
           wd.nb = (uint32_t)w.nb;
           wd.njoin = (uint32_t)((w.nb + kJoinGroup - 1) / kJoinGroup);
         }
-        CK(D.tchunks.ensure(8 * std::max<size_t>(1, tch.size())));
-        if (int ru_ = upload(D.tchunks.p, tch.data(), 8 * tch.size())) return ru_;
+        unsigned long long *tch = reinterpret_cast<unsigned long long *>(ring_take(8 * ntch));
+        std::vector<unsigned long long> &tcv = D.h_tch;
+        if (!tch) { tcv.resize(std::max<size_t>(1, ntch)); tch = tcv.data(); }
+        for (size_t wi = 0, o = 0; wi < pw.size(); ++wi) {
+          const PWave &w = pw[wi];
+          const uint64_t tt = wtt[wi];
+          uint64_t t = 0;
+          for (size_t i = w.u0; i < w.u1; ++i) {
+            const uint64_t nt = P.tiles[2 * (size_t)units[i].gid + units[i].side];
+            const unsigned long long hi = (unsigned long long)(i - w.u0) << 48;
+            for (uint64_t k = 0; k < nt; k += tt) tch[o++] = (t + k) | (std::min<uint64_t>(tt, nt - k) << 32) | hi;
+            t += nt;
+          }
+        }
+        hmark("task chunks built");
+        CK(D.tchunks.ensure(8 * std::max<size_t>(1, ntch)));
+        if (tch == tcv.data()) {
+          if (int ru_ = upload(D.tchunks.p, tch, 8 * ntch)) return ru_;
+        } else if (int ru_ = ring_send(D.tchunks.p, 8 * ntch)) {
+          return ru_;
+        }
         CK(D.wdesc.ensure(sizeof(WaveDesc) * wds.size()));
         if (int ru_ = upload(D.wdesc.p, wds.data(), sizeof(WaveDesc) * wds.size())) return ru_;
         rc = ensure_wave_buffers(max_scratch);
         if (rc) return rc;
+        hmark("chunks uploaded");
         WavesArgs W{};
         W.sc = sa;
         W.sc.tiles = D.tdesc.as<TileDesc>();

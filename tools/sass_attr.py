@@ -23,7 +23,7 @@ for r in rows:
     op = ins.split()[0] if not ins.startswith('@') else ins.split()[1]
     if want and not op.startswith(want): continue
     agg[loc] += ex; aggop[loc][op.split('.')[0]] += ex
-P = 2.147455258e9
+P = float(__import__("os").environ.get("PAIRS", "2.147455258e9"))
 for loc, v in agg.most_common(int(sys.argv[5]) if len(sys.argv) > 5 else 30):
     top = ', '.join(f"{o} {c/P:.3f}" for o, c in aggop[loc].most_common(4))
     print(f"{v/P:6.3f} {loc}  [{top}]")
