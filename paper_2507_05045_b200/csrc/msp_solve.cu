@@ -1746,16 +1746,37 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   if (rc) return rc;
   mark("joins queued");
 
-  // ---- overflowed partitioned batches are re-joined with the global table
+  // ---- overflowed partitioned batches are re-joined with the global table.  The per-batch totals
+  //      are read back in the same round trip: without global-table batches they are final.
   unsigned long long n_v2_hits = 0;
+  std::vector<unsigned long long> bf(P.G), bh(P.G), zk(2 * (size_t)P.G);
+  unsigned long long nh = 0;
+  int err = 0;
+  bool totals_read = false;
+  auto read_totals = [&]() -> int {
+    CK(cudaEventRecord(D.ev[2], st));
+    if (P.G) {
+      CK(cudaMemcpyAsync(bf.data(), D.bfilt.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(bh.data(), D.bhits.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(zk.data(), D.zkeys.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
+    return MSP_OK;
+  };
   if (!stopped && (!part_b.empty() || !huge_b.empty())) {
     std::vector<uint32_t> ovf(P.G);
     CK(cudaMemcpyAsync(ovf.data(), D.bovf.p, 4 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&n_v2_hits, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+    if (global_b.empty()) {
+      if (int r_ = read_totals()) return r_;
+      totals_read = true;
+    }
     CK(cudaStreamSynchronize(st));
     if (stop_state()) stopped = true;  // the kernels stopped early: nothing left to re-join
     for (uint32_t g = 0; g < P.G && !stopped; ++g) {
       if (!ovf[g]) continue;
+      totals_read = false;  // the re-joined batches change them
       dropped[g] = 1;
       global_b.push_back(g);
       CK(cudaMemsetAsync(D.bfilt.as<unsigned long long>() + g, 0, 8, st));
@@ -1882,18 +1903,10 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   }
 
   // ---- totals
-  CK(cudaEventRecord(D.ev[2], st));
-  std::vector<unsigned long long> bf(P.G), bh(P.G), zk(2 * (size_t)P.G);
-  unsigned long long nh = 0;
-  int err = 0;
-  if (P.G) {
-    CK(cudaMemcpyAsync(bf.data(), D.bfilt.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(bh.data(), D.bhits.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(zk.data(), D.zkeys.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+  if (!totals_read || stopped) {
+    if (int r_ = read_totals()) return r_;
+    CK(cudaStreamSynchronize(st));
   }
-  CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
   S.t_validate = now_s() - t_join0;
   S.dev_ms_tables = elapsed_ms(D.ev[0], D.ev[1]);
   S.dev_ms_join = elapsed_ms(D.ev[1], D.ev[2]);

@@ -37,15 +37,18 @@ HIT_ALPHAS = [1499, 638, 665, 1343, 1309, 739, 1281, 1261, 799, 1226, 1220, 823,
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--alphas", default="", help="comma-separated subset, in the order given (default: all)")
+    ap.add_argument("--out", default="", help="output path (default: alpha_groups_9_100_1_hits_all.json)")
     args = ap.parse_args()
     done = {g["alpha"] for g in json.load(open(os.path.join(HERE, "alpha_groups_9_100_1_hits.json")))["groups"]}
     inst = generate_instance(9, 100, 1)
-    path = os.path.join(HERE, "alpha_groups_9_100_1_hits_all.json")
+    path = args.out or os.path.join(HERE, "alpha_groups_9_100_1_hits_all.json")
+    todo = [int(x) for x in args.alphas.split(",") if x] or HIT_ALPHAS
     out = {"source": "oracle.AlphaGroups.run(method=1) (filter join, oracle/msp_oracle_groups.cc), pinned to the "
                      "reference; instance generate_instance(9, 100, 1)",
            "hit_alphas": HIT_ALPHAS, "groups": []}
     with O.AlphaGroups(inst.a, inst.d) as G:
-        for alpha in HIT_ALPHAS:
+        for alpha in todo:
             if alpha in done:
                 continue
             t0 = time.time()
