@@ -217,6 +217,20 @@ def stream(a, d):
     return out
 
 
+def stream_headers(a, d):
+    """Batch headers (alpha, beta, n_left, n_right) of the reference stream, without the pairs."""
+    a = _u64(a)
+    d = _u64(d)
+    m, n = a.shape
+    maxb = 1 << 20
+    hdr = np.zeros((maxb, 4), np.int64)
+    nb = lib().oracle_stream(m, n, _ptr(a), _ptr(d), maxb, _ptr(hdr, C.c_int64), 0, None)
+    nb = nb if nb >= 0 else -nb - 1  # (max_pairs 0: the count comes back encoded as -nb - 1)
+    if nb > maxb:
+        raise ValueError("too many batches for stream_headers")
+    return [tuple(int(v) for v in row) for row in hdr[:nb].tolist()]
+
+
 def _group_dict(res: GroupResult, n: int) -> dict:
     ns = res.n_solutions
     xb = np.ctypeslib.as_array(res.xbits, shape=(ns * n,)).reshape(ns, n).copy() if ns else np.zeros((0, n), np.uint8)

@@ -155,6 +155,8 @@ struct TileGenArgs {
   const uint32_t *gs_unit;             // by (batch, side): unit within its scatter launch, or
                                        // 0xFFFFFFFF to skip the rectangle (nullptr: unit 0)
   TileDesc *out;
+  uint64_t tiles;                      // total tiles written (picks the kernel: few rectangles with
+                                       // many tiles each take a warp per rectangle)
 };
 void launch_tiles(const TileGenArgs &a, cudaStream_t st);
 

@@ -292,9 +292,37 @@ __global__ void k_tiles(const TileGenArgs a) {
   }
 }
 
+// One warp per rectangle, lanes over its nl x nq warp tiles: for the few large rectangles of a huge
+// batch side (~1000 tiles each), where 32 rectangles per warp would leave too few warps.
+__global__ void k_tiles_wide(const TileGenArgs a) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t wpg = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t r = a.rect_lo + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < a.rect_hi; r += wpg) {
+    const RectDesc R = a.rects[r];
+    const uint32_t gs = R.gs();
+    const uint32_t unit = a.gs_unit ? a.gs_unit[gs] : 0u;
+    if (unit == 0xFFFFFFFFu) continue;
+    TileDesc *out = a.out + (a.gs_tile_base ? a.gs_tile_base[gs] : 0ull) + R.tile_off;
+    const uint32_t w2 = unit | ((R.lane_is_x() ? 1u : 0u) << 18);
+    const uint32_t nt = R.nl * R.nq;
+    for (uint32_t t = lane; t < nt; t += 32) {
+      const uint32_t lc = t / R.nq, qc = t - lc * R.nq;
+      const uint32_t ln = min(32u, R.L - lc * 32);
+      const uint32_t qn = min((uint32_t)kTQ, R.Q - qc * kTQ);
+      const uint4 v = make_uint4(R.lane_start + lc * 32, R.loop_start + qc * kTQ, w2 | ((ln - 1) << 8) | ((qn - 1) << 13), 0u);
+      *reinterpret_cast<uint4 *>(out + t) = v;
+    }
+  }
+}
+
 void launch_tiles(const TileGenArgs &a, cudaStream_t st) {
   const uint32_t n = a.rect_hi - a.rect_lo;
   if (!n) return;
+  if (a.tiles > 8ull * n) {  // large rectangles: a warp each
+    const uint32_t blocks = (n + 7) / 8;
+    k_tiles_wide<<<blocks < 2368 ? blocks : 2368, 256, 0, st>>>(a);
+    return;
+  }
   const uint32_t blocks = (n + 255) / 256;  // 8 warps per block, 32 rectangles per warp
   k_tiles<<<blocks < 2368 ? blocks : 2368, 256, 0, st>>>(a);
 }

@@ -1347,6 +1347,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
       tg.gs_tile_base = D.gstb.as<uint64_t>();
       tg.gs_unit = D.gsu.as<uint32_t>();
       tg.out = D.tdesc.as<TileDesc>();
+      tg.tiles = all_tiles;
       mark("tiles launch");
       launch_tiles(tg, st);
       ++S.kernel_launches;
@@ -1578,6 +1579,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
         tg.rect_lo = P.rect_base[gs];
         tg.rect_hi = P.rect_base[gs] + P.nrect[gs];
         tg.out = D.tdesc.as<TileDesc>();
+        tg.tiles = P.tiles[gs];
         launch_tiles(tg, st);
         c1.scratch = D.cscratch[role].as<unsigned long long>();
         c1.start[0] = cbkd + role * NC;
