@@ -42,7 +42,7 @@ WORKLOADS = {  # name -> (m, K, seed)
 }
 METRIC = "candidate pairs verified/sec (full enumeration, all solutions)"
 # ncu --set full capture of the current k_waves (update with the kernel; profiles/README.md)
-TRAFFIC_CAPTURE = "r2g_kernels.json"
+TRAFFIC_CAPTURE = "r2v_kernels.json"
 UNIT = "pairs/s"
 
 

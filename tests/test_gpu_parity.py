@@ -366,6 +366,16 @@ def test_full_9_80_hits_match_oracle_groups():
         assert sum(grp["hash_hits"] for grp in groups.values()) == 99
         sols = sorted(s for grp in groups.values() for s in grp["solutions"])
         assert sorted("".join(map(str, r)) for r in xb.tolist()) == sols
+    # the heap-free plan against the reference stream's 1911 batch headers (heap enumeration restated)
+    stream = load_golden("stream_9_100_1.json")["headers"]
+    assert [b[:3] for b in st["batch_stats"]] == [(h[0], h[2], h[3]) for h in stream]
+    # every other batch's counters against the oracle's filter join (tests/golden/make_golden_batches_9_80.py)
+    gb = load_golden("batches_9_100_1.json")
+    by_alpha = {b[0]: b for b in st["batch_stats"]}
+    for alpha, nl, nr, filt, hh, eh in gb["records"]:
+        assert by_alpha[alpha] == (alpha, nl, nr, filt, hh), alpha
+        assert hh == 0 and eh == 0
+    assert len(gb["records"]) + len(groups) == len(stream) or not gb["complete"]
 
 
 @pytest.mark.slow
