@@ -7,9 +7,9 @@ exact_hits, peak_*), plus the row-1 candidate pair count.
 
 from __future__ import annotations
 
-import numpy as np
 import os
 
+import numpy as np
 import pytest
 
 from conftest import STAT_KEYS, inst_from, load_golden, seeded_instance
