@@ -106,12 +106,28 @@ struct Device {
   // waits for the stream to drain first, which would idle the GPU between launches
   unsigned char *ring = nullptr;
   size_t ring_cap = 0, ring_off = 0;
+  // pinned landing area of the end-of-join readback (per-batch counters, flags): pageable
+  // destinations make each copy a staged, synchronous transfer
+  unsigned char *pin = nullptr;
+  size_t pin_cap = 0;
+  unsigned char *pinned(size_t bytes) {
+    if (bytes <= pin_cap) return pin;
+    if (pin) cudaFreeHost(pin);
+    pin = nullptr;
+    pin_cap = 0;
+    if (cudaMallocHost(&pin, bytes) != cudaSuccess) { pin = nullptr; return nullptr; }
+    pin_cap = bytes;
+    return pin;
+  }
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t pev[2] = {nullptr, nullptr};
   void release_all() {
     if (ring) cudaFreeHost(ring);
     ring = nullptr;
     ring_cap = ring_off = 0;
+    if (pin) cudaFreeHost(pin);
+    pin = nullptr;
+    pin_cap = 0;
     DBuf *all[] = {&a, &d, &yn, &hl, &hr, &galpha, &gnl, &gnr, &gcount, &rects, &nrect, &rbase, &tiles, &err,
                    &units, &ufilt, &uhits, &keys, &cnt, &zero, &zhit, &hits, &nhits, &recs,
                    &nrecs, &bout, &bcnt, &rkeys, &runits, &rfilt, &rhits,
@@ -1755,26 +1771,45 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   unsigned long long nh = 0;
   int err = 0;
   bool totals_read = false;
+  // pinned layout: bf | bh | zk (2G) | ovf (G x 4 B) | nh | n_v2_hits | err
+  const size_t G8 = 8 * (size_t)P.G;
+  unsigned char *pin = D.pinned(4 * G8 + 4 * (size_t)P.G + 32);
+  if (!pin) { set_err("cudaMallocHost failed"); return MSP_CUDA_ERROR; }
+  unsigned long long *p_nh = reinterpret_cast<unsigned long long *>(pin + 4 * G8 + ((4 * (size_t)P.G + 7) & ~(size_t)7));
+  unsigned long long *p_nv2 = p_nh + 1;
+  int *p_err = reinterpret_cast<int *>(p_nh + 2);
   auto read_totals = [&]() -> int {
     CK(cudaEventRecord(D.ev[2], st));
     if (P.G) {
-      CK(cudaMemcpyAsync(bf.data(), D.bfilt.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(bh.data(), D.bhits.p, 8 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(zk.data(), D.zkeys.p, 16 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(pin, D.bfilt.p, G8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(pin + G8, D.bhits.p, G8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(pin + 2 * G8, D.zkeys.p, 2 * G8, cudaMemcpyDeviceToHost, st));
     }
-    CK(cudaMemcpyAsync(&nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(p_nh, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(p_err, D.err.p, 4, cudaMemcpyDeviceToHost, st));
     return MSP_OK;
+  };
+  auto take_totals = [&]() {  // after the stream synchronised
+    if (P.G) {
+      memcpy(bf.data(), pin, G8);
+      memcpy(bh.data(), pin + G8, G8);
+      memcpy(zk.data(), pin + 2 * G8, 2 * G8);
+    }
+    nh = *p_nh;
+    err = *p_err;
   };
   if (!stopped && (!part_b.empty() || !huge_b.empty())) {
     std::vector<uint32_t> ovf(P.G);
-    CK(cudaMemcpyAsync(ovf.data(), D.bovf.p, 4 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&n_v2_hits, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
+    if (P.G) CK(cudaMemcpyAsync(pin + 4 * G8, D.bovf.p, 4 * (size_t)P.G, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(p_nv2, D.nhits.p, 8, cudaMemcpyDeviceToHost, st));
     if (global_b.empty()) {
       if (int r_ = read_totals()) return r_;
       totals_read = true;
     }
     CK(cudaStreamSynchronize(st));
+    if (P.G) memcpy(ovf.data(), pin + 4 * G8, 4 * (size_t)P.G);
+    n_v2_hits = *p_nv2;
+    if (totals_read) take_totals();
     if (stop_state()) stopped = true;  // the kernels stopped early: nothing left to re-join
     for (uint32_t g = 0; g < P.G && !stopped; ++g) {
       if (!ovf[g]) continue;
@@ -1908,6 +1943,7 @@ int solve_impl(const msp_problem *pr, const msp_options *opt, msp_result *res) {
   if (!totals_read || stopped) {
     if (int r_ = read_totals()) return r_;
     CK(cudaStreamSynchronize(st));
+    take_totals();
   }
   S.t_validate = now_s() - t_join0;
   S.dev_ms_tables = elapsed_ms(D.ev[0], D.ev[1]);
