@@ -30,12 +30,15 @@ def main():
     ap.add_argument("--deadline", type=float, default=0.0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--descending", action="store_true", help="largest batches first (a second worker)")
+    ap.add_argument("--skip-done", default="", help="a previous output: its batches are skipped")
     args = ap.parse_args()
     t_start = time.time()
     inst = generate_instance(9, 100, 1)
     hdrs = [tuple(h) for h in json.load(open(os.path.join(HERE, "stream_9_100_1.json")))["headers"]]
     pinned = {g["alpha"] for f in ("alpha_groups_9_100_1_hits.json", "alpha_groups_9_100_1_hits_all.json")
               for g in json.load(open(os.path.join(HERE, f)))["groups"]}
+    if args.skip_done:
+        pinned |= {r[0] for r in json.load(open(args.skip_done))["records"]}
     todo = sorted((h for h in hdrs if h[0] not in pinned), key=lambda h: h[2] + h[3], reverse=args.descending)
     out = {"source": "oracle.stream_headers (reference batch stream) + oracle.AlphaGroups.run(method=1) per batch; "
                      "instance generate_instance(9, 100, 1); the 92 hit-bearing batches are in "

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-T=r2w
+T=${TAG:-r2w}
 timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${T}_pytest.log
 timeout 600 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-headline > /dev/null 2>&1 && \
